@@ -1,0 +1,184 @@
+/*
+ * streamconv_b200.h — C-ABI of the B200-native multi-stream cached-padding engine.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2204.07064 as specified by the
+ * reference (`/root/reference/SPEC.md`, module `stream_runtime`) and implemented, for its
+ * arithmetic core, by `proj/src/kernels.cpp`.  The reference is an in-process C++ API in
+ * `namespace streamconv` with no C ABI; every entry point below names the
+ * reference function it replaces.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - Every function returns an `int` status: SC_OK (0) or 1 + the ordinal of the reference
+ *     `streamconv::ErrCode` (proj/include/streamconv/error.hpp:8-29), or SC_ERR_CUDA_BASE +
+ *     cudaError_t.  `sc_last_error()` returns the message of the last failure on the calling
+ *     thread, formatted like `streamconv::Error::what()` ("<ErrCode>: <msg>", error.hpp:59-60).
+ *   - Signals at the boundary use the reference layout (SignalTensor, tensor.hpp:14-48):
+ *     fp32, channel-major `[channels][length]` per stream; a batch of streams is
+ *     `[stream][channels][length]` contiguous.  Device pointers unless stated otherwise.
+ *   - Conv weights use the reference `Kernel` layout (tensor.hpp:52-88): weights `[n][m][k]`
+ *     followed by bias `[n]`, fp32, in ONE host array addressed by `sc_node.weight_offset`.
+ *   - `stream` arguments are `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ */
+#ifndef STREAMCONV_B200_H
+#define STREAMCONV_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SC_API __attribute__((visibility("default")))
+#else
+#define SC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1 + streamconv::ErrCode ordinal (error.hpp:8-29) ------------------- */
+enum sc_status {
+  SC_OK = 0,
+  SC_ERR_INVALID_ARGUMENT = 1,            /* ErrCode::InvalidArgument */
+  SC_ERR_INPUT_TOO_SHORT = 2,             /* ErrCode::InputTooShort */
+  SC_ERR_CHANNEL_MISMATCH = 3,            /* ErrCode::ChannelMismatch */
+  SC_ERR_CYCLE_DETECTED = 4,              /* ErrCode::CycleDetected */
+  SC_ERR_DANGLING_NODE = 5,               /* ErrCode::DanglingNode */
+  SC_ERR_RATE_MISMATCH_AT_SUM = 6,        /* ErrCode::RateMismatchAtSum */
+  SC_ERR_MALFORMED_GRAPH = 7,             /* ErrCode::MalformedGraph */
+  SC_ERR_NOT_CAUSAL = 8,                  /* ErrCode::NotCausal */
+  SC_ERR_PADDING_NOT_STREAMABLE = 9,      /* ErrCode::PaddingNotStreamable */
+  SC_ERR_INTERNAL_NON_INTEGER_DELAY = 10, /* ErrCode::InternalNonIntegerDelay */
+  SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO = 11, /* ErrCode::BufferNotMultipleOfRatio */
+  SC_ERR_LENGTH_NOT_MULTIPLE_OF_RATIO = 12, /* ErrCode::LengthNotMultipleOfRatio */
+  SC_ERR_CHUNK_TOO_SMALL = 13,            /* ErrCode::ChunkTooSmall */
+  SC_ERR_LENGTH_MISMATCH = 14,            /* ErrCode::LengthMismatch */
+  SC_ERR_ZERO_ENERGY = 15,                /* ErrCode::ZeroEnergy */
+  SC_ERR_VERSION_MISMATCH = 16,           /* ErrCode::VersionMismatch */
+  SC_ERR_CORRUPT_BLOB = 17,               /* ErrCode::CorruptBlob */
+  SC_ERR_SCHEMA_ERROR = 18,               /* ErrCode::SchemaError */
+  SC_ERR_UNSUPPORTED_FORMAT = 19,         /* ErrCode::UnsupportedFormat */
+  SC_ERR_MALFORMED_HEADER = 20,           /* ErrCode::MalformedHeader */
+  SC_ERR_CUDA_BASE = 1000                 /* 1000 + cudaError_t */
+};
+
+/* ---- activation kinds: streamconv::Act (kernels.hpp:9) --------------------------------- */
+enum sc_act { SC_ACT_IDENTITY = 0, SC_ACT_TANH = 1, SC_ACT_LEAKY_RELU = 2 };
+
+/* ---- graph nodes ------------------------------------------------------------------------
+ * A model is a flat, topologically ordered node list: a sequential stack with nested
+ * residual scopes.  This is the subset of SPEC graph_ir that the
+ * north-star models need: Conv / ZeroUpsample+Conv (ConvTranspose1d) /
+ * Activation / Fanout+Sum with an identity skip / channel gate / slice.
+ * Paddings are the ORIGINAL (possibly non-causal) ones; plan creation runs the causalize
+ * rewrite and inserts the Eq. (2) and branch-alignment delays itself.  */
+enum sc_node_kind {
+  SC_NODE_CONV = 0,      /* conv1d(pad(x,(L,R)), k, stride, dilation)        kernels.cpp:73  */
+  SC_NODE_CONVT = 1,     /* conv1d(pad(zero_upsample(x,stride),(L,R)), k)   kernels.cpp:106 */
+  SC_NODE_ACT = 2,       /* activation(x, act, alpha)                        kernels.cpp:119 */
+  SC_NODE_RES_BEGIN = 3, /* Fanout: start of a residual branch; skip = identity           */
+  SC_NODE_RES_END = 4,   /* Sum(branch, Delay_A(skip)) with A from branch_alignment        */
+  SC_NODE_GATE = 5,      /* y[c] = tanh(x[c]) * sigmoid(x[c + C/2]), C -> C/2  (RAVE head) */
+  SC_NODE_SLICE = 6      /* keep channels [slice_begin, slice_begin + slice_count)         */
+};
+
+typedef struct sc_node {
+  int32_t kind;          /* enum sc_node_kind */
+  int32_t in_channels;   /* CONV/CONVT: M */
+  int32_t out_channels;  /* CONV/CONVT: N */
+  int32_t taps;          /* CONV/CONVT: K */
+  int32_t stride;        /* CONV: S;  CONVT: upsampling factor */
+  int32_t dilation;      /* CONV: d (CONVT: must be 1) */
+  int64_t pad_left;      /* original PaddingSpec{left,right} (tensor.hpp:90-95) */
+  int64_t pad_right;
+  int32_t act;           /* ACT: enum sc_act */
+  float alpha;           /* ACT: leaky_relu slope (reference default 0.01f, kernels.hpp:32) */
+  int64_t weight_offset; /* CONV/CONVT: float offset of weights[N][M][K] then bias[N] */
+  int32_t slice_begin;   /* SLICE */
+  int32_t slice_count;   /* SLICE */
+} sc_node;
+
+/* arithmetic variants of the dense path */
+enum sc_precision {
+  SC_PREC_FP32 = 0,      /* fp32-accurate: FFMA or 3xTF32 tensor-core, fp32 accumulate */
+  SC_PREC_BF16 = 1       /* bf16 operands, fp32 accumulate (separately stated bound)     */
+};
+
+typedef struct sc_plan sc_plan;
+typedef struct sc_state sc_state;
+
+/* ---- library / errors ------------------------------------------------------------------ */
+SC_API const char* sc_last_error(void);
+SC_API const char* sc_version(void);
+SC_API const char* sc_status_name(int status); /* streamconv::to_string(ErrCode) (error.hpp:31-55) */
+
+/* ---- causalize arithmetic -------------------------------------------- */
+/* Eq. (2): D_a = (S - ((R + D_c) mod S)) mod S */
+SC_API int64_t sc_delay_for_stride(int64_t stride, int64_t right_pad, int64_t cumulated_delay);
+/* A_i = max_j D_j - D_i */
+SC_API int sc_branch_alignment(const int64_t* delays, int32_t n, int64_t* out);
+
+/* ---- plans: a validated + causalized graph with device-resident weights ---------------- */
+/* Replaces: SPEC causalize(g) + weight upload.  `weights_host` holds every
+ * node's Kernel (tensor.hpp:52-88).  `device` is the CUDA ordinal; device = -1 creates a
+ * host-only plan (validation, causalize, ledger and lowering only; no states, no GPU).     */
+SC_API int sc_plan_create(const sc_node* nodes, int32_t n_nodes, const float* weights_host,
+                   int64_t n_weights, int32_t in_channels, int32_t precision, int32_t device,
+                   sc_plan** out);
+SC_API int sc_plan_destroy(sc_plan* plan);
+/* SPEC compression_ratio: granularity of the buffer length. */
+SC_API int sc_plan_ratio(const sc_plan* plan, int64_t* ratio);
+/* Sink rate ratio: output samples per input sample = num/den. */
+SC_API int sc_plan_sink_rate(const sc_plan* plan, int64_t* num, int64_t* den, int32_t* out_channels);
+/* SPEC latency_of: total input->output latency in input samples. */
+SC_API int sc_plan_latency(const sc_plan* plan, int64_t* samples);
+/* SPEC closed-form state size: sum over causalized Conv caches and Delay
+ * rings of (len x channels x 4) bytes per stream.                                      */
+SC_API int sc_plan_state_bytes(const sc_plan* plan, int64_t* bytes_per_stream);
+/* Algorithmic work per stream per input sample (no zero-stuffed MACs, SPEC.md:405 fixed). */
+SC_API int sc_plan_macs_per_sample(const sc_plan* plan, double* macs);
+/* Human-readable lowering summary (buffers, ops, kernels), valid until plan destroy. */
+SC_API const char* sc_plan_describe(const sc_plan* plan);
+
+/* ---- stream states: SPEC StreamState for a batch of independent streams ----------------- */
+/* Replaces: init_state, one per stream, zeroed.  `max_frames` = largest
+ * per-call buffer length (input samples per stream) this state will be used with.          */
+SC_API int sc_state_create(const sc_plan* plan, int32_t n_streams, int64_t max_frames, sc_state** out);
+SC_API int sc_state_destroy(sc_state* state);
+/* Replaces: reset for the listed streams (NULL ids = all). Async. */
+SC_API int sc_state_reset(sc_state* state, const int32_t* stream_ids, int32_t n_ids, void* stream);
+/* Device bytes actually held by the state (caches + step working buffers). */
+SC_API int sc_state_device_bytes(const sc_state* state, int64_t* bytes);
+/* Resident cache bytes per stream (<= sc_plan_state_bytes: skip delays share conv caches). */
+SC_API int sc_state_cache_bytes(const sc_state* state, int64_t* bytes_per_stream);
+
+/* Replaces: process_buffer for every stream of `state` at once.
+ * d_in  : [n_streams][in_channels][frames]  fp32 device
+ * d_out : [n_streams][out_channels][frames * sink_rate] fp32 device
+ * frames must be a positive multiple of sc_plan_ratio and <= max_frames.  Asynchronous on
+ * `stream`; the steady-state launch sequence is replayed from a cached CUDA graph.        */
+SC_API int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t frames, void* stream);
+/* Number of kernels one sc_process launches (for launch accounting). */
+SC_API int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n);
+/* Enable/disable CUDA-graph replay (default on). */
+SC_API int sc_state_set_graphs(sc_state* state, int32_t enabled);
+
+/* ---- tensor_core ops on device batches (kernels.hpp:16-32) ----------------------------- */
+/* conv1d (kernels.cpp:73-104) over a batch: x [batch][M][L] -> y [batch][N][Lout],
+ * Lout = (L - ((K-1)d+1))/S + 1 (kernels.cpp:46-49).  w/b device, reference layout.      */
+SC_API int sc_conv1d(const float* d_x, int32_t batch, int32_t in_channels, int64_t length,
+              const float* d_w, const float* d_b, int32_t out_channels, int32_t taps,
+              int32_t stride, int32_t dilation, float* d_y, void* stream);
+SC_API int64_t sc_conv_output_length(int64_t in_len, int32_t taps, int32_t stride, int32_t dilation);
+
+/* ---- PQMF filter bank (not in the reference: builder-defined, parity unpinned) ---------- */
+/* Kaiser-windowed lowpass prototype (taps), cosine-modulated into `bands` analysis and
+ * synthesis filters, written in the sc_node conv weight layout:
+ *   analysis : CONV  M=1, N=bands, K=taps, S=bands, pad (taps-bands, 0)  -> [bands][1][taps]
+ *   synthesis: CONVT M=bands, N=1,  K=taps, S=bands, pad (taps-1, 0)     -> [1][bands][taps]
+ * Each array is followed by a zero bias.  Computed in double, rounded once to fp32.      */
+SC_API int sc_pqmf_filters(int32_t bands, int32_t taps, float* analysis, float* synthesis,
+                    double* prototype);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STREAMCONV_B200_H */

@@ -1,0 +1,211 @@
+// capi.cpp — the extern "C" boundary (include/streamconv_b200.h).  No exception crosses it:
+// every entry point maps scb::Error to its sc_status and records the message for
+// sc_last_error(), formatted like streamconv::Error::what() (error.hpp:59-60).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "runtime.hpp"
+
+struct sc_plan {
+  std::unique_ptr<scb::Plan> p;
+};
+struct sc_state {
+  std::unique_ptr<scb::State> s;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+const char* kNames[] = {"InvalidArgument",       "InputTooShort",
+                        "ChannelMismatch",       "CycleDetected",
+                        "DanglingNode",          "RateMismatchAtSum",
+                        "MalformedGraph",        "NotCausal",
+                        "PaddingNotStreamable",  "InternalNonIntegerDelay",
+                        "BufferNotMultipleOfRatio", "LengthNotMultipleOfRatio",
+                        "ChunkTooSmall",         "LengthMismatch",
+                        "ZeroEnergy",            "VersionMismatch",
+                        "CorruptBlob",           "SchemaError",
+                        "UnsupportedFormat",     "MalformedHeader"};
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SC_OK;
+  } catch (const scb::Error& e) {
+    g_err = std::string(sc_status_name(e.code)) + ": " + e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = std::string("InvalidArgument: ") + e.what();
+    return SC_ERR_INVALID_ARGUMENT;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) scb::fail(SC_ERR_INVALID_ARGUMENT, what);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sc_last_error(void) { return g_err.c_str(); }
+const char* sc_version(void) { return "streamconv-b200 0.1 (sm_100a)"; }
+
+const char* sc_status_name(int status) {
+  if (status == SC_OK) return "OK";
+  if (status >= 1 && status <= 20) return kNames[status - 1];
+  if (status >= SC_ERR_CUDA_BASE) return "CudaError";
+  return "UnknownError";
+}
+
+int64_t sc_delay_for_stride(int64_t S, int64_t R, int64_t Dc) {
+  if (S < 1 || R < 0 || Dc < 0) return -1;
+  return (S - ((R + Dc) % S)) % S;  // Eq. (2)
+}
+
+int sc_branch_alignment(const int64_t* D, int32_t n, int64_t* out) {
+  return guard([&] {
+    need(n >= 1 && D && out, "branch_alignment: empty input");
+    int64_t mx = D[0];
+    for (int i = 0; i < n; ++i) {
+      need(D[i] >= 0, "branch_alignment: negative delay");
+      mx = std::max(mx, D[i]);
+    }
+    for (int i = 0; i < n; ++i) out[i] = mx - D[i];
+  });
+}
+
+int sc_plan_create(const sc_node* nodes, int32_t n_nodes, const float* weights_host,
+                   int64_t n_weights, int32_t in_channels, int32_t precision, int32_t device,
+                   sc_plan** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    *out = nullptr;
+    auto p = scb::make_plan(nodes, n_nodes, weights_host, n_weights, in_channels, precision, device);
+    *out = new sc_plan{std::move(p)};
+  });
+}
+
+int sc_plan_destroy(sc_plan* plan) {
+  return guard([&] { delete plan; });
+}
+
+int sc_plan_ratio(const sc_plan* plan, int64_t* ratio) {
+  return guard([&] {
+    need(plan && ratio, "null argument");
+    *ratio = plan->p->prog.ratio;
+  });
+}
+
+int sc_plan_sink_rate(const sc_plan* plan, int64_t* num, int64_t* den, int32_t* out_channels) {
+  return guard([&] {
+    need(plan && num && den && out_channels, "null argument");
+    *num = plan->p->prog.sink_rate.num;
+    *den = plan->p->prog.sink_rate.den;
+    *out_channels = plan->p->prog.sink_C;
+  });
+}
+
+int sc_plan_latency(const sc_plan* plan, int64_t* samples) {
+  return guard([&] {
+    need(plan && samples, "null argument");
+    *samples = plan->p->prog.latency_in;
+  });
+}
+
+int sc_plan_state_bytes(const sc_plan* plan, int64_t* bytes) {
+  return guard([&] {
+    need(plan && bytes, "null argument");
+    *bytes = plan->p->prog.state_bytes_spec;
+  });
+}
+
+int sc_plan_macs_per_sample(const sc_plan* plan, double* macs) {
+  return guard([&] {
+    need(plan && macs, "null argument");
+    *macs = plan->p->prog.macs_per_sample;
+  });
+}
+
+const char* sc_plan_describe(const sc_plan* plan) { return plan ? plan->p->desc.c_str() : ""; }
+
+int sc_state_create(const sc_plan* plan, int32_t n_streams, int64_t max_frames, sc_state** out) {
+  return guard([&] {
+    need(plan && out, "null argument");
+    *out = nullptr;
+    auto s = scb::make_state(plan->p.get(), n_streams, max_frames);
+    *out = new sc_state{std::move(s)};
+  });
+}
+
+int sc_state_destroy(sc_state* state) {
+  return guard([&] { delete state; });
+}
+
+int sc_state_reset(sc_state* state, const int32_t* ids, int32_t n_ids, void* stream) {
+  return guard([&] {
+    need(state != nullptr, "null state");
+    state->s->reset(ids, n_ids, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sc_state_device_bytes(const sc_state* state, int64_t* bytes) {
+  return guard([&] {
+    need(state && bytes, "null argument");
+    *bytes = state->s->mem_bytes;
+  });
+}
+
+int sc_state_cache_bytes(const sc_state* state, int64_t* bytes) {
+  return guard([&] {
+    need(state && bytes, "null argument");
+    *bytes = state->s->cache_bytes_per_stream;
+  });
+}
+
+int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t frames, void* stream) {
+  return guard([&] {
+    need(state != nullptr, "null state");
+    state->s->process(d_in, d_out, frames, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n) {
+  return guard([&] {
+    need(state && n, "null argument");
+    *n = state->s->launches(frames);
+  });
+}
+
+int sc_state_set_graphs(sc_state* state, int32_t enabled) {
+  return guard([&] {
+    need(state != nullptr, "null state");
+    state->s->use_graphs = enabled != 0;
+  });
+}
+
+int sc_conv1d(const float* d_x, int32_t batch, int32_t in_channels, int64_t length, const float* d_w,
+              const float* d_b, int32_t out_channels, int32_t taps, int32_t stride, int32_t dilation,
+              float* d_y, void* stream) {
+  return guard([&] {
+    scb::conv1d_batched(d_x, batch, in_channels, length, d_w, d_b, out_channels, taps, stride,
+                        dilation, d_y, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int64_t sc_conv_output_length(int64_t L, int32_t K, int32_t S, int32_t d) {
+  // kernels.cpp:46-49
+  const int64_t span = static_cast<int64_t>(K - 1) * d + 1;
+  return (L - span) / S + 1;
+}
+
+int sc_pqmf_filters(int32_t bands, int32_t taps, float* analysis, float* synthesis, double* proto) {
+  return guard([&] { scb::pqmf_filters(bands, taps, analysis, synthesis, proto); });
+}
+
+}  // extern "C"

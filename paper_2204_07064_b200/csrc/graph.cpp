@@ -1,0 +1,333 @@
+// graph.cpp — validate + causalize a node list and lower it to frame buffers and fused ops.
+//
+// Follows SPEC causalize: every Conv pad (L,R) becomes (L+R,0); before a
+// stride-S conv an Eq. (2) delay D_a = (S - ((R + D_c) mod S)) mod S is inserted
+// (SPEC.md:191-194); at a Sum the lower-delay branch gets A_i = max_j D_j - D_i
+// (SPEC.md:200-204); the ledger maps conv D -> (D + R + D_a)/S, ZeroUpsample D -> D*s
+// (SPEC.md:212).  Unlike the reference's node-per-op runtime, inserted
+// Delays are not materialised: an Eq. (2) delay widens the conv's cache, and a skip Delay
+// becomes a row offset into the residual input's own cache (no ring, no copy).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+
+#include "program.hpp"
+
+namespace scb {
+
+namespace {
+
+int64_t delay_for_stride(int64_t S, int64_t R, int64_t Dc) { return (S - ((R + Dc) % S)) % S; }
+
+struct Value {
+  int buf = 0;
+  int off = 0;
+  int C = 1;
+  int act = ACT_ID;
+  float alpha = 0.f;
+  int producer = -1;  // op index that wrote it and may still take a fused epilogue
+  Rate rate;
+  int64_t D = 0;      // cumulated delay D_c, native rate
+};
+
+struct Lowerer {
+  const sc_node* nodes;
+  int n;
+  const float* W;
+  int64_t nW;
+  Program* p;
+  int pos = 0;
+  int64_t ratio = 1;
+
+  static int64_t lcm(int64_t a, int64_t b) { return a / Rate::gcd(a, b) * b; }
+
+  void need_cache(int buf, int64_t frames) {
+    BufferSpec& b = p->bufs[buf];
+    b.cache = std::max(b.cache, frames);
+  }
+
+  int new_buffer(int C, Rate rate, const std::string& name) {
+    BufferSpec b;
+    b.C = C;
+    b.rate = rate;
+    b.name = name;
+    p->bufs.push_back(b);
+    return static_cast<int>(p->bufs.size()) - 1;
+  }
+
+  void conv_node(const sc_node& nd, Value& v) {
+    const bool convt = nd.kind == SC_NODE_CONVT;
+    if (nd.in_channels < 1 || nd.out_channels < 1 || nd.taps < 1 || nd.stride < 1 ||
+        nd.dilation < 1 || nd.pad_left < 0 || nd.pad_right < 0)
+      fail(SC_ERR_INVALID_ARGUMENT, "conv node " + std::to_string(pos - 1) + ": bad shape");
+    if (nd.in_channels != v.C)
+      fail(SC_ERR_CHANNEL_MISMATCH, "conv node " + std::to_string(pos - 1) + " expects " +
+                                        std::to_string(nd.in_channels) + " channels, got " +
+                                        std::to_string(v.C));
+    const int64_t M = nd.in_channels, N = nd.out_channels, K = nd.taps;
+    const int64_t need = N * M * K + N;
+    if (nd.weight_offset < 0 || nd.weight_offset + need > nW)
+      fail(SC_ERR_INVALID_ARGUMENT, "conv node " + std::to_string(pos - 1) + ": weights out of range");
+    const float* w = W + nd.weight_offset;
+    const float* b = w + N * M * K;
+    const int64_t L = nd.pad_left, R = nd.pad_right, Ptot = L + R;
+    const int64_t span = (K - 1) * nd.dilation + 1;
+
+    ConvOp op;
+    op.convt = convt;
+    op.in_buf = v.buf;
+    op.in_off = v.off;
+    op.cin = nd.in_channels;
+    op.pre_act = v.act;
+    op.pre_alpha = v.alpha;
+    op.cout = nd.out_channels;
+    op.K = nd.taps;
+    op.in_rate = v.rate;
+    Rate out_rate = v.rate;
+    char nm[96];
+
+    if (convt) {
+      // ConvTranspose1d = zero_upsample(r) + conv1d(stride 1), lowered to
+      // its polyphase form: y[r*i+phi] = b + sum_j w[k0(phi)+j*r] . x[i + j - e(phi)]
+      const int r = nd.stride;
+      if (nd.dilation != 1) fail(SC_ERR_INVALID_ARGUMENT, "convT dilation must be 1");
+      if (Ptot != K - 1) fail(SC_ERR_PADDING_NOT_STREAMABLE, "convT pad must total K-1");
+      const int64_t emax = (K - 1) / r;
+      op.r = r;
+      op.S = 1;
+      op.d = 1;
+      op.look = emax;
+      op.taps = static_cast<int>(emax + 1);
+      op.row_step = 1;
+      op.tap_step = 1;
+      op.nout = static_cast<int>(r * N);
+      op.w.assign(static_cast<size_t>(op.taps) * M * op.nout, 0.0f);
+      op.bias.resize(op.nout);
+      for (int phi = 0; phi < r; ++phi) {
+        const int64_t k0 = ((K - 1 - phi) % r + r) % r;
+        const int64_t e = (K - 1 - phi - k0) / r;
+        for (int q = 0; q < op.taps; ++q) {
+          const int64_t k = k0 + (q + e - emax) * r;  // tap of the original kernel
+          if (k < 0 || k >= K) continue;
+          for (int64_t c = 0; c < M; ++c)
+            for (int64_t nn = 0; nn < N; ++nn)
+              op.w[(static_cast<size_t>(q) * M + c) * op.nout + phi * N + nn] =
+                  w[(nn * M + c) * K + k];
+        }
+        for (int64_t nn = 0; nn < N; ++nn) op.bias[phi * N + nn] = b[nn];
+      }
+      need_cache(v.buf, emax);
+      p->state_bytes_spec += M * Ptot * 4;   // SPEC: cache of the zero-stuffed signal
+      v.D = v.D * r + R;                     // ledger: ZeroUpsample D*s, then conv + R
+      out_rate.num *= r;
+      out_rate.norm();
+      // per input frame: r output frames x N x (K/r live taps) x M — no zero-stuffed MACs
+      op.macs_per_sample = static_cast<double>(M) * N * K;
+      std::snprintf(nm, sizeof nm, "convT%d %d->%d K%d", r, (int)M, (int)N, (int)K);
+    } else {
+      const int S = nd.stride;
+      int64_t Da = 0;
+      if (S == 1) {
+        if (Ptot != span - 1)
+          fail(SC_ERR_PADDING_NOT_STREAMABLE, "conv node " + std::to_string(pos - 1) +
+                                                  ": pad must total (K-1)*d");
+        v.D += R;
+      } else {
+        if (Ptot < span - S)
+          fail(SC_ERR_PADDING_NOT_STREAMABLE, "strided conv: pad must be >= span - stride");
+        Da = delay_for_stride(S, R, v.D);
+        if ((v.D + R + Da) % S != 0) fail(SC_ERR_INTERNAL_NON_INTEGER_DELAY, "ledger division");
+        v.D = (v.D + R + Da) / S;
+        out_rate.den *= S;
+        out_rate.norm();
+        p->state_bytes_spec += M * Da * 4;  // inserted Delay(D_a) ring
+      }
+      p->state_bytes_spec += M * Ptot * 4;
+      op.S = S;
+      op.d = nd.dilation;
+      op.look = Ptot + Da;
+      op.taps = nd.taps;
+      op.row_step = S;
+      op.tap_step = nd.dilation;
+      op.nout = nd.out_channels;
+      op.w.assign(static_cast<size_t>(K) * M * N, 0.0f);
+      for (int64_t k = 0; k < K; ++k)
+        for (int64_t c = 0; c < M; ++c)
+          for (int64_t nn = 0; nn < N; ++nn)
+            op.w[(k * M + c) * N + nn] = w[(nn * M + c) * K + k];
+      op.bias.assign(b, b + N);
+      need_cache(v.buf, op.look);
+      op.macs_per_sample = static_cast<double>(M) * N * K / S;  // per input frame
+      std::snprintf(nm, sizeof nm, "conv%s %d->%d K%d d%d", S > 1 ? ("/" + std::to_string(S)).c_str() : "",
+                    (int)M, (int)N, (int)K, nd.dilation);
+    }
+    op.name = nm;
+    // scale per-input-frame MACs to per-input-SAMPLE of the model
+    op.macs_per_sample *= static_cast<double>(v.rate.num) / static_cast<double>(v.rate.den);
+    op.out_rstride = op.nout;
+    ratio = lcm(ratio, out_rate.den);
+    op.out_buf = new_buffer(nd.out_channels, out_rate, op.name);
+    p->ops.push_back(std::move(op));
+    v.buf = p->ops.back().out_buf;
+    v.off = 0;
+    v.C = nd.out_channels;
+    v.act = ACT_ID;
+    v.alpha = 0.f;
+    v.producer = static_cast<int>(p->ops.size()) - 1;
+    v.rate = out_rate;
+  }
+
+  void parse(Value& v, int depth) {
+    while (pos < n) {
+      const sc_node& nd = nodes[pos];
+      if (nd.kind == SC_NODE_RES_END) {
+        if (depth == 0) fail(SC_ERR_MALFORMED_GRAPH, "RES_END without RES_BEGIN at node " + std::to_string(pos));
+        return;
+      }
+      ++pos;
+      switch (nd.kind) {
+        case SC_NODE_CONV:
+        case SC_NODE_CONVT:
+          conv_node(nd, v);
+          break;
+        case SC_NODE_ACT: {
+          if (nd.act < 0 || nd.act > 2) fail(SC_ERR_INVALID_ARGUMENT, "activation kind");
+          if (nd.act == ACT_ID) break;
+          if (v.producer >= 0 && p->ops[v.producer].post_act == ACT_ID &&
+              !p->ops[v.producer].gate && p->ops[v.producer].res_buf < 0 &&
+              p->ops[v.producer].out_buf == v.buf) {
+            // fused epilogue activation of the producing conv
+            p->ops[v.producer].post_act = nd.act;
+            p->ops[v.producer].post_alpha = nd.alpha;
+          } else if (v.act == ACT_ID) {
+            v.act = nd.act;  // pending: applied by the consumer on load (prologue)
+            v.alpha = nd.alpha;
+          } else {
+            fail(SC_ERR_UNSUPPORTED_FORMAT, "two unfused activations in a row");
+          }
+          break;
+        }
+        case SC_NODE_GATE: {
+          if (v.C % 2) fail(SC_ERR_CHANNEL_MISMATCH, "gate needs an even channel count");
+          if (v.producer < 0 || p->ops[v.producer].post_act != ACT_ID ||
+              p->ops[v.producer].res_buf >= 0 || p->ops[v.producer].gate || v.off != 0 ||
+              p->ops[v.producer].convt)
+            fail(SC_ERR_UNSUPPORTED_FORMAT, "gate must directly follow a stride-1 conv");
+          ConvOp& op = p->ops[v.producer];
+          // interleave columns: new col 2j = wave j, 2j+1 = amp j
+          const int H = op.nout / 2;
+          std::vector<float> w2(op.w.size()), b2(op.nout);
+          const size_t rows = op.w.size() / op.nout;
+          for (size_t rr = 0; rr < rows; ++rr)
+            for (int j = 0; j < H; ++j) {
+              w2[rr * op.nout + 2 * j] = op.w[rr * op.nout + j];
+              w2[rr * op.nout + 2 * j + 1] = op.w[rr * op.nout + H + j];
+            }
+          for (int j = 0; j < H; ++j) {
+            b2[2 * j] = op.bias[j];
+            b2[2 * j + 1] = op.bias[H + j];
+          }
+          op.w.swap(w2);
+          op.bias.swap(b2);
+          op.gate = true;
+          op.out_rstride = H;
+          p->bufs[op.out_buf].C = H;
+          v.C = H;
+          break;
+        }
+        case SC_NODE_SLICE: {
+          if (nd.slice_begin < 0 || nd.slice_count < 1 || nd.slice_begin + nd.slice_count > v.C)
+            fail(SC_ERR_CHANNEL_MISMATCH, "slice out of range");
+          v.off += nd.slice_begin;
+          v.C = nd.slice_count;
+          break;
+        }
+        case SC_NODE_RES_BEGIN: {
+          Value skip = v;
+          Value br = v;
+          br.producer = -1;  // the branch input is shared with the skip: no fused epilogue
+          parse(br, depth + 1);
+          if (pos >= n || nodes[pos].kind != SC_NODE_RES_END)
+            fail(SC_ERR_MALFORMED_GRAPH, "RES_BEGIN without RES_END");
+          ++pos;
+          if (br.C != skip.C) fail(SC_ERR_CHANNEL_MISMATCH, "residual branch changes channels");
+          if (br.rate != skip.rate) fail(SC_ERR_RATE_MISMATCH_AT_SUM, "residual rates differ");
+          const int64_t Dmax = std::max(br.D, skip.D);  // branch_alignment
+          if (Dmax != br.D) fail(SC_ERR_UNSUPPORTED_FORMAT, "branch-side alignment delay");
+          if (br.producer < 0 || br.act != ACT_ID || br.off != 0 || br.buf != p->ops[br.producer].out_buf)
+            fail(SC_ERR_UNSUPPORTED_FORMAT, "residual branch must end with a conv");
+          ConvOp& op = p->ops[br.producer];
+          if (op.res_buf >= 0 || op.gate) fail(SC_ERR_UNSUPPORTED_FORMAT, "residual epilogue busy");
+          op.res_buf = skip.buf;
+          op.res_off = skip.off;
+          op.res_act = skip.act;
+          op.res_alpha = skip.alpha;
+          op.res_delay = Dmax - skip.D;
+          need_cache(skip.buf, op.res_delay);
+          p->state_bytes_spec += static_cast<int64_t>(skip.C) * op.res_delay * 4;
+          v = br;
+          v.D = Dmax;
+          v.producer = -1;  // y = post(acc) + skip: a following act cannot fuse
+          break;
+        }
+        default:
+          fail(SC_ERR_SCHEMA_ERROR, "unknown node kind " + std::to_string(nd.kind) + " at node " +
+                                        std::to_string(pos - 1));
+      }
+    }
+    if (depth > 0) fail(SC_ERR_MALFORMED_GRAPH, "RES_BEGIN without RES_END");
+  }
+};
+
+}  // namespace
+
+Program lower_graph(const sc_node* nodes, int n_nodes, const float* W, int64_t nW, int in_C) {
+  if (in_C < 1) fail(SC_ERR_INVALID_ARGUMENT, "in_channels must be >= 1");
+  if (n_nodes < 0 || (n_nodes > 0 && !nodes)) fail(SC_ERR_INVALID_ARGUMENT, "node list");
+  Program p;
+  p.in_C = in_C;
+  BufferSpec src;
+  src.C = in_C;
+  src.name = "source";
+  p.bufs.push_back(src);
+  Lowerer lw{nodes, n_nodes, W, nW, &p};
+  Value v;
+  v.C = in_C;
+  lw.parse(v, 0);
+  p.sink_buf = v.buf;
+  p.sink_off = v.off;
+  p.sink_C = v.C;
+  p.sink_act = v.act;
+  p.sink_alpha = v.alpha;
+  p.sink_rate = v.rate;
+  p.ratio = lw.ratio;
+  p.latency_sink = v.D;
+  p.latency_in = v.D * v.rate.den / v.rate.num;
+  for (const ConvOp& op : p.ops) p.macs_per_sample += op.macs_per_sample;
+  return p;
+}
+
+std::string Program::describe() const {
+  std::ostringstream os;
+  os << "buffers:\n";
+  for (size_t i = 0; i < bufs.size(); ++i)
+    os << "  b" << i << " C=" << bufs[i].C << " cache=" << bufs[i].cache << " rate=" << bufs[i].rate.num
+       << "/" << bufs[i].rate.den << " (" << bufs[i].name << ")\n";
+  os << "ops:\n";
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const ConvOp& o = ops[i];
+    os << "  op" << i << " " << o.name << " b" << o.in_buf << "[" << o.in_off << ":+" << o.cin
+       << "] -> b" << o.out_buf << " look=" << o.look << " taps=" << o.taps << " nout=" << o.nout
+       << " pre=" << o.pre_act << " post=" << o.post_act << (o.gate ? " gate" : "");
+    if (o.res_buf >= 0) os << " +res(b" << o.res_buf << ", delay " << o.res_delay << ")";
+    os << "\n";
+  }
+  os << "sink: b" << sink_buf << "[" << sink_off << ":+" << sink_C << "] act=" << sink_act
+     << " rate=" << sink_rate.num << "/" << sink_rate.den << " ratio=" << ratio
+     << " latency_sink=" << latency_sink << " state_bytes_spec=" << state_bytes_spec
+     << " macs/sample=" << macs_per_sample << "\n";
+  return os.str();
+}
+
+}  // namespace scb

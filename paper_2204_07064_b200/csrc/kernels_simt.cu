@@ -1,0 +1,334 @@
+// kernels_simt.cu — bandwidth-class kernels of the streamconv B200 engine (sm_100a):
+//   * conv_simt: generic cached frame-convolution on FFMA (narrow layers: PQMF, 16-channel
+//     in/out convs, the gated head; and the fallback for shapes the tensor-core path does
+//     not take).  Replaces conv1d (kernels.cpp:73-104) applied to concat(cache, buffer).
+//   * ingest / egress: reference layout [stream][C][T] <-> frame-major buffers.
+//   * carry: cached-padding update "keep the trailing N frames"
+//     for every buffer and stream in ONE launch.
+//   * reset_streams: SPEC reset for a subset of streams.
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace scb {
+
+namespace {
+
+__device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
+  if (kind == ACT_LRELU) return v < 0.f ? alpha * v : v;  // kernels.cpp:125
+  if (kind == ACT_TANH) return tanhf(v);                  // kernels.cpp:123
+  return v;
+}
+
+// ------------------------------------------------------------------------ generic conv
+// C tile BM x BN per CTA, BK=16 K-slab, 256 threads, TM x TN register micro-tile.
+// K order is (tap, channel) ascending — fixed per layer, independent of T and of the number
+// of streams, so outputs are bit-identical across buffer partitions.
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__(256) conv_simt_kernel(const ConvParams p) {
+  constexpr int BK = 16;
+  constexpr int NT = (BM / TM) * (BN / TN);
+  static_assert(NT == 256, "256 threads");
+  constexpr int A_PER = BM * BK / NT;
+  constexpr int B_PER = BN * BK / NT;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN + 4];
+
+  const int tid = threadIdx.x;
+  const int64_t M = static_cast<int64_t>(p.streams) * p.t_out;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+  const int n0 = blockIdx.y * BN;
+  const int Ktot = p.taps * p.cin;
+
+  // A loader: fixed column (k within slab) per thread, A_PER rows
+  const int a_col = tid % BK;
+  const int a_row0 = tid / BK;
+  const float* a_ptr[A_PER];
+#pragma unroll
+  for (int e = 0; e < A_PER; ++e) {
+    const int64_t m = m0 + a_row0 + e * (NT / BK);
+    if (m < M) {
+      const int64_t s = m / p.t_out;
+      const int64_t i = m - s * p.t_out;
+      a_ptr[e] = p.in + s * p.in_sstride +
+                 (static_cast<int64_t>(p.in_f0) + i * p.row_step) * p.in_fstride + p.in_off;
+    } else {
+      a_ptr[e] = nullptr;
+    }
+  }
+  const int64_t tap_stride = static_cast<int64_t>(p.tap_step) * p.in_fstride;
+
+  const int tx = tid % (BN / TN);
+  const int ty = tid / (BN / TN);
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < Ktot; k0 += BK) {
+    {
+      const int kk = k0 + a_col;
+      const int q = kk / p.cin;
+      const int c = kk - q * p.cin;
+      const bool kv = kk < Ktot;
+#pragma unroll
+      for (int e = 0; e < A_PER; ++e) {
+        float v = 0.f;
+        if (kv && a_ptr[e]) v = act_apply(__ldg(a_ptr[e] + q * tap_stride + c), p.pre_act, p.pre_alpha);
+        As[a_col][a_row0 + e * (NT / BK)] = v;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < B_PER; ++e) {
+      const int idx = tid + e * NT;
+      const int kr = idx / BN;
+      const int nc = idx - kr * BN;
+      const int kk = k0 + kr;
+      const int n = n0 + nc;
+      Bs[kr][nc] = (kk < Ktot && n < p.nout) ? __ldg(p.w + static_cast<int64_t>(kk) * p.nout + n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[k][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[k][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+  // epilogue: bias -> post-activation -> (gate) -> + residual -> store
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t m = m0 + ty * TM + i;
+    if (m >= M) continue;
+    const int64_t s = m / p.t_out;
+    const int64_t row = m - s * p.t_out;
+    float* orow = p.out + s * p.out_sstride + p.out_base + row * p.out_rstride;
+    const float* rrow = p.res ? p.res + s * p.res_sstride +
+                                    (static_cast<int64_t>(p.res_f0) + row) * p.res_fstride + p.res_off
+                              : nullptr;
+    if (p.gate) {
+#pragma unroll
+      for (int j = 0; j < TN; j += 2) {
+        const int n = n0 + tx * TN + j;
+        if (n >= p.nout) continue;
+        const float a = acc[i][j] + __ldg(p.bias + n);
+        const float g = acc[i][j + 1] + __ldg(p.bias + n + 1);
+        orow[n >> 1] = tanhf(a) * (1.0f / (1.0f + expf(-g)));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = n0 + tx * TN + j;
+        if (n >= p.nout) continue;
+        float v = act_apply(acc[i][j] + __ldg(p.bias + n), p.post_act, p.post_alpha);
+        if (rrow) v = v + act_apply(rrow[n], p.res_act, p.res_alpha);
+        orow[n] = v;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ ingest / egress
+__global__ void ingest_kernel(const IngestArgs a) {
+  if (a.C == 1) {  // mono: contiguous copy per stream
+    const int64_t total = static_cast<int64_t>(a.streams) * a.T;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t s = g / a.T, t = g - s * a.T;
+      a.buf[s * a.sstride + a.cache + t] = a.in[g];
+    }
+    return;
+  }
+  __shared__ float tile[32][33];
+  const int ntt = (a.T + 31) / 32, ntc = (a.C + 31) / 32;
+  const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+    const int64_t s = tile_id / (ntt * ntc);
+    const int rem = static_cast<int>(tile_id - s * ntt * ntc);
+    const int t0 = (rem / ntc) * 32, c0 = (rem % ntc) * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int c = c0 + j, t = t0 + threadIdx.x;
+      tile[j][threadIdx.x] = (c < a.C && t < a.T) ? a.in[(s * a.C + c) * a.T + t] : 0.f;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int t = t0 + j, c = c0 + threadIdx.x;
+      if (t < a.T && c < a.C)
+        a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.C + c] = tile[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void egress_kernel(const EgressArgs a) {
+  if (a.C == 1) {
+    const int64_t total = static_cast<int64_t>(a.streams) * a.T;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t s = g / a.T, t = g - s * a.T;
+      a.out[g] = act_apply(a.buf[s * a.sstride + (a.cache + t) * static_cast<int64_t>(a.fstride) + a.off],
+                           a.act, a.alpha);
+    }
+    return;
+  }
+  __shared__ float tile[32][33];
+  const int ntt = (a.T + 31) / 32, ntc = (a.C + 31) / 32;
+  const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+    const int64_t s = tile_id / (ntt * ntc);
+    const int rem = static_cast<int>(tile_id - s * ntt * ntc);
+    const int t0 = (rem / ntc) * 32, c0 = (rem % ntc) * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int t = t0 + j, c = c0 + threadIdx.x;
+      tile[j][threadIdx.x] =
+          (t < a.T && c < a.C)
+              ? act_apply(a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.fstride + a.off + c],
+                          a.act, a.alpha)
+              : 0.f;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int c = c0 + j, t = t0 + threadIdx.x;
+      if (t < a.T && c < a.C) a.out[(s * a.C + c) * a.T + t] = tile[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------ carry / reset
+// One thread per (buffer, stream, channel column).  Frames move in ascending order in chunks
+// of 8 (all loads of a chunk before its stores): a chunk never reads a frame a previous
+// store wrote, because every load index f+T+u exceeds every earlier store index (T >= 1).
+__global__ void carry_kernel(const BufDesc* __restrict__ bufs, int nbuf, int streams,
+                             int64_t items, int64_t frames) {
+  __shared__ BufDesc sb[64];
+  for (int i = threadIdx.x; i < nbuf; i += blockDim.x) sb[i] = bufs[i];
+  __syncthreads();
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < items;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int b = 0;
+    while (b + 1 < nbuf && sb[b + 1].item0 <= g) ++b;
+    const BufDesc d = sb[b];
+    const int64_t loc = g - d.item0;
+    const int64_t s = loc / d.C;
+    const int c = static_cast<int>(loc - s * d.C);
+    const int64_t T = frames * d.rnum / d.rden;
+    float* col = d.base + s * d.sstride + c;
+    const int64_t fs = d.C;
+    int f = 0;
+    for (; f + 8 <= d.cache; f += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = col[(f + u + T) * fs];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) col[(f + u) * fs] = v[u];
+    }
+    for (; f < d.cache; ++f) col[f * fs] = col[(f + T) * fs];
+  }
+  (void)streams;
+}
+
+__global__ void reset_streams_kernel(const BufDesc* __restrict__ bufs, int nbuf,
+                                     const int* __restrict__ ids, int n_ids, int64_t per_stream) {
+  __shared__ BufDesc sb[64];
+  for (int i = threadIdx.x; i < nbuf; i += blockDim.x) sb[i] = bufs[i];
+  __syncthreads();
+  const int64_t items = per_stream * n_ids;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < items;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = g / per_stream;
+    const int64_t r = g - k * per_stream;
+    int b = 0;
+    while (b + 1 < nbuf && sb[b + 1].ritem0 <= r) ++b;
+    const BufDesc d = sb[b];
+    const int c = static_cast<int>(r - d.ritem0);
+    float* col = d.base + static_cast<int64_t>(ids[k]) * d.sstride + c;
+    for (int f = 0; f < d.cache; ++f) col[static_cast<int64_t>(f) * d.C] = 0.f;
+  }
+}
+
+// reference Kernel weights [N][M][K] -> [K][M][N] (the generic conv's B layout)
+__global__ void relayout_w_kernel(const float* __restrict__ w, int N, int M, int K,
+                                  float* __restrict__ o) {
+  const int64_t total = static_cast<int64_t>(N) * M * K;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = g / (static_cast<int64_t>(M) * K);
+    const int64_t r = g - n * M * K;
+    const int64_t m = r / K, k = r - m * K;
+    o[(k * M + m) * N + n] = w[g];
+  }
+}
+
+int grid_for(int64_t items, int threads) {
+  int64_t g = (items + threads - 1) / threads;
+  const int64_t cap = 148 * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+const void* ingest_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_kernel); }
+const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_kernel); }
+
+void launch_ingest(const IngestArgs& a, cudaStream_t st) {
+  if (a.C == 1) {
+    ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), dim3(256, 1), 0, st>>>(a);
+  } else {
+    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + 31) / 32) * ((a.C + 31) / 32);
+    ingest_kernel<<<grid_for(tiles, 1), dim3(32, 8), 0, st>>>(a);
+  }
+}
+
+void launch_egress(const EgressArgs& a, cudaStream_t st) {
+  if (a.C == 1) {
+    egress_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), dim3(256, 1), 0, st>>>(a);
+  } else {
+    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + 31) / 32) * ((a.C + 31) / 32);
+    egress_kernel<<<grid_for(tiles, 1), dim3(32, 8), 0, st>>>(a);
+  }
+}
+
+void launch_conv_simt(const ConvParams& p, cudaStream_t st) {
+  const int64_t M = static_cast<int64_t>(p.streams) * p.t_out;
+  if (p.nout > 32) {
+    dim3 grid(static_cast<unsigned>((M + 63) / 64), (p.nout + 63) / 64);
+    conv_simt_kernel<64, 64, 4, 4><<<grid, 256, 0, st>>>(p);
+  } else if (p.nout > 16) {
+    dim3 grid(static_cast<unsigned>((M + 127) / 128), (p.nout + 31) / 32);
+    conv_simt_kernel<128, 32, 4, 4><<<grid, 256, 0, st>>>(p);
+  } else {
+    dim3 grid(static_cast<unsigned>((M + 255) / 256), (p.nout + 15) / 16);
+    conv_simt_kernel<256, 16, 4, 4><<<grid, 256, 0, st>>>(p);
+  }
+}
+
+void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, int64_t frames,
+                  cudaStream_t st) {
+  if (nbuf == 0 || items == 0) return;
+  carry_kernel<<<grid_for(items, 256), 256, 0, st>>>(d_bufs, nbuf, streams, items, frames);
+}
+
+void launch_relayout_w(const float* w, int N, int M, int K, float* o, cudaStream_t st) {
+  relayout_w_kernel<<<grid_for(static_cast<int64_t>(N) * M * K, 256), 256, 0, st>>>(w, N, M, K, o);
+}
+
+void launch_reset_streams(const BufDesc* d_bufs, int nbuf, const int* d_ids, int n_ids,
+                          int64_t per_stream, cudaStream_t st) {
+  if (nbuf == 0 || n_ids == 0 || per_stream == 0) return;
+  reset_streams_kernel<<<grid_for(per_stream * n_ids, 256), 256, 0, st>>>(d_bufs, nbuf, d_ids,
+                                                                           n_ids, per_stream);
+}
+
+}  // namespace scb

@@ -1,0 +1,408 @@
+// runtime.cu — plans, stream states and the per-call launch sequence (the stream_runtime).
+//
+// A plan is the causalized, lowered model with device-resident weights (one per device).  A
+// state is SPEC's StreamState for a whole batch of independent streams:
+// every activation buffer [stream][cache + T][C] lives in HBM; the first `cache` frames of
+// each buffer ARE the cached padding.  One call (process_buffer) is:
+//   ingest(x) -> fused cached-conv ops in topological order -> egress(y) -> carry(caches)
+// replayed from a CUDA graph captured once per buffer length.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "program.hpp"
+#include "runtime.hpp"
+
+namespace scb {
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(SC_ERR_CUDA_BASE + static_cast<int>(e), std::string(what) + ": " + cudaGetErrorString(e));
+}
+int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+}  // namespace
+
+Plan::~Plan() {
+  if (wmem && device >= 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaFree(wmem);
+    cudaSetDevice(prev);
+  }
+}
+
+std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* W, int64_t nW,
+                                int in_C, int precision, int device) {
+  if (precision != SC_PREC_FP32 && precision != SC_PREC_BF16)
+    fail(SC_ERR_INVALID_ARGUMENT, "precision must be SC_PREC_FP32 or SC_PREC_BF16");
+  if (n_nodes > 0 && !W && nW > 0) fail(SC_ERR_INVALID_ARGUMENT, "weights pointer is null");
+  auto plan = std::make_unique<Plan>();
+  plan->prog = lower_graph(nodes, n_nodes, W, nW, in_C);
+  plan->precision = precision;
+  plan->device = device;
+  plan->desc = plan->prog.describe();
+  if (device == -1) return plan;  // host-only plan: lowering/causalize facts, no device state
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) fail(SC_ERR_INVALID_ARGUMENT, "bad device ordinal");
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  // one weight blob; each op's arrays 256-byte aligned
+  int64_t total = 0;
+  std::vector<int64_t> woff, boff;
+  for (const ConvOp& op : plan->prog.ops) {
+    woff.push_back(total);
+    total += round_up(static_cast<int64_t>(op.w.size()), 64);
+    boff.push_back(total);
+    total += round_up(static_cast<int64_t>(op.bias.size()), 64);
+  }
+  std::vector<float> host(static_cast<size_t>(std::max<int64_t>(total, 1)), 0.f);
+  for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
+    const ConvOp& op = plan->prog.ops[i];
+    std::memcpy(host.data() + woff[i], op.w.data(), op.w.size() * sizeof(float));
+    std::memcpy(host.data() + boff[i], op.bias.data(), op.bias.size() * sizeof(float));
+  }
+  ck(cudaMalloc(&plan->wmem, host.size() * sizeof(float)), "cudaMalloc(weights)");
+  ck(cudaMemcpy(plan->wmem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice),
+     "cudaMemcpy(weights)");
+  for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
+    DevOp d;
+    d.w = plan->wmem + woff[i];
+    d.bias = plan->wmem + boff[i];
+    d.kernel = KERNEL_SIMT;
+    plan->dops.push_back(d);
+  }
+  plan->desc = plan->prog.describe();
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+  return plan;
+}
+
+// --------------------------------------------------------------------------- state
+State::~State() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  for (auto& kv : graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  if (capture_stream) cudaStreamDestroy(capture_stream);
+  if (mem) cudaFree(mem);
+  if (d_desc) cudaFree(d_desc);
+  if (d_ids) cudaFree(d_ids);
+  cudaSetDevice(prev);
+}
+
+std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_frames) {
+  const Program& pg = plan->prog;
+  if (plan->device < 0) fail(SC_ERR_INVALID_ARGUMENT, "plan was created host-only (device -1)");
+  if (streams < 1) fail(SC_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
+  if (max_frames < 1) fail(SC_ERR_INVALID_ARGUMENT, "max_frames must be >= 1");
+  if (max_frames % pg.ratio != 0)
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO,
+         "max_frames " + std::to_string(max_frames) + " not a multiple of ratio " + std::to_string(pg.ratio));
+  auto st = std::make_unique<State>();
+  st->plan = plan;
+  st->streams = streams;
+  st->max_frames = max_frames;
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  int64_t total = 0;
+  std::vector<int64_t> off;
+  for (const BufferSpec& b : pg.bufs) {
+    const int64_t T = max_frames * b.rate.num / b.rate.den;
+    const int64_t sstride = round_up((b.cache + T) * b.C, 32);
+    st->buf_sstride.push_back(sstride);
+    off.push_back(total);
+    total += round_up(sstride * streams, 64);
+    st->cache_bytes_per_stream += b.cache * b.C * 4;
+  }
+  st->mem_bytes = total * 4;
+  ck(cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256)), "cudaMalloc(state)");
+  ck(cudaMemset(st->mem, 0, std::max<int64_t>(st->mem_bytes, 256)), "cudaMemset(state)");
+  for (size_t i = 0; i < pg.bufs.size(); ++i) st->buf_base.push_back(st->mem + off[i]);
+  // carry / reset table: buffers with a cache
+  std::vector<BufDesc> desc;
+  int64_t items = 0, ritems = 0;
+  for (size_t i = 0; i < pg.bufs.size(); ++i) {
+    const BufferSpec& b = pg.bufs[i];
+    if (b.cache == 0) continue;
+    BufDesc d{};
+    d.base = st->buf_base[i];
+    d.sstride = st->buf_sstride[i];
+    d.item0 = items;
+    d.ritem0 = ritems;
+    d.C = b.C;
+    d.cache = static_cast<int>(b.cache);
+    d.rnum = static_cast<int>(b.rate.num);
+    d.rden = static_cast<int>(b.rate.den);
+    items += static_cast<int64_t>(streams) * b.C;
+    ritems += b.C;
+    desc.push_back(d);
+  }
+  if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
+  st->n_desc = static_cast<int>(desc.size());
+  st->carry_items = items;
+  st->reset_items = ritems;
+  if (!desc.empty()) {
+    ck(cudaMalloc(&st->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
+    ck(cudaMemcpy(st->d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice),
+       "cudaMemcpy(desc)");
+  }
+  ck(cudaMalloc(&st->d_ids, sizeof(int) * streams), "cudaMalloc(ids)");
+  ck(cudaStreamCreateWithFlags(&st->capture_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+  return st;
+}
+
+ConvParams State::conv_params(size_t i, int64_t F) const {
+  const Program& pg = plan->prog;
+  const ConvOp& op = pg.ops[i];
+  const BufferSpec& bi = pg.bufs[op.in_buf];
+  const BufferSpec& bo = pg.bufs[op.out_buf];
+  const int64_t Tin = F * op.in_rate.num / op.in_rate.den;
+  ConvParams p{};
+  p.in = buf_base[op.in_buf];
+  p.in_sstride = buf_sstride[op.in_buf];
+  p.in_fstride = bi.C;
+  p.in_off = op.in_off;
+  p.cin = op.cin;
+  p.in_f0 = static_cast<int>(bi.cache - op.look);
+  p.row_step = op.row_step;
+  p.tap_step = op.tap_step;
+  p.taps = op.taps;
+  p.w = plan->dops[i].w;
+  p.bias = plan->dops[i].bias;
+  p.nout = op.nout;
+  p.out = buf_base[op.out_buf];
+  p.out_sstride = buf_sstride[op.out_buf];
+  p.out_base = bo.cache * bo.C;
+  p.out_rstride = op.out_rstride;
+  p.t_out = static_cast<int>(op.convt ? Tin : Tin / op.S);
+  p.streams = streams;
+  p.pre_act = op.pre_act;
+  p.pre_alpha = op.pre_alpha;
+  p.post_act = op.post_act;
+  p.post_alpha = op.post_alpha;
+  p.gate = op.gate ? 1 : 0;
+  if (op.res_buf >= 0) {
+    const BufferSpec& br = pg.bufs[op.res_buf];
+    p.res = buf_base[op.res_buf];
+    p.res_sstride = buf_sstride[op.res_buf];
+    p.res_fstride = br.C;
+    p.res_off = op.res_off;
+    p.res_f0 = static_cast<int>(br.cache - op.res_delay);
+    p.res_act = op.res_act;
+    p.res_alpha = op.res_alpha;
+  }
+  return p;
+}
+
+IngestArgs State::ingest_args(const float* in, int64_t F) const {
+  const Program& pg = plan->prog;
+  IngestArgs a{};
+  a.in = in;
+  a.buf = buf_base[0];
+  a.sstride = buf_sstride[0];
+  a.C = pg.in_C;
+  a.T = static_cast<int>(F);
+  a.cache = static_cast<int>(pg.bufs[0].cache);
+  a.streams = streams;
+  return a;
+}
+
+EgressArgs State::egress_args(float* out, int64_t F) const {
+  const Program& pg = plan->prog;
+  const BufferSpec& b = pg.bufs[pg.sink_buf];
+  EgressArgs a{};
+  a.buf = buf_base[pg.sink_buf];
+  a.sstride = buf_sstride[pg.sink_buf];
+  a.fstride = b.C;
+  a.off = pg.sink_off;
+  a.C = pg.sink_C;
+  a.T = static_cast<int>(F * pg.sink_rate.num / pg.sink_rate.den);
+  a.cache = static_cast<int>(b.cache);
+  a.streams = streams;
+  a.act = pg.sink_act;
+  a.alpha = pg.sink_alpha;
+  a.out = out;
+  return a;
+}
+
+int State::launches(int64_t F) const {
+  (void)F;
+  return 2 + static_cast<int>(plan->prog.ops.size()) + (n_desc > 0 ? 1 : 0);
+}
+
+void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s) const {
+  launch_ingest(ingest_args(in, F), s);
+  for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
+    const ConvParams p = conv_params(i, F);
+    launch_conv_simt(p, s);
+  }
+  launch_egress(egress_args(out, F), s);
+  launch_carry(d_desc, n_desc, streams, carry_items, F, s);
+}
+
+void State::check_frames(int64_t F) const {
+  if (F <= 0) fail(SC_ERR_INVALID_ARGUMENT, "frames must be positive");
+  if (F % plan->prog.ratio != 0)
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer length " + std::to_string(F) +
+                                                  " is not a multiple of the compression ratio " +
+                                                  std::to_string(plan->prog.ratio));
+  if (F > max_frames)
+    fail(SC_ERR_INVALID_ARGUMENT, "buffer length " + std::to_string(F) + " exceeds max_frames " +
+                                      std::to_string(max_frames));
+}
+
+void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
+  check_frames(F);
+  if (!in || !out) fail(SC_ERR_INVALID_ARGUMENT, "null I/O pointer");
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  if (!use_graphs) {
+    enqueue(in, out, F, s);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaSetDevice(prev), "cudaSetDevice");
+    return;
+  }
+  auto it = graphs.find(F);
+  if (it == graphs.end()) {
+    GraphEntry g;
+    ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+    enqueue(in, out, F, capture_stream);
+    cudaError_t le = cudaGetLastError();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);
+    ck(le, "launch (capture)");
+    ck(ee, "EndCapture");
+    g.graph = graph;
+    size_t n = 0;
+    ck(cudaGraphGetNodes(graph, nullptr, &n), "GraphGetNodes");
+    std::vector<cudaGraphNode_t> nodes(n);
+    ck(cudaGraphGetNodes(graph, nodes.data(), &n), "GraphGetNodes");
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
+      if (kp.func == ingest_kernel_ptr()) {
+        g.ingest_node = nd;
+        g.ingest_params = kp;
+      } else if (kp.func == egress_kernel_ptr()) {
+        g.egress_node = nd;
+        g.egress_params = kp;
+      }
+    }
+    if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
+    ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
+    g.ia = ingest_args(in, F);
+    g.ea = egress_args(out, F);
+    it = graphs.emplace(F, g).first;
+  }
+  GraphEntry& g = it->second;
+  if (g.ia.in != in) {
+    g.ia = ingest_args(in, F);
+    void* args[] = {&g.ia};
+    cudaKernelNodeParams kp = g.ingest_params;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
+  }
+  if (g.ea.out != out) {
+    g.ea = egress_args(out, F);
+    void* args[] = {&g.ea};
+    cudaKernelNodeParams kp = g.egress_params;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
+  }
+  ck(cudaGraphLaunch(g.exec, s), "GraphLaunch");
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+}
+
+void State::reset(const int* ids, int n_ids, cudaStream_t s) {
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  if (!ids) {
+    ck(cudaMemsetAsync(mem, 0, mem_bytes, s), "cudaMemsetAsync");
+  } else {
+    if (n_ids < 0 || n_ids > streams) fail(SC_ERR_INVALID_ARGUMENT, "bad id count");
+    for (int i = 0; i < n_ids; ++i)
+      if (ids[i] < 0 || ids[i] >= streams) fail(SC_ERR_INVALID_ARGUMENT, "stream id out of range");
+    if (n_ids > 0) {
+      ck(cudaMemcpyAsync(d_ids, ids, sizeof(int) * n_ids, cudaMemcpyHostToDevice, s), "copy ids");
+      launch_reset_streams(d_desc, n_desc, d_ids, n_ids, reset_items, s);
+      ck(cudaGetLastError(), "reset launch");
+      // the host id array may be reused by the caller after return
+      ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
+  }
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+}
+
+void conv1d_batched(const float* x, int batch, int M, int64_t L, const float* w, const float* b,
+                    int N, int K, int S, int d, float* y, cudaStream_t s) {
+  // check_conv_args (kernels.cpp:17-29)
+  if (batch < 1 || M < 1 || N < 1 || K < 1 || L < 0) fail(SC_ERR_INVALID_ARGUMENT, "conv1d shape");
+  if (S < 1 || d < 1) fail(SC_ERR_INVALID_ARGUMENT, "conv1d stride/dilation must be >= 1");
+  const int64_t span = static_cast<int64_t>(K - 1) * d + 1;
+  if (span > L)
+    fail(SC_ERR_INPUT_TOO_SHORT, "conv1d input length " + std::to_string(L) +
+                                     " shorter than kernel span " + std::to_string(span));
+  if (!x || !w || !b || !y) fail(SC_ERR_INVALID_ARGUMENT, "null pointer");
+  const int64_t Lo = (L - span) / S + 1;
+  float *xt = nullptr, *wt = nullptr, *yt = nullptr;
+  ck(cudaMallocAsync(&xt, sizeof(float) * batch * L * M, s), "cudaMallocAsync");
+  ck(cudaMallocAsync(&wt, sizeof(float) * static_cast<int64_t>(K) * M * N, s), "cudaMallocAsync");
+  ck(cudaMallocAsync(&yt, sizeof(float) * batch * Lo * N, s), "cudaMallocAsync");
+  IngestArgs ia{x, xt, L * M, M, static_cast<int>(L), 0, batch};
+  launch_ingest(ia, s);
+  launch_relayout_w(w, N, M, K, wt, s);
+  ConvParams p{};
+  p.in = xt;
+  p.in_sstride = L * M;
+  p.in_fstride = M;
+  p.cin = M;
+  p.row_step = S;
+  p.tap_step = d;
+  p.taps = K;
+  p.w = wt;
+  p.bias = b;
+  p.nout = N;
+  p.out = yt;
+  p.out_sstride = Lo * N;
+  p.out_rstride = N;
+  p.t_out = static_cast<int>(Lo);
+  p.streams = batch;
+  launch_conv_simt(p, s);
+  EgressArgs ea{};
+  ea.buf = yt;
+  ea.sstride = Lo * N;
+  ea.fstride = N;
+  ea.C = N;
+  ea.T = static_cast<int>(Lo);
+  ea.streams = batch;
+  ea.out = y;
+  launch_egress(ea, s);
+  ck(cudaGetLastError(), "conv1d launch");
+  cudaFreeAsync(xt, s);
+  cudaFreeAsync(wt, s);
+  cudaFreeAsync(yt, s);
+}
+
+}  // namespace scb

@@ -1,0 +1,82 @@
+// runtime.hpp — Plan (causalized model + device weights) and State (device StreamStates).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "program.hpp"
+
+namespace scb {
+
+enum KernelKind { KERNEL_SIMT = 0, KERNEL_TC = 1 };
+
+struct DevOp {
+  float* w = nullptr;
+  float* bias = nullptr;
+  int kernel = KERNEL_SIMT;
+};
+
+struct Plan {
+  Program prog;
+  int precision = SC_PREC_FP32;
+  int device = 0;
+  float* wmem = nullptr;
+  std::vector<DevOp> dops;
+  std::string desc;
+  ~Plan();
+};
+
+struct GraphEntry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t ingest_node = nullptr, egress_node = nullptr;
+  cudaKernelNodeParams ingest_params{}, egress_params{};
+  IngestArgs ia{};
+  EgressArgs ea{};
+};
+
+struct State {
+  const Plan* plan = nullptr;
+  int streams = 0;
+  int64_t max_frames = 0;
+  float* mem = nullptr;
+  int64_t mem_bytes = 0;
+  int64_t cache_bytes_per_stream = 0;
+  std::vector<float*> buf_base;
+  std::vector<int64_t> buf_sstride;
+  BufDesc* d_desc = nullptr;
+  int n_desc = 0;
+  int64_t carry_items = 0, reset_items = 0;
+  int* d_ids = nullptr;
+  bool use_graphs = true;
+  cudaStream_t capture_stream = nullptr;
+  std::map<int64_t, GraphEntry> graphs;
+
+  ConvParams conv_params(size_t op, int64_t frames) const;
+  IngestArgs ingest_args(const float* in, int64_t frames) const;
+  EgressArgs egress_args(float* out, int64_t frames) const;
+  void check_frames(int64_t frames) const;
+  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s) const;
+  int launches(int64_t frames) const;
+  void process(const float* in, float* out, int64_t frames, cudaStream_t s);
+  void reset(const int* ids, int n_ids, cudaStream_t s);
+  ~State();
+};
+
+std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* W, int64_t nW,
+                                int in_C, int precision, int device);
+std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_frames);
+
+// tensor_core conv1d (kernels.cpp:73-104) on a device batch, reference layout in and out.
+void conv1d_batched(const float* x, int batch, int M, int64_t L, const float* w, const float* b,
+                    int N, int K, int S, int d, float* y, cudaStream_t s);
+
+// PQMF filter bank design (pqmf.cpp).
+void pqmf_filters(int bands, int taps, float* analysis, float* synthesis, double* prototype);
+
+}  // namespace scb

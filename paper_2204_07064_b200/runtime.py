@@ -1,0 +1,162 @@
+"""Plan / StreamState: the Python face of the C-ABI (include/streamconv_b200.h).
+
+Mirrors the reference stream_runtime: `Plan` = causalize(g) + device
+weights, `StreamState` = init_state for a batch of independent streams, `.process_buffer` =
+process_buffer for all of them in one asynchronous call, `.reset` = reset.  Errors raise
+`StreamconvError` whose `.code` is the reference ErrCode name (error.hpp:8-29).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import PREC_BF16, PREC_FP32, check, lib
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            return 0
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _ptr(t) -> int:
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return int(t)
+
+
+class Plan:
+    def __init__(self, model, precision: str = "fp32", device: int = 0):
+        nodes, n, w = model.pack()
+        self._w = w
+        self.in_channels = model.in_channels
+        prec = {"fp32": PREC_FP32, "bf16": PREC_BF16}[precision]
+        h = C.c_void_p()
+        check(lib().sc_plan_create(nodes, n, w.ctypes.data_as(C.POINTER(C.c_float)), w.size,
+                                   model.in_channels, prec, device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.precision = precision
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sc_plan_destroy(self._h)
+            self._h = None
+
+    @property
+    def ratio(self) -> int:
+        r = C.c_int64()
+        check(lib().sc_plan_ratio(self._h, C.byref(r)))
+        return r.value
+
+    @property
+    def sink(self):
+        """(num, den, out_channels): output samples per input frame = num/den."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int32()
+        check(lib().sc_plan_sink_rate(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def latency(self) -> int:
+        r = C.c_int64()
+        check(lib().sc_plan_latency(self._h, C.byref(r)))
+        return r.value
+
+    @property
+    def state_bytes(self) -> int:
+        r = C.c_int64()
+        check(lib().sc_plan_state_bytes(self._h, C.byref(r)))
+        return r.value
+
+    @property
+    def macs_per_sample(self) -> float:
+        r = C.c_double()
+        check(lib().sc_plan_macs_per_sample(self._h, C.byref(r)))
+        return r.value
+
+    def describe(self) -> str:
+        return lib().sc_plan_describe(self._h).decode()
+
+    def out_frames(self, frames: int) -> int:
+        num, den, _ = self.sink
+        return frames * num // den
+
+
+class StreamState:
+    def __init__(self, plan: Plan, n_streams: int, max_frames: int):
+        self.plan = plan
+        self.n_streams = n_streams
+        self.max_frames = max_frames
+        h = C.c_void_p()
+        check(lib().sc_state_create(plan._h, n_streams, max_frames, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sc_state_destroy(self._h)
+            self._h = None
+
+    def process_buffer(self, x, y, frames: int, stream=None) -> None:
+        """x: device [n_streams][in_C][frames] fp32, y: device [n_streams][out_C][out_frames]."""
+        check(lib().sc_process(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
+                               C.c_void_p(_stream_handle(stream))))
+
+    def reset(self, stream_ids=None, stream=None) -> None:
+        if stream_ids is None:
+            check(lib().sc_state_reset(self._h, None, 0, C.c_void_p(_stream_handle(stream))))
+        else:
+            ids = np.ascontiguousarray(stream_ids, dtype=np.int32)
+            check(lib().sc_state_reset(self._h, ids.ctypes.data_as(C.POINTER(C.c_int32)), ids.size,
+                                       C.c_void_p(_stream_handle(stream))))
+
+    def set_graphs(self, enabled: bool) -> None:
+        check(lib().sc_state_set_graphs(self._h, 1 if enabled else 0))
+
+    def launches(self, frames: int) -> int:
+        n = C.c_int32()
+        check(lib().sc_process_launches(self._h, frames, C.byref(n)))
+        return n.value
+
+    @property
+    def device_bytes(self) -> int:
+        r = C.c_int64()
+        check(lib().sc_state_device_bytes(self._h, C.byref(r)))
+        return r.value
+
+    @property
+    def cache_bytes(self) -> int:
+        r = C.c_int64()
+        check(lib().sc_state_cache_bytes(self._h, C.byref(r)))
+        return r.value
+
+
+def conv1d(x, w, b, y, batch: int, in_channels: int, length: int, out_channels: int, taps: int,
+           stride: int = 1, dilation: int = 1, stream=None) -> None:
+    """Device conv1d (kernels.cpp:73-104) over a batch; reference layouts, device pointers."""
+    check(lib().sc_conv1d(C.c_void_p(_ptr(x)), batch, in_channels, length, C.c_void_p(_ptr(w)),
+                          C.c_void_p(_ptr(b)), out_channels, taps, stride, dilation,
+                          C.c_void_p(_ptr(y)), C.c_void_p(_stream_handle(stream))))
+
+
+def conv_output_length(length: int, taps: int, stride: int = 1, dilation: int = 1) -> int:
+    return lib().sc_conv_output_length(length, taps, stride, dilation)
+
+
+def delay_for_stride(stride: int, right_pad: int, cumulated: int) -> int:
+    return lib().sc_delay_for_stride(stride, right_pad, cumulated)
+
+
+def branch_alignment(delays):
+    d = np.ascontiguousarray(delays, dtype=np.int64)
+    out = np.zeros_like(d)
+    check(lib().sc_branch_alignment(d.ctypes.data_as(C.POINTER(C.c_int64)), d.size,
+                                    out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out.tolist()
