@@ -135,6 +135,9 @@ SC_API int sc_plan_latency(const sc_plan* plan, int64_t* samples);
 SC_API int sc_plan_state_bytes(const sc_plan* plan, int64_t* bytes_per_stream);
 /* Algorithmic work per stream per input sample (no zero-stuffed MACs, SPEC.md:405 fixed). */
 SC_API int sc_plan_macs_per_sample(const sc_plan* plan, double* macs);
+/* Number of fused conv ops, and op i's algorithmic MACs per stream per input sample. */
+SC_API int sc_plan_num_ops(const sc_plan* plan, int32_t* n);
+SC_API int sc_plan_op_macs(const sc_plan* plan, int32_t i, double* macs);
 /* Human-readable lowering summary (buffers, ops, kernels), valid until plan destroy. */
 SC_API const char* sc_plan_describe(const sc_plan* plan);
 
@@ -158,6 +161,12 @@ SC_API int sc_state_cache_bytes(const sc_state* state, int64_t* bytes_per_stream
 SC_API int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t frames, void* stream);
 /* Number of kernels one sc_process launches (for launch accounting). */
 SC_API int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n);
+/* Measurement: run `steps` calls WITHOUT graph replay with CUDA events between launches;
+ * ms_per_launch[i] = mean device time of launch i (sc_process_launches entries).          */
+SC_API int sc_state_profile(sc_state* state, const float* d_in, float* d_out, int64_t frames,
+                            int32_t steps, float* ms_per_launch, void* stream);
+/* Name of launch i of one call ("ingest", "op3 conv 128->128 K3 d9 [simt]", "carry", ...). */
+SC_API const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t i);
 /* Enable/disable CUDA-graph replay (default on). */
 SC_API int sc_state_set_graphs(sc_state* state, int32_t enabled);
 

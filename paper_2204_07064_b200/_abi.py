@@ -67,6 +67,8 @@ _SIGS = {
     "sc_plan_state_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_plan_macs_per_sample": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "sc_plan_describe": (C.c_char_p, [C.c_void_p]),
+    "sc_plan_num_ops": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "sc_plan_op_macs": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double)]),
     "sc_state_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_void_p)]),
     "sc_state_destroy": (C.c_int, [C.c_void_p]),
     "sc_state_reset": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
@@ -75,6 +77,9 @@ _SIGS = {
     "sc_process": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_launches": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32)]),
     "sc_state_set_graphs": (C.c_int, [C.c_void_p, C.c_int32]),
+    "sc_state_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                   C.POINTER(C.c_float), C.c_void_p]),
+    "sc_launch_name": (C.c_char_p, [C.c_void_p, C.c_int64, C.c_int32]),
     "sc_conv1d": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "sc_conv_output_length": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),

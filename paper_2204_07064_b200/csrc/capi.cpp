@@ -132,6 +132,21 @@ int sc_plan_macs_per_sample(const sc_plan* plan, double* macs) {
   });
 }
 
+int sc_plan_num_ops(const sc_plan* plan, int32_t* n) {
+  return guard([&] {
+    need(plan && n, "null argument");
+    *n = static_cast<int32_t>(plan->p->prog.ops.size());
+  });
+}
+
+int sc_plan_op_macs(const sc_plan* plan, int32_t i, double* macs) {
+  return guard([&] {
+    need(plan && macs, "null argument");
+    need(i >= 0 && i < static_cast<int32_t>(plan->p->prog.ops.size()), "op index out of range");
+    *macs = plan->p->prog.ops[i].macs_per_sample;
+  });
+}
+
 const char* sc_plan_describe(const sc_plan* plan) { return plan ? plan->p->desc.c_str() : ""; }
 
 int sc_state_create(const sc_plan* plan, int32_t n_streams, int64_t max_frames, sc_state** out) {
@@ -180,6 +195,21 @@ int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n) {
     need(state && n, "null argument");
     *n = state->s->launches(frames);
   });
+}
+
+int sc_state_profile(sc_state* state, const float* d_in, float* d_out, int64_t frames, int32_t steps,
+                     float* ms_per_launch, void* stream) {
+  return guard([&] {
+    need(state && ms_per_launch, "null argument");
+    state->s->profile(d_in, d_out, frames, steps, ms_per_launch, static_cast<cudaStream_t>(stream));
+  });
+}
+
+const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t i) {
+  if (!state) return "";
+  thread_local std::string name;
+  name = state->s->launch_name(frames, i);
+  return name.c_str();
 }
 
 int sc_state_set_graphs(sc_state* state, int32_t enabled) {

@@ -245,14 +245,62 @@ int State::launches(int64_t F) const {
   return 2 + static_cast<int>(plan->prog.ops.size()) + (n_desc > 0 ? 1 : 0);
 }
 
-void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s) const {
+std::string State::launch_name(int64_t F, int i) const {
+  const int nops = static_cast<int>(plan->prog.ops.size());
+  if (i == 0) return "ingest";
+  if (i >= 1 && i <= nops) {
+    const ConvOp& op = plan->prog.ops[i - 1];
+    return "op" + std::to_string(i - 1) + " " + op.name + " [" +
+           (plan->dops[i - 1].kernel == KERNEL_TC ? "tc" : "simt") + "]";
+  }
+  if (i == nops + 1) return "egress";
+  if (i == nops + 2 && n_desc > 0) return "carry";
+  (void)F;
+  return "";
+}
+
+void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s,
+                    cudaEvent_t* ev) const {
+  int e = 0;
+  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   launch_ingest(ingest_args(in, F), s);
+  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
     const ConvParams p = conv_params(i, F);
     launch_conv_simt(p, s);
+    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
   launch_egress(egress_args(out, F), s);
-  launch_carry(d_desc, n_desc, streams, carry_items, F, s);
+  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  if (n_desc > 0) {
+    launch_carry(d_desc, n_desc, streams, carry_items, F, s);
+    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  }
+}
+
+void State::profile(const float* in, float* out, int64_t F, int steps, float* ms, cudaStream_t s) {
+  check_frames(F);
+  if (steps < 1) fail(SC_ERR_INVALID_ARGUMENT, "steps must be >= 1");
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  const int n = launches(F);
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(n + 1) * steps);
+  for (auto& e : ev) ck(cudaEventCreate(&e), "EventCreate");
+  for (int k = 0; k < steps; ++k) enqueue(in, out, F, s, ev.data() + static_cast<size_t>(k) * (n + 1));
+  ck(cudaGetLastError(), "launch");
+  ck(cudaStreamSynchronize(s), "StreamSynchronize");
+  for (int i = 0; i < n; ++i) ms[i] = 0.f;
+  for (int k = 0; k < steps; ++k)
+    for (int i = 0; i < n; ++i) {
+      float t = 0.f;
+      ck(cudaEventElapsedTime(&t, ev[static_cast<size_t>(k) * (n + 1) + i],
+                              ev[static_cast<size_t>(k) * (n + 1) + i + 1]),
+         "EventElapsedTime");
+      ms[i] += t / steps;
+    }
+  for (auto& e : ev) cudaEventDestroy(e);
+  ck(cudaSetDevice(prev), "cudaSetDevice");
 }
 
 void State::check_frames(int64_t F) const {
@@ -273,7 +321,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
   if (!use_graphs) {
-    enqueue(in, out, F, s);
+    enqueue(in, out, F, s, nullptr);
     ck(cudaGetLastError(), "launch");
     ck(cudaSetDevice(prev), "cudaSetDevice");
     return;
@@ -282,7 +330,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   if (it == graphs.end()) {
     GraphEntry g;
     ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
-    enqueue(in, out, F, capture_stream);
+    enqueue(in, out, F, capture_stream, nullptr);
     cudaError_t le = cudaGetLastError();
     cudaGraph_t graph = nullptr;
     cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);

@@ -61,8 +61,10 @@ struct State {
   IngestArgs ingest_args(const float* in, int64_t frames) const;
   EgressArgs egress_args(float* out, int64_t frames) const;
   void check_frames(int64_t frames) const;
-  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s) const;
+  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s, cudaEvent_t* ev) const;
+  void profile(const float* in, float* out, int64_t frames, int steps, float* ms, cudaStream_t s);
   int launches(int64_t frames) const;
+  std::string launch_name(int64_t frames, int i) const;
   void process(const float* in, float* out, int64_t frames, cudaStream_t s);
   void reset(const int* ids, int n_ids, cudaStream_t s);
   ~State();

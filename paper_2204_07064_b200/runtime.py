@@ -82,6 +82,17 @@ class Plan:
         check(lib().sc_plan_macs_per_sample(self._h, C.byref(r)))
         return r.value
 
+    def op_macs(self):
+        """Algorithmic MACs per stream per input sample of each fused op."""
+        n = C.c_int32()
+        check(lib().sc_plan_num_ops(self._h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            v = C.c_double()
+            check(lib().sc_plan_op_macs(self._h, i, C.byref(v)))
+            out.append(v.value)
+        return out
+
     def describe(self) -> str:
         return lib().sc_plan_describe(self._h).decode()
 
@@ -124,6 +135,15 @@ class StreamState:
         n = C.c_int32()
         check(lib().sc_process_launches(self._h, frames, C.byref(n)))
         return n.value
+
+    def profile(self, x, y, frames: int, steps: int = 3, stream=None):
+        """Per-launch mean device ms over `steps` un-graphed calls (CUDA events between
+        launches on the launching stream).  Returns [(name, ms)]."""
+        n = self.launches(frames)
+        ms = (C.c_float * n)()
+        check(lib().sc_state_profile(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
+                                     steps, ms, C.c_void_p(_stream_handle(stream))))
+        return [(lib().sc_launch_name(self._h, frames, i).decode(), float(ms[i])) for i in range(n)]
 
     @property
     def device_bytes(self) -> int:

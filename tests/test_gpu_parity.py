@@ -1,0 +1,176 @@
+"""GPU parity: the C-ABI streaming path vs the CPU oracle (oracle/oracle.cpp, pinned to the
+reference's kernels.cpp) on the five BASELINE configs, plus SPEC stream_runtime properties.
+
+Tolerance (north star): fp32 path max |gpu - oracle| <= 1e-4 x RMS(oracle output).
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2204_07064_b200 import configs
+from paper_2204_07064_b200.runtime import Plan, StreamState
+
+torch = pytest.importorskip("torch")
+
+FP32_TOL = 1e-4
+
+
+def run_gpu(model, x, parts, precision="fp32", plan=None, state=None, graphs=True):
+    S, Cin, T = x.shape
+    plan = plan or Plan(model, precision=precision, device=0)
+    num, den, Cout = plan.sink
+    state = state or StreamState(plan, S, max(parts))
+    state.set_graphs(graphs)
+    xd = torch.from_numpy(x).cuda()
+    outs = []
+    t0 = 0
+    for p in parts:
+        xin = xd[:, :, t0:t0 + p].contiguous()
+        y = torch.empty((S, Cout, p * num // den), device="cuda", dtype=torch.float32)
+        state.process_buffer(xin, y, p)
+        outs.append(y)
+        t0 += p
+    torch.cuda.synchronize()
+    return torch.cat(outs, dim=2).cpu().numpy(), plan, state
+
+
+def rel_err(a, b):
+    rms = float(np.sqrt(np.mean(b.astype(np.float64) ** 2)))
+    return float(np.abs(a - b).max()) / rms, rms
+
+
+CASES = [
+    # cfg, streams, parts (input frames per call)
+    (1, 1, [2048] * 64),
+    (2, 4, [2048, 2048]),
+    (3, 3, [4096, 4096]),
+    (4, 4, [1, 1, 1]),
+    (5, 2, [2048, 2048]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,streams,parts", CASES, ids=[f"cfg{c[0]}" for c in CASES])
+def test_config_parity_fp32(cfg, streams, parts):
+    m = configs.build(cfg, seed=cfg)
+    x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=cfg)
+    y_or = po.run(m, x, parts, "stream")
+    y_gpu, plan, _ = run_gpu(m, x, parts)
+    err, rms = rel_err(y_gpu, y_or)
+    assert np.isfinite(y_gpu).all()
+    assert err <= FP32_TOL, f"cfg{cfg}: max err {err:.3e} x RMS ({rms:.3e})"
+    # and the offline convolution of the concatenated signal
+    y_off = po.run(m, x, None, "offline")
+    err2, _ = rel_err(y_gpu, y_off)
+    assert err2 <= FP32_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,parts_a,parts_b", [
+    (2, [512, 1536, 2048], [2048, 256, 1792]),
+    (3, [128 * 3, 128 * 29], [128 * 32]),
+    (5, [2048, 4096], [6144]),
+])
+def test_partition_bit_identity(cfg, parts_a, parts_b):
+    """identical outputs bit-for-bit across buffer partitions."""
+    m = configs.build(cfg, seed=11)
+    x = configs.batch_input(cfg, range(2), m.in_channels, sum(parts_a), seed=11)
+    ya, _, _ = run_gpu(m, x, parts_a)
+    yb, _, _ = run_gpu(m, x, parts_b)
+    assert np.array_equal(ya, yb)
+
+
+@pytest.mark.gpu
+def test_graph_vs_eager_identical():
+    m = configs.build(2, seed=3)
+    x = configs.batch_input(2, range(2), 128, 1024, seed=3)
+    ya, _, _ = run_gpu(m, x, [512, 512], graphs=True)
+    yb, _, _ = run_gpu(m, x, [512, 512], graphs=False)
+    assert np.array_equal(ya, yb)
+
+
+@pytest.mark.gpu
+def test_reset_all_and_subset():
+    """SPEC reset: processing after reset == fresh state."""
+    m = configs.build(2, seed=5)
+    x = configs.batch_input(2, range(3), 128, 1024, seed=5)
+    plan = Plan(m)
+    st = StreamState(plan, 3, 512)
+    y_fresh, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan)
+    run_gpu(m, x, [512, 512], plan=plan, state=st)          # dirty caches
+    st.reset()
+    y1, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan, state=st)
+    assert np.array_equal(y1, y_fresh)
+    run_gpu(m, x, [512, 512], plan=plan, state=st)          # dirty again
+    st.reset([1])
+    y2, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan, state=st)
+    assert np.array_equal(y2[1], y_fresh[1])
+    assert not np.array_equal(y2[0], y_fresh[0])
+
+
+@pytest.mark.gpu
+def test_memory_constancy():
+    """state size is a constant of the model, not of the stream length."""
+    m = configs.build(2, seed=1)
+    plan = Plan(m)
+    st = StreamState(plan, 2, 256)
+    b0 = (st.device_bytes, st.cache_bytes)
+    x = torch.randn(2, 128, 256, device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(200):
+        st.process_buffer(x, y, 256)
+    torch.cuda.synchronize()
+    assert (st.device_bytes, st.cache_bytes) == b0
+    assert plan.state_bytes == 61440  # closed form, SPEC.md:259 (4 blocks x 128 x 3d x 4 B)
+
+
+@pytest.mark.gpu
+def test_no_lookahead():
+    """perturbing a future input never changes already-emitted output."""
+    m = configs.build(3, seed=2)
+    x = configs.batch_input(3, range(1), 16, 128 * 8, seed=2)
+    x2 = x.copy()
+    x2[:, :, 128 * 5 + 7] += 10.0
+    ya, _, _ = run_gpu(m, x, [128] * 8)
+    yb, _, _ = run_gpu(m, x2, [128] * 8)
+    assert np.array_equal(ya[..., :128 * 5], yb[..., :128 * 5])
+
+
+@pytest.mark.gpu
+def test_process_errors():
+    from paper_2204_07064_b200 import StreamconvError
+    m = configs.build(3, seed=0)
+    plan = Plan(m)
+    st = StreamState(plan, 1, 256)
+    x = torch.zeros(1, 16, 256, device="cuda")
+    y = torch.zeros(1, 16, 256, device="cuda")
+    with pytest.raises(StreamconvError) as e:
+        st.process_buffer(x, y, 100)  # not a multiple of r=128
+    assert e.value.code == "BufferNotMultipleOfRatio"
+    with pytest.raises(StreamconvError) as e:
+        st.process_buffer(x, y, 512)  # > max_frames
+    assert e.value.code == "InvalidArgument"
+    with pytest.raises(StreamconvError) as e:
+        StreamState(plan, 1, 200)
+    assert e.value.code == "BufferNotMultipleOfRatio"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K,S,d,L", [(1, 1, 3, 1, 1, 4), (3, 5, 4, 2, 3, 37), (16, 64, 9, 4, 1, 130),
+                                         (64, 64, 3, 1, 1, 2050), (128, 128, 3, 1, 27, 300)])
+def test_conv1d_device_vs_reference(M, N, K, S, d, L):
+    """sc_conv1d (kernels.cpp:73-104) on a device batch vs the oracle conv1d."""
+    from paper_2204_07064_b200.runtime import conv1d
+    rng = np.random.default_rng(M * 1000 + K)
+    x = rng.standard_normal((3, M, L)).astype(np.float32)
+    w = rng.uniform(-1, 1, (N, M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, N).astype(np.float32)
+    Lo = (L - ((K - 1) * d + 1)) // S + 1
+    y = torch.empty((3, N, Lo), device="cuda")
+    conv1d(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda(), y,
+           3, M, L, N, K, S, d)
+    yr = np.stack([po.conv1d(x[i], w, b, S, d) for i in range(3)])
+    # fp32 FMA accumulation vs the reference's double accumulation: relative error bound
+    # ~ sqrt(M*K) ulps (SPEC.md:84 asks <= 1e-6 abs at |x|,|w| <= 1, M,N <= 8, K <= 16)
+    scale = np.abs(yr).max()
+    assert np.abs(y.cpu().numpy() - yr).max() <= 1e-6 * max(1.0, scale) * max(1.0, np.sqrt(M * K) / 4)
