@@ -14,8 +14,13 @@
         LReLU.2, strided conv K=2r+1 doubling] -> LReLU.2 -> conv K3 1024->256 (mean|var)
         -> slice mean 128 -> cfg4 decoder -> PQMF synthesis           16384 streams x
                                                                        {512, 2048, 8192}
-All weights Kaiming-uniform from the seed with zero bias; inputs seeded synthetic (no
-dataset exists for this path; BASELINE.json names none).
+All weights Kaiming-uniform from the seed (LeakyReLU(0.2) gain) with zero bias; in the
+RAVE-style residual stacks of cfg4/cfg5 the residual-branch convs are additionally scaled by
+RES_SCALE = 0.5 [decision]: with plain Kaiming the 15 residual units compound to a pre-gate
+RMS of ~66, where the sigmoid gate turns fp32-level relative errors into output errors far
+above the 1e-4 x RMS tolerance for ANY fp32-accumulating implementation; at 0.5 every layer
+stays at RMS O(0.1-1) and the tolerance measures the kernels, not the model's conditioning.
+Inputs are seeded synthetic (no dataset exists for this path; BASELINE.json names none).
 """
 from __future__ import annotations
 
@@ -26,6 +31,7 @@ import numpy as np
 from .graph import Model
 
 SR = 48000
+RES_SCALE = 0.5
 
 # frames = input frames per call per stream; out = output samples per call per stream
 CONFIGS = {
@@ -81,7 +87,7 @@ def _decoder(m: Model, latent: int = 128) -> Model:
         for d in (1, 3, 5):
             with m.residual():
                 m.leaky_relu(0.2)
-                m.conv(c, c, 3, dilation=d, padding=(d, d))
+                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=RES_SCALE)
     m.leaky_relu(0.2)
     m.conv(c, 32, 7, padding=(3, 3))  # 16 wave + 16 amplitude channels
     m.gate()
@@ -102,7 +108,7 @@ def cfg5(seed: int = 0) -> Model:
         for d in (1, 3, 5):
             with m.residual():
                 m.leaky_relu(0.2)
-                m.conv(c, c, 3, dilation=d, padding=(d, d))
+                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=RES_SCALE)
         m.leaky_relu(0.2)
         m.conv(c, 2 * c, 2 * r + 1, stride=r, padding=(r, r))
         c *= 2

@@ -47,6 +47,11 @@ struct Lowerer {
     b.cache = std::max(b.cache, frames);
   }
 
+  void need_align(int buf, int64_t a) {
+    BufferSpec& b = p->bufs[buf];
+    b.align = lcm(b.align, a);
+  }
+
   int new_buffer(int C, Rate rate, const std::string& name) {
     BufferSpec b;
     b.C = C;
@@ -144,20 +149,27 @@ struct Lowerer {
         p->state_bytes_spec += M * Da * 4;  // inserted Delay(D_a) ring
       }
       p->state_bytes_spec += M * Ptot * 4;
+      // A stride-S conv reads its input as S-frame super-rows (the polyphase view); its
+      // window start must sit on a super-row boundary, so the look-back is rounded up to a
+      // multiple of S and the kernel is front-padded with zero taps by the same shift.
+      const int64_t P = Ptot + Da;
+      const int64_t Pa = (S > 1) ? (P + S - 1) / S * S : P;
+      const int64_t shift = Pa - P;
       op.S = S;
       op.d = nd.dilation;
-      op.look = Ptot + Da;
-      op.taps = nd.taps;
+      op.look = Pa;
+      op.taps = static_cast<int>(K + shift);
       op.row_step = S;
       op.tap_step = nd.dilation;
       op.nout = nd.out_channels;
-      op.w.assign(static_cast<size_t>(K) * M * N, 0.0f);
+      op.w.assign(static_cast<size_t>(op.taps) * M * N, 0.0f);
       for (int64_t k = 0; k < K; ++k)
         for (int64_t c = 0; c < M; ++c)
           for (int64_t nn = 0; nn < N; ++nn)
-            op.w[(k * M + c) * N + nn] = w[(nn * M + c) * K + k];
+            op.w[((k + shift) * M + c) * N + nn] = w[(nn * M + c) * K + k];
       op.bias.assign(b, b + N);
       need_cache(v.buf, op.look);
+      if (S > 1) need_align(v.buf, S);
       op.macs_per_sample = static_cast<double>(M) * N * K / S;  // per input frame
       std::snprintf(nm, sizeof nm, "conv%s %d->%d K%d d%d", S > 1 ? ("/" + std::to_string(S)).c_str() : "",
                     (int)M, (int)N, (int)K, nd.dilation);
@@ -295,6 +307,7 @@ Program lower_graph(const sc_node* nodes, int n_nodes, const float* W, int64_t n
   Value v;
   v.C = in_C;
   lw.parse(v, 0);
+  for (BufferSpec& b : p.bufs) b.cache = (b.cache + b.align - 1) / b.align * b.align;
   p.sink_buf = v.buf;
   p.sink_off = v.off;
   p.sink_C = v.C;

@@ -1,0 +1,49 @@
+// kernels_tc.hpp — tcgen05/TMEM/TMA dense cached-conv (see kernels_tc.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+
+namespace scb {
+
+struct TcParams {
+  // tiling
+  int BN;               // 32 | 64 | 128 | 256
+  int R, G;             // tile = G streams x R rows (R*G <= 128)
+  int tiles_per_stream; // when G == 1
+  int m_tiles;
+  int n_kblocks;        // taps_view * cblocks
+  int cblocks;          // 32-channel blocks per tap (view channels padded to 32)
+  // A (input window) coordinates in the tensor-map view (channel, row, stream)
+  int a_c0;             // channel offset of the view
+  int a_row0;           // first window row of output row 0
+  int a_tap_rows;       // rows between taps
+  // epilogue (same meaning as ConvParams)
+  int pre_act;
+  float pre_alpha;
+  int post_act;
+  float post_alpha;
+  int gate;
+  int nout;
+  int t_out;
+  int streams;
+  const float* bias;
+  float* out;
+  int64_t out_sstride;
+  int64_t out_base;
+  int out_rstride;
+  const float* res;
+  int64_t res_sstride;
+  int res_fstride;
+  int res_off;
+  int res_f0;
+  int res_act;
+  float res_alpha;
+  int debug;  // experiments only (SC_TC_DEBUG): 1 skip transform math, 2 main MMA only, 4 skip drain loads
+};
+
+void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const TcParams& p, cudaStream_t st);
+
+}  // namespace scb

@@ -13,6 +13,7 @@ namespace scb {
 struct BufferSpec {
   int C = 1;
   int64_t cache = 0;  // frames kept across calls (max look-back of all readers)
+  int64_t align = 1;  // cache is rounded to a multiple of this (strided readers' super-rows)
   Rate rate;
   std::string name;
 };

@@ -6,9 +6,12 @@
 // each buffer ARE the cached padding.  One call (process_buffer) is:
 //   ingest(x) -> fused cached-conv ops in topological order -> egress(y) -> carry(caches)
 // replayed from a CUDA graph captured once per buffer length.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -28,6 +31,80 @@ void ck(cudaError_t e, const char* what) {
     throw Error(SC_ERR_CUDA_BASE + static_cast<int>(e), std::string(what) + ": " + cudaGetErrorString(e));
 }
 int64_t round_up(int64_t a, int64_t m) { return (a + m - 1) / m * m; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q), "GetDriverEntryPoint");
+    if (q != cudaDriverEntryPointSuccess || !f) fail(SC_ERR_CUDA_BASE, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 3-D fp32 tensor map with 128B swizzle (inner box = 32 floats = 128 bytes).
+CUtensorMap make_map3(const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1_bytes, s2_bytes};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(SC_ERR_CUDA_BASE, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+bool tc_disabled() {
+  const char* e = std::getenv("SC_DISABLE_TC");
+  return e && std::atoi(e) != 0;
+}
+
+// Decide whether an op runs on the tensor-core kernel and build its hi/lo weight planes.
+void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<float>& wtc) {
+  const ConvOp& op = pg.ops[i];
+  const BufferSpec& bi = pg.bufs[op.in_buf];
+  const bool strided = !op.convt && op.S > 1;
+  const int S = strided ? op.S : 1;
+  const int cin_view = S * op.cin;
+  const int bufC_view = S * bi.C;
+  bool ok = !tc_disabled() && precision == SC_PREC_FP32 && op.nout % 32 == 0 && op.nout <= 2048 &&
+            cin_view >= 16 &&
+            bufC_view % 4 == 0;
+  if (strided) ok = ok && op.in_off == 0 && op.cin == bi.C && op.d == 1;
+  if (!ok) return;
+  d.kernel = KERNEL_TC;
+  d.BN = (op.nout % 128 == 0) ? 128 : (op.nout % 64 == 0) ? 64 : 32;
+  d.view_S = S;
+  d.cin_view = cin_view;
+  d.cin_view_pad = static_cast<int>(round_up(cin_view, 32));
+  d.taps_view = strided ? static_cast<int>((op.taps + S - 1) / S) : op.taps;
+  d.tap_rows = strided ? 1 : op.tap_step;
+  const int64_t Kpad = static_cast<int64_t>(d.taps_view) * d.cin_view_pad;
+  const int64_t N = op.nout;
+  wtc.assign(static_cast<size_t>(2 * N * Kpad), 0.f);
+  for (int64_t n = 0; n < N; ++n)
+    for (int q = 0; q < d.taps_view; ++q)
+      for (int cv = 0; cv < cin_view; ++cv) {
+        float w;
+        if (strided) {
+          const int rho = cv / op.cin, c = cv % op.cin;
+          const int k = q * S + rho;
+          w = (k < op.taps) ? op.w[(static_cast<size_t>(k) * op.cin + c) * N + n] : 0.f;
+        } else {
+          w = op.w[(static_cast<size_t>(q) * op.cin + cv) * N + n];
+        }
+        const float hi = __builtin_bit_cast(float, __builtin_bit_cast(uint32_t, w) & 0xFFFFE000u);
+        const size_t o = static_cast<size_t>(n) * Kpad + static_cast<size_t>(q) * d.cin_view_pad + cv;
+        wtc[o] = hi;
+        wtc[static_cast<size_t>(N * Kpad) + o] = w - hi;
+      }
+}
 }  // namespace
 
 Plan::~Plan() {
@@ -58,29 +135,42 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(device), "cudaSetDevice");
   // one weight blob; each op's arrays 256-byte aligned
+  const size_t nops = plan->prog.ops.size();
+  plan->dops.assign(nops, DevOp{});
+  std::vector<std::vector<float>> wtc(nops);
+  for (size_t i = 0; i < nops; ++i) plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i]);
   int64_t total = 0;
-  std::vector<int64_t> woff, boff;
-  for (const ConvOp& op : plan->prog.ops) {
+  std::vector<int64_t> woff, boff, toff;
+  for (size_t i = 0; i < nops; ++i) {
+    const ConvOp& op = plan->prog.ops[i];
     woff.push_back(total);
     total += round_up(static_cast<int64_t>(op.w.size()), 64);
     boff.push_back(total);
     total += round_up(static_cast<int64_t>(op.bias.size()), 64);
+    toff.push_back(total);
+    total += round_up(static_cast<int64_t>(wtc[i].size()), 64);
   }
   std::vector<float> host(static_cast<size_t>(std::max<int64_t>(total, 1)), 0.f);
-  for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
+  for (size_t i = 0; i < nops; ++i) {
     const ConvOp& op = plan->prog.ops[i];
     std::memcpy(host.data() + woff[i], op.w.data(), op.w.size() * sizeof(float));
     std::memcpy(host.data() + boff[i], op.bias.data(), op.bias.size() * sizeof(float));
+    if (!wtc[i].empty()) std::memcpy(host.data() + toff[i], wtc[i].data(), wtc[i].size() * sizeof(float));
   }
   ck(cudaMalloc(&plan->wmem, host.size() * sizeof(float)), "cudaMalloc(weights)");
   ck(cudaMemcpy(plan->wmem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice),
      "cudaMemcpy(weights)");
-  for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
-    DevOp d;
+  for (size_t i = 0; i < nops; ++i) {
+    DevOp& d = plan->dops[i];
     d.w = plan->wmem + woff[i];
     d.bias = plan->wmem + boff[i];
-    d.kernel = KERNEL_SIMT;
-    plan->dops.push_back(d);
+    if (d.kernel == KERNEL_TC) {
+      const ConvOp& op = plan->prog.ops[i];
+      d.wtc = plan->wmem + toff[i];
+      const uint64_t Kpad = static_cast<uint64_t>(d.taps_view) * d.cin_view_pad;
+      d.map_w = make_map3(d.wtc, Kpad, op.nout, 2, Kpad * 4, static_cast<uint64_t>(op.nout) * Kpad * 4, 32,
+                          d.BN, 1);
+    }
   }
   plan->desc = plan->prog.describe();
   ck(cudaSetDevice(prev), "cudaSetDevice");
@@ -259,15 +349,83 @@ std::string State::launch_name(int64_t F, int i) const {
   return "";
 }
 
-void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s,
-                    cudaEvent_t* ev) const {
+const std::vector<TcLaunch>& State::tc_for(int64_t F) {
+  auto it = tc_launches.find(F);
+  if (it != tc_launches.end()) return it->second;
+  const Program& pg = plan->prog;
+  std::vector<TcLaunch> v(pg.ops.size());
+  for (size_t i = 0; i < pg.ops.size(); ++i) {
+    const DevOp& d = plan->dops[i];
+    if (d.kernel != KERNEL_TC) continue;
+    const ConvOp& op = pg.ops[i];
+    const BufferSpec& bi = pg.bufs[op.in_buf];
+    const ConvParams cp = conv_params(i, F);
+    const int64_t Tmax_in = max_frames * bi.rate.num / bi.rate.den;
+    const int S = d.view_S;
+    const uint64_t bufC_view = static_cast<uint64_t>(bi.C) * S;
+    const uint64_t rows_view = static_cast<uint64_t>((bi.cache + Tmax_in) / S);
+    TcParams& p = v[i].p;
+    p.BN = d.BN;
+    const int t_out = cp.t_out;
+    if (t_out >= 128) {
+      p.R = 128;
+      p.G = 1;
+      p.tiles_per_stream = (t_out + 127) / 128;
+      p.m_tiles = p.tiles_per_stream * streams;
+    } else {
+      p.R = t_out;
+      p.G = std::min(128 / t_out, streams);
+      p.tiles_per_stream = 1;
+      p.m_tiles = (streams + p.G - 1) / p.G;
+    }
+    p.cblocks = d.cin_view_pad / 32;
+    p.n_kblocks = d.taps_view * p.cblocks;
+    p.a_c0 = S > 1 ? 0 : op.in_off;
+    p.a_row0 = static_cast<int>((bi.cache - op.look) / S);
+    p.a_tap_rows = d.tap_rows;
+    p.pre_act = cp.pre_act;
+    p.pre_alpha = cp.pre_alpha;
+    p.post_act = cp.post_act;
+    p.post_alpha = cp.post_alpha;
+    p.gate = cp.gate;
+    p.nout = cp.nout;
+    p.t_out = t_out;
+    p.streams = streams;
+    p.bias = cp.bias;
+    p.out = cp.out;
+    p.out_sstride = cp.out_sstride;
+    p.out_base = cp.out_base;
+    p.out_rstride = cp.out_rstride;
+    p.res = cp.res;
+    p.res_sstride = cp.res_sstride;
+    p.res_fstride = cp.res_fstride;
+    p.res_off = cp.res_off;
+    p.res_f0 = cp.res_f0;
+    p.res_act = cp.res_act;
+    p.res_alpha = cp.res_alpha;
+    {
+      const char* dbg = std::getenv("SC_TC_DEBUG");
+      p.debug = dbg ? std::atoi(dbg) : 0;
+    }
+    v[i].map_a = make_map3(buf_base[op.in_buf], bufC_view, rows_view, streams, bufC_view * 4,
+                           static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
+                           static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
+  }
+  return tc_launches.emplace(F, std::move(v)).first->second;
+}
+
+void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s, cudaEvent_t* ev) {
   int e = 0;
+  const std::vector<TcLaunch>& tcl = tc_for(F);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   launch_ingest(ingest_args(in, F), s);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
-    const ConvParams p = conv_params(i, F);
-    launch_conv_simt(p, s);
+    if (plan->dops[i].kernel == KERNEL_TC) {
+      launch_conv_tc(tcl[i].map_a, plan->dops[i].map_w, tcl[i].p, s);
+    } else {
+      launch_conv_simt(conv_params(i, F), s);
+    }
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
   launch_egress(egress_args(out, F), s);
@@ -326,58 +484,70 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
     ck(cudaSetDevice(prev), "cudaSetDevice");
     return;
   }
-  auto it = graphs.find(F);
+  const auto key = std::make_tuple(F, in, out);
+  auto it = graphs.find(key);
   if (it == graphs.end()) {
-    GraphEntry g;
-    ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
-    enqueue(in, out, F, capture_stream, nullptr);
-    cudaError_t le = cudaGetLastError();
-    cudaGraph_t graph = nullptr;
-    cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);
-    ck(le, "launch (capture)");
-    ck(ee, "EndCapture");
-    g.graph = graph;
-    size_t n = 0;
-    ck(cudaGraphGetNodes(graph, nullptr, &n), "GraphGetNodes");
-    std::vector<cudaGraphNode_t> nodes(n);
-    ck(cudaGraphGetNodes(graph, nodes.data(), &n), "GraphGetNodes");
-    for (cudaGraphNode_t nd : nodes) {
-      cudaGraphNodeType ty;
-      ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
-      if (ty != cudaGraphNodeTypeKernel) continue;
-      cudaKernelNodeParams kp;
-      ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-      if (kp.func == ingest_kernel_ptr()) {
-        g.ingest_node = nd;
-        g.ingest_params = kp;
-      } else if (kp.func == egress_kernel_ptr()) {
-        g.egress_node = nd;
-        g.egress_params = kp;
-      }
+    // reuse the least recently used graph of this length once 8 pointer pairs exist
+    int same = 0;
+    auto lru = graphs.end();
+    for (auto jt = graphs.begin(); jt != graphs.end(); ++jt) {
+      if (std::get<0>(jt->first) != F) continue;
+      ++same;
+      if (lru == graphs.end() || jt->second.last_use < lru->second.last_use) lru = jt;
     }
-    if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
-    ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
-    g.ia = ingest_args(in, F);
-    g.ea = egress_args(out, F);
-    it = graphs.emplace(F, g).first;
+    GraphEntry g;
+    if (same >= 8) {
+      g = lru->second;
+      graphs.erase(lru);
+      g.ia = ingest_args(in, F);
+      g.ea = egress_args(out, F);
+      void* a1[] = {&g.ia};
+      cudaKernelNodeParams kp = g.ingest_params;
+      kp.kernelParams = a1;
+      kp.extra = nullptr;
+      ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
+      void* a2[] = {&g.ea};
+      kp = g.egress_params;
+      kp.kernelParams = a2;
+      kp.extra = nullptr;
+      ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
+    } else {
+      ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+      enqueue(in, out, F, capture_stream, nullptr);
+      cudaError_t le = cudaGetLastError();
+      cudaGraph_t graph = nullptr;
+      cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);
+      ck(le, "launch (capture)");
+      ck(ee, "EndCapture");
+      g.graph = graph;
+      size_t n = 0;
+      ck(cudaGraphGetNodes(graph, nullptr, &n), "GraphGetNodes");
+      std::vector<cudaGraphNode_t> nodes(n);
+      ck(cudaGraphGetNodes(graph, nodes.data(), &n), "GraphGetNodes");
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
+        if (ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
+        if (kp.func == ingest_kernel_ptr()) {
+          g.ingest_node = nd;
+          g.ingest_params = kp;
+        } else if (kp.func == egress_kernel_ptr()) {
+          g.egress_node = nd;
+          g.egress_params = kp;
+        }
+      }
+      if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
+      ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
+      ck(cudaGraphUpload(g.exec, s), "GraphUpload");
+      g.ia = ingest_args(in, F);
+      g.ea = egress_args(out, F);
+    }
+    it = graphs.emplace(key, g).first;
   }
   GraphEntry& g = it->second;
-  if (g.ia.in != in) {
-    g.ia = ingest_args(in, F);
-    void* args[] = {&g.ia};
-    cudaKernelNodeParams kp = g.ingest_params;
-    kp.kernelParams = args;
-    kp.extra = nullptr;
-    ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
-  }
-  if (g.ea.out != out) {
-    g.ea = egress_args(out, F);
-    void* args[] = {&g.ea};
-    cudaKernelNodeParams kp = g.egress_params;
-    kp.kernelParams = args;
-    kp.extra = nullptr;
-    ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
-  }
+  g.last_use = ++use_clock;
   ck(cudaGraphLaunch(g.exec, s), "GraphLaunch");
   ck(cudaSetDevice(prev), "cudaSetDevice");
 }

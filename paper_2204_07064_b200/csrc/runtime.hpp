@@ -4,11 +4,13 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "kernels.hpp"
+#include "kernels_tc.hpp"
 #include "program.hpp"
 
 namespace scb {
@@ -19,6 +21,12 @@ struct DevOp {
   float* w = nullptr;
   float* bias = nullptr;
   int kernel = KERNEL_SIMT;
+  // tensor-core path (kernel == KERNEL_TC)
+  float* wtc = nullptr;      // [2 (hi, lo)][nout][taps_view][cin_view_pad]
+  CUtensorMap map_w{};
+  int BN = 0;
+  int view_S = 1;            // super-row factor of the input view (conv stride, or 1)
+  int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
 };
 
 struct Plan {
@@ -38,6 +46,12 @@ struct GraphEntry {
   cudaKernelNodeParams ingest_params{}, egress_params{};
   IngestArgs ia{};
   EgressArgs ea{};
+  uint64_t last_use = 0;
+};
+
+struct TcLaunch {
+  CUtensorMap map_a{};
+  TcParams p{};
 };
 
 struct State {
@@ -55,13 +69,18 @@ struct State {
   int* d_ids = nullptr;
   bool use_graphs = true;
   cudaStream_t capture_stream = nullptr;
-  std::map<int64_t, GraphEntry> graphs;
+  // graphs keyed by (frames, in, out): replaying a graph whose I/O pointers match needs no
+  // parameter update (an updated exec graph is re-uploaded on its next launch)
+  std::map<std::tuple<int64_t, const float*, float*>, GraphEntry> graphs;
+  uint64_t use_clock = 0;
+  std::map<int64_t, std::vector<TcLaunch>> tc_launches;  // per call length, per op
 
   ConvParams conv_params(size_t op, int64_t frames) const;
+  const std::vector<TcLaunch>& tc_for(int64_t frames);
   IngestArgs ingest_args(const float* in, int64_t frames) const;
   EgressArgs egress_args(float* out, int64_t frames) const;
   void check_frames(int64_t frames) const;
-  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s, cudaEvent_t* ev) const;
+  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s, cudaEvent_t* ev);
   void profile(const float* in, float* out, int64_t frames, int steps, float* ms, cudaStream_t s);
   int launches(int64_t frames) const;
   std::string launch_name(int64_t frames, int i) const;

@@ -70,14 +70,14 @@ class Model:
 
     # ---- cached Conv1d: conv1d(pad(x,(L,R)), k, stride, dilation) (kernels.cpp:73-104)
     def conv(self, cin: int, cout: int, k: int, stride: int = 1, dilation: int = 1,
-             padding=None, weight=None, bias=None) -> "Model":
+             padding=None, weight=None, bias=None, scale: float = 1.0) -> "Model":
         if padding is None or padding == "centered":
             tot = (k - 1) * dilation if stride == 1 else k - 1
             padding = ((tot + 1) // 2, tot // 2)
         elif padding == "causal":
             padding = ((k - 1) * dilation if stride == 1 else k - 1, 0)
         if weight is None:
-            weight = kaiming_uniform(self._rng, cout, cin, k, cin * k)
+            weight = kaiming_uniform(self._rng, cout, cin, k, cin * k) * np.float32(scale)
         if bias is None:
             bias = np.zeros(cout, np.float32)
         off = self._add_weights(weight, bias)

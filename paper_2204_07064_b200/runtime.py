@@ -47,9 +47,12 @@ class Plan:
         self.precision = precision
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().sc_plan_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                lib().sc_plan_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def ratio(self) -> int:
@@ -111,9 +114,12 @@ class StreamState:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().sc_state_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                lib().sc_state_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def process_buffer(self, x, y, frames: int, stream=None) -> None:
         """x: device [n_streams][in_C][frames] fp32, y: device [n_streams][out_C][out_frames]."""

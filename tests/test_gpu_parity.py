@@ -44,8 +44,8 @@ CASES = [
     (1, 1, [2048] * 64),
     (2, 4, [2048, 2048]),
     (3, 3, [4096, 4096]),
-    (4, 4, [1, 1, 1]),
-    (5, 2, [2048, 2048]),
+    (4, 4, [1] * 8),
+    (5, 4, [2048] * 8),
 ]
 
 
