@@ -23,9 +23,10 @@
 //
 // Persistent: grid = #SMs, static tile striding; the TMA/transform/MMA pipeline runs across
 // tile boundaries and the drain/epilogue of tile t overlaps the MMAs of tile t+1.
-// Warp roles (448 threads): w0 TMA producer | w1 TMEM alloc + single-thread MMA issuer |
+// Warp roles (480 threads): w0 TMA producer | w1 TMEM alloc + single-thread MMA issuer |
 // w2..w5 transform | w6..w13 drain + epilogue (TMEM lane quarter = warp % 4, column half =
-// (warp - 6) / 4).
+// (warp - 6) / 4) | w14 epilogue I/O: residual tile TMA-loaded into the staging buffer as soon
+// as the previous output store has read it, output tile TMA-stored from staging.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -40,9 +41,10 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzled row
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
-constexpr int NUM_THREADS = 448;
+constexpr int NUM_THREADS = 480;
 constexpr int XF_WARP0 = 2;   // transform warps 2..5
 constexpr int EP_WARP0 = 6;   // drain/epilogue warps 6..13
+constexpr int IO_WARP = 14;   // residual TMA loads + output TMA stores
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -134,8 +136,33 @@ template <int BN, int STAGES>
 struct TcSmem {
   static constexpr uint32_t B_TILE = BN * BK * 4;
   static constexpr uint32_t STAGE = 2 * A_TILE + 2 * B_TILE;
-  static constexpr uint32_t BYTES = STAGES * STAGE + 1024 /*barriers*/ + 8192 /*bias*/ + 1024 /*align*/;
+  static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
+  static constexpr uint32_t BYTES = STAGES * STAGE + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
 };
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// float offset of (row, col) inside a staging tile of 32-column 128B-swizzled slabs
+__device__ __forceinline__ int stg_off(int row, int col) {
+  const int slab = col >> 5, c = col & 31;
+  return slab * (BM * 32) + row * 32 + ((((c >> 2) ^ (row & 7))) << 2) + (c & 3);
+}
 
 struct TileCoord {
   int s0, i0, n0;
@@ -159,18 +186,23 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
 template <int BN, int STAGES, int CK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
+                   const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
   using L = TcSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE);
+  float* stg = reinterpret_cast<float*>(smem + STAGES * L::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE + L::STAGING);
   uint64_t* full = bars;
   uint64_t* xform = bars + STAGES;
   uint64_t* empty = bars + 2 * STAGES;
   uint64_t* tfull = bars + 3 * STAGES;       // [2]
   uint64_t* tempty = bars + 3 * STAGES + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
-  float* sbias = reinterpret_cast<float*>(smem + STAGES * L::STAGE + 1024);  // <= 2048 floats
+  uint64_t* res_full = bars + 3 * STAGES + 4;
+  uint64_t* stg_written = bars + 3 * STAGES + 5;
+  uint64_t* stg_free = bars + 3 * STAGES + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 7);
+  float* sbias = reinterpret_cast<float*>(smem + STAGES * L::STAGE + L::STAGING + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
   auto a_lo = [&](int s) { return smem + s * L::STAGE + A_TILE; };
@@ -194,6 +226,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8);
     }
+    mbar_init(res_full, 1);
+    mbar_init(stg_written, 8);
+    mbar_init(stg_free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -205,6 +240,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_out)) : "memory");
   }
   for (int i = threadIdx.x; i < p.nout; i += NUM_THREADS) sbias[i] = p.bias[i];
   tc_fence_before();
@@ -268,6 +304,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+  } else if (warp == IO_WARP) {
+    // ===================== epilogue I/O (one thread) =====================
+    if (lane == 0) {
+      const int n_tiles_n2 = n_tiles_n;
+      const int out_cols = p.gate ? BN / 2 : BN;
+      int tcount = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+        const TileCoord tc = tile_coord(p, tile, n_tiles_n2, BN);
+        if (p.res) {  // staging is free (previous store read it): bring this tile's residual in
+          mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * 4u * p.R * p.G);
+          for (int k = 0; k < BN / 32; ++k)
+            tma_load_3d(&tmap_res, res_full, stg + k * (BM * 32), p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
+        }
+        if (p.debug & 8) continue;
+        mbar_wait(stg_written, tcount & 1);
+        const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
+        for (int k = 0; k < (out_cols + 31) / 32; ++k)
+          tma_store_3d(&tmap_out, stg + k * (BM * 32), oc0 + 32 * k, tc.i0, tc.s0);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(stg_free);
+      }
+      bulk_wait0();
+    }
   } else if (warp < EP_WARP0) {
     // ===================== transform (w2..w5) =====================
     const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
@@ -309,8 +369,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float acc[COLS];
 #pragma unroll
     for (int u = 0; u < COLS; ++u) acc[u] = 0.f;
-    int c = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    int c = 0, tcount = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
       for (int kb = 0; kb < nk; ++kb) {
         const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
@@ -341,58 +401,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[b]);
         ++c;
       }
-      // ---- epilogue of this tile: bias/act/gate/residual -> global
-      const int sl = r / p.R;
-      const int srow = tc.s0 + sl;
-      const int i = tc.i0 + (r - sl * p.R);
-      const bool valid = (r < p.R * p.G) && (srow < p.streams) && (i < p.t_out);
-      if (!valid) continue;
-      float* orow = p.out + static_cast<int64_t>(srow) * p.out_sstride + p.out_base +
-                    static_cast<int64_t>(i) * p.out_rstride;
-      const float* rrow = p.res ? p.res + static_cast<int64_t>(srow) * p.res_sstride +
-                                      (static_cast<int64_t>(p.res_f0) + i) * p.res_fstride + p.res_off
-                                : nullptr;
-      const int n0 = tc.n0 + col0;
+      // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
+      if (p.debug & 8) continue;
+      if (p.res) {
+        mbar_wait(res_full, tcount & 1);
+      } else if (tcount > 0) {
+        mbar_wait(stg_free, (tcount - 1) & 1);
+      }
       if (p.gate) {
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
-          const int n = n0 + u;
-          if (n < p.nout) {
-            const float a = acc[u] + sbias[n];
-            const float gg = acc[u + 1] + sbias[n + 1];
-            orow[n >> 1] = tanhf(a) * (1.0f / (1.0f + expf(-gg)));
-          }
+          const int n = tc.n0 + col0 + u;
+          const float a = acc[u] + sbias[n];
+          const float gg = acc[u + 1] + sbias[n + 1];
+          stg[stg_off(r, (col0 + u) >> 1)] = tanhf(a) * (1.0f / (1.0f + expf(-gg)));
         }
-      } else if (n0 + COLS <= p.nout && (p.out_rstride % 4) == 0 && (!rrow || (p.res_fstride % 4) == 0) &&
-                 (p.res_off % 4) == 0) {
+      } else {
 #pragma unroll
         for (int u = 0; u < COLS; u += 4) {
-          const float4 bv = *reinterpret_cast<const float4*>(sbias + n0 + u);
+          const int n = tc.n0 + col0 + u;
+          const float4 bv = *reinterpret_cast<const float4*>(sbias + n);
+          float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
           float4 o;
           o.x = act_apply(acc[u] + bv.x, p.post_act, p.post_alpha);
           o.y = act_apply(acc[u + 1] + bv.y, p.post_act, p.post_alpha);
           o.z = act_apply(acc[u + 2] + bv.z, p.post_act, p.post_alpha);
           o.w = act_apply(acc[u + 3] + bv.w, p.post_act, p.post_alpha);
-          if (rrow) {
-            const float4 rv = *reinterpret_cast<const float4*>(rrow + n0 + u);
+          if (p.res) {
+            const float4 rv = *dst;
             o.x += act_apply(rv.x, p.res_act, p.res_alpha);
             o.y += act_apply(rv.y, p.res_act, p.res_alpha);
             o.z += act_apply(rv.z, p.res_act, p.res_alpha);
             o.w += act_apply(rv.w, p.res_act, p.res_alpha);
           }
-          *reinterpret_cast<float4*>(orow + n0 + u) = o;
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < COLS; ++u) {
-          const int n = n0 + u;
-          if (n < p.nout) {
-            float x = act_apply(acc[u] + sbias[n], p.post_act, p.post_alpha);
-            if (rrow) x += act_apply(rrow[n], p.res_act, p.res_alpha);
-            orow[n] = x;
-          }
+          *dst = o;
         }
       }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(stg_written);
     }
   }
 
@@ -408,7 +455,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 int g_num_sms = 0;
 
 template <int BN, int STAGES, int CK>
-void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const TcParams& p, cudaStream_t st) {
+void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
+               const TcParams& p, cudaStream_t st) {
   using L = TcSmem<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -422,16 +470,17 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const TcParams& p, 
   }
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
-  conv_tc_kernel<BN, STAGES, CK><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, p);
+  conv_tc_kernel<BN, STAGES, CK><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 
 }  // namespace
 
-void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const TcParams& p, cudaStream_t st) {
+void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
+                    const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
   switch (p.BN) {
-    case 32: launch_bn<32, 4, 1>(map_a, map_w, p, st); break;
-    case 64: launch_bn<64, 4, 1>(map_a, map_w, p, st); break;
-    default: launch_bn<128, 3, 1>(map_a, map_w, p, st); break;
+    case 32: launch_bn<32, 4, 1>(map_a, map_w, map_out, map_res, p, st); break;
+    case 64: launch_bn<64, 3, 1>(map_a, map_w, map_out, map_res, p, st); break;
+    default: launch_bn<128, 2, 1>(map_a, map_w, map_out, map_res, p, st); break;
   }
 }
 

@@ -44,6 +44,9 @@ struct TcParams {
   int debug;  // experiments only (SC_TC_DEBUG): 1 skip transform math, 2 main MMA only, 4 skip drain loads
 };
 
-void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const TcParams& p, cudaStream_t st);
+// map_out: output rows (dims out_rstride x t_out x streams, base at the first output row),
+// map_res: residual rows (dims res_fstride x t_out x streams, base at res_f0); box 32 x R x G.
+void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
+                    const CUtensorMap& map_res, const TcParams& p, cudaStream_t st);
 
 }  // namespace scb

@@ -78,8 +78,16 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
             bufC_view % 4 == 0;
   if (strided) ok = ok && op.in_off == 0 && op.cin == bi.C && op.d == 1;
   if (!ok) return;
+  if (op.gate) {
+    // the output tile (BN/2 columns) must be a whole 32-column TMA box
+    if (op.nout > 64 && op.nout % 64 != 0) return;
+    d.BN = (op.nout % 128 == 0) ? 128 : 64;
+  } else {
+    d.BN = (op.nout % 128 == 0) ? 128 : (op.nout % 64 == 0) ? 64 : 32;
+  }
+  if (op.out_rstride % 4 != 0 || (op.res_buf >= 0 && (pg.bufs[op.res_buf].C % 4 != 0 || op.res_off % 4 != 0)))
+    return;
   d.kernel = KERNEL_TC;
-  d.BN = (op.nout % 128 == 0) ? 128 : (op.nout % 64 == 0) ? 64 : 32;
   d.view_S = S;
   d.cin_view = cin_view;
   d.cin_view_pad = static_cast<int>(round_up(cin_view, 32));
@@ -410,6 +418,20 @@ const std::vector<TcLaunch>& State::tc_for(int64_t F) {
     v[i].map_a = make_map3(buf_base[op.in_buf], bufC_view, rows_view, streams, bufC_view * 4,
                            static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
                            static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
+    // output rows start at out_base; rows >= t_out and streams >= n_streams are clipped by TMA
+    v[i].map_out = make_map3(cp.out + cp.out_base, static_cast<uint64_t>(cp.out_rstride),
+                             static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(cp.out_rstride) * 4,
+                             static_cast<uint64_t>(cp.out_sstride) * 4, 32, static_cast<uint32_t>(p.R),
+                             static_cast<uint32_t>(p.G));
+    if (cp.res) {
+      v[i].map_res = make_map3(cp.res + static_cast<int64_t>(cp.res_f0) * cp.res_fstride,
+                               static_cast<uint64_t>(cp.res_fstride), static_cast<uint64_t>(t_out), streams,
+                               static_cast<uint64_t>(cp.res_fstride) * 4,
+                               static_cast<uint64_t>(cp.res_sstride) * 4, 32, static_cast<uint32_t>(p.R),
+                               static_cast<uint32_t>(p.G));
+    } else {
+      v[i].map_res = v[i].map_out;  // unused
+    }
   }
   return tc_launches.emplace(F, std::move(v)).first->second;
 }
@@ -422,7 +444,7 @@ void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s, cuda
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
     if (plan->dops[i].kernel == KERNEL_TC) {
-      launch_conv_tc(tcl[i].map_a, plan->dops[i].map_w, tcl[i].p, s);
+      launch_conv_tc(tcl[i].map_a, plan->dops[i].map_w, tcl[i].map_out, tcl[i].map_res, tcl[i].p, s);
     } else {
       launch_conv_simt(conv_params(i, F), s);
     }

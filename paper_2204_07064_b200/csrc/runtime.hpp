@@ -51,6 +51,8 @@ struct GraphEntry {
 
 struct TcLaunch {
   CUtensorMap map_a{};
+  CUtensorMap map_out{};
+  CUtensorMap map_res{};
   TcParams p{};
 };
 
