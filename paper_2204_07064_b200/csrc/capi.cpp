@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 
+#include "kernels_tc.hpp"
 #include "runtime.hpp"
 
 struct sc_plan {
@@ -210,6 +211,11 @@ const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t i) {
   thread_local std::string name;
   name = state->s->launch_name(frames, i);
   return name.c_str();
+}
+
+// experiments only: timestamps written by the TC kernel when SC_TC_DEBUG has bit 32
+SC_API int sc_debug_tc_trace(long long* host) {
+  return guard([&] { scb::tc_trace_dump(host); });
 }
 
 int sc_state_set_graphs(sc_state* state, int32_t enabled) {

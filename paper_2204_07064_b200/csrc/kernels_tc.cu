@@ -24,11 +24,13 @@
 // Persistent: grid = #SMs, static tile striding; the TMA/transform/MMA pipeline runs across
 // tile boundaries and the drain/epilogue of tile t overlaps the MMAs of tile t+1.
 // Warp roles (480 threads): w0 TMA producer | w1 TMEM alloc + single-thread MMA issuer |
-// w2..w5 transform | w6..w13 drain + epilogue (TMEM lane quarter = warp % 4, column half =
-// (warp - 6) / 4) | w14 epilogue I/O: residual tile TMA-loaded into the staging buffer as soon
-// as the previous output store has read it, output tile TMA-stored from staging.
+// w2 epilogue I/O (residual tile TMA-loaded into the staging buffer once the previous output
+// store has read it; output tile TMA-stored from staging) | w3..w6 transform | w7..w14 drain +
+// epilogue (TMEM lane quarter = warp % 4, column half = (warp - 7) / 4).
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cuda_bf16.h>
 
 #include <cstdint>
 
@@ -38,13 +40,17 @@ namespace scb {
 
 namespace {
 
+__device__ long long g_tc_trace[10 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
+
+__device__ __forceinline__ long long clk() { return clock64(); }  // SM cycles (per-SM counter)
+
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzled row
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr int NUM_THREADS = 480;
-constexpr int XF_WARP0 = 2;   // transform warps 2..5
-constexpr int EP_WARP0 = 6;   // drain/epilogue warps 6..13
-constexpr int IO_WARP = 14;   // residual TMA loads + output TMA stores
+constexpr int IO_WARP = 2;    // residual TMA loads + output TMA stores
+constexpr int XF_WARP0 = 3;   // transform warps 3..6
+constexpr int EP_WARP0 = 7;   // drain/epilogue warps 7..14
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -110,6 +116,49 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       : "memory");
 }
 
+// K-major, 64B-swizzled canonical layout (bf16 rows of 32 elements): atoms of 8 rows x 64 B.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(512 >> 4) << 32;  // SBO: 8 rows x 64 B
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;         // SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// A operand from TMEM (lanes = M rows, 32-bit columns = K)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -126,16 +175,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// tanh / sigmoid are kept out of line: inlining them into the fully unrolled transform and
+// epilogue loops bloats the kernel past the instruction cache (measured: 4-16 us epilogues).
+__device__ __noinline__ float tanh_ool(float v) { return tanhf(v); }
+__device__ __noinline__ float gate_ool(float a, float g) { return tanhf(a) * (1.0f / (1.0f + expf(-g))); }
+
+// LeakyReLU / identity as one branch-free form (slope 1 = identity): no call, no spill
+__device__ __forceinline__ float act_lin(float v, float slope) { return v < 0.f ? slope * v : v; }
+__device__ __forceinline__ float slope_of(int kind, float alpha) { return kind == ACT_LRELU ? alpha : 1.f; }
+
 __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
   if (kind == ACT_LRELU) return v < 0.f ? alpha * v : v;
-  if (kind == ACT_TANH) return tanhf(v);
+  if (kind == ACT_TANH) return tanh_ool(v);
   return v;
 }
 
-template <int BN, int STAGES>
+// fp32 (3xTF32) stage: A (raw -> hi, in place) | W hi | W lo, K-major SW128 (32 fp32/row);
+//                      A lo goes to TMEM (the correction MMA reads A from TMEM).
+// bf16 stage:          A raw fp32 (SW128) | A bf16 (SW64, 32 bf16/row) | W bf16 (SW64).
+template <int BN, int STAGES, bool BF = false>
 struct TcSmem {
-  static constexpr uint32_t B_TILE = BN * BK * 4;
-  static constexpr uint32_t STAGE = 2 * A_TILE + 2 * B_TILE;
+  static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
+  static constexpr uint32_t A_BF = BM * BK * 2;
+  static constexpr uint32_t STAGE = BF ? A_TILE + A_BF + B_TILE : A_TILE + 2 * B_TILE;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
   static constexpr uint32_t BYTES = STAGES * STAGE + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
 };
@@ -183,12 +245,12 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
   return tc;
 }
 
-template <int BN, int STAGES, int CK>
+template <int BN, int STAGES, int CK, bool BF>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
-  using L = TcSmem<BN, STAGES>;
+  using L = TcSmem<BN, STAGES, BF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* stg = reinterpret_cast<float*>(smem + STAGES * L::STAGE);
@@ -201,20 +263,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* res_full = bars + 3 * STAGES + 4;
   uint64_t* stg_written = bars + 3 * STAGES + 5;
   uint64_t* stg_free = bars + 3 * STAGES + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 7);
+  uint64_t* corr_empty = bars + 3 * STAGES + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 8);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * L::STAGE + L::STAGING + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
-  auto a_lo = [&](int s) { return smem + s * L::STAGE + A_TILE; };
-  auto b_hi = [&](int s) { return smem + s * L::STAGE + 2 * A_TILE; };
-  auto b_lo = [&](int s) { return smem + s * L::STAGE + 2 * A_TILE + L::B_TILE; };
+  auto b_hi = [&](int s) { return smem + s * L::STAGE + A_TILE; };
+  auto b_lo = [&](int s) { return smem + s * L::STAGE + A_TILE + L::B_TILE; };
+  auto a_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
+  auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE + L::A_BF; };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = p.n_kblocks;
   const int n_tiles_n = (p.nout + BN - 1) / BN;
   const int n_tiles = p.m_tiles * n_tiles_n;
-  constexpr uint32_t TMEM_COLS = (4 * BN < 32) ? 32 : 4 * BN;  // 2 buffers x (main, corr)
+  // fp32: main x2 (chunk double buffer) | corr (whole tile) | A lo x STAGES (32 cols each)
+  // bf16: main x2
+  constexpr uint32_t COLS_USED = BF ? 2 * BN : 3 * BN + 32 * STAGES;
+  constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
+                                 : COLS_USED <= 256 ? 256 : 512;
+  static_assert(COLS_USED <= 512, "TMEM budget");
+  constexpr uint32_t CORR_COL = 2 * BN;
+  constexpr uint32_t ALO_COL = 3 * BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -229,6 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(res_full, 1);
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
+    mbar_init(corr_empty, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -242,6 +314,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_out)) : "memory");
   }
+  if ((p.debug & 32) && threadIdx.x == 0 && blockIdx.x < 256) {
+    g_tc_trace[7 * 256 + blockIdx.x] = clk();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tc_trace[9 * 256 + blockIdx.x] = smid;
+  }
   for (int i = threadIdx.x; i < p.nout; i += NUM_THREADS) sbias[i] = p.bias[i];
   tc_fence_before();
   __syncthreads();
@@ -251,29 +329,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      const uint32_t bytes = static_cast<uint32_t>(BK * 4 * p.R * p.G) + 2 * L::B_TILE;
+      const uint32_t bytes = static_cast<uint32_t>(BK * 4 * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
       int g = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[4 * 256 + g] = clk();
           const int q = kb / p.cblocks;
           const int cb = kb - q * p.cblocks;
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[0 * 256 + g] = clk();
           mbar_expect_tx(&full[s], bytes);
           tma_load_3d(&tmap_a, &full[s], a_hi(s), p.a_c0 + cb * BK, p.a_row0 + tc.i0 + q * p.a_tap_rows, tc.s0);
-          tma_load_3d(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
-          tma_load_3d(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+          if (BF) {
+            tma_load_3d(&tmap_w, &full[s], b_bf(s), kb * BK, tc.n0, 0);
+          } else {
+            tma_load_3d(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
+            tma_load_3d(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+      // c_format F32 | a,b format TF32 (2) or BF16 (1) | N >> 3 | M >> 4
+      const uint32_t fmt = BF ? 1u : 2u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(BM >> 4) << 24);
-      int g = 0, c = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int g = 0, c = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
           const int b = c & 1;
@@ -281,20 +367,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
           if (chunk_first && c >= 2) mbar_wait(&tempty[b], ((c >> 1) + 1) & 1);
           mbar_wait(&xform[s], (g / STAGES) & 1);
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[3 * 256 + g] = clk();
           tc_fence_after();
-          const uint32_t dmain = tmem_base + static_cast<uint32_t>(b * 2 * BN);
-          const uint32_t dcorr = dmain + BN;
-          const uint32_t ah = smem_u32(a_hi(s)), al = smem_u32(a_lo(s));
-          const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+          const uint32_t dmain = tmem_base + static_cast<uint32_t>(b * BN);
+          if (BF) {
+            const uint32_t ab = smem_u32(a_bf(s)), bb = smem_u32(b_bf(s));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-            const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-            if (!(p.debug & 2)) {
-              mma_tf32(dcorr, sw128_desc(al + off), sw128_desc(bh + off), idesc, acc0);
-              mma_tf32(dcorr, sw128_desc(ah + off), sw128_desc(bl + off), idesc, 1u);
+            for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes along the 64B row
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_bf16(dmain, sw64_desc(ab + kk * 32), sw64_desc(bb + kk * 32), idesc, acc0);
             }
-            mma_tf32(dmain, sw128_desc(ah + off), sw128_desc(bh + off), idesc, acc0);
+          } else {
+            const uint32_t ah = smem_u32(a_hi(s));
+            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+            const uint32_t dcorr = tmem_base + CORR_COL;
+            const uint32_t alo = tmem_base + ALO_COL + 32 * s;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 32 bytes along the swizzled row
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_tf32(dmain, sw128_desc(ah + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+            }
+            // corrections accumulate over the whole tile in one buffer (2^-10 of the signal: its
+            // own truncation is negligible); wait until the drain has read the previous tile's
+            if (kb == 0 && tcount > 0) mbar_wait(corr_empty, (tcount - 1) & 1);
+            if (!(p.debug & 2)) {
+#pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+                mma_tf32_ts(dcorr, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+                mma_tf32(dcorr, sw128_desc(ah + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+              }
+            }
           }
           mma_commit(&empty[s]);
           if (chunk_last) {
@@ -328,7 +431,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       bulk_wait0();
     }
-  } else if (warp < EP_WARP0) {
+  } else if (warp >= XF_WARP0 && warp < EP_WARP0) {
     // ===================== transform (w2..w5) =====================
     const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
     int g = 0;
@@ -336,30 +439,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
-        float4* ah = reinterpret_cast<float4*>(a_hi(s));
-        float4* al = reinterpret_cast<float4*>(a_lo(s));
+        if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[1 * 256 + g] = clk();
+        if (BF) {
+          // fp32 row t (SW128: 16B chunk j at j ^ (t & 7)) -> bf16 row t (SW64: 16B chunk jb at
+          // jb ^ ((t >> 1) & 3)), pre-activation fused
+          const float4* src = reinterpret_cast<const float4*>(a_hi(s)) + t * 8;
+          uint8_t* dst = a_bf(s) + t * 64;
+          const bool pre_tanh = p.pre_act == ACT_TANH;
+          const float pre_s = slope_of(p.pre_act, p.pre_alpha);
 #pragma unroll
-        for (int j = 0; j < ((p.debug & 1) ? 0 : (BM * BK / 4) / 128); ++j) {
-          const int e = t + j * 128;
-          const float4 v = ah[e];
-          float x[4] = {v.x, v.y, v.z, v.w};
-          float h[4], l[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float a = act_apply(x[u], p.pre_act, p.pre_alpha);
-            h[u] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-            l[u] = a - h[u];
+          for (int j4 = 0; j4 < 8; ++j4) {
+            float4 v = src[j4 ^ (t & 7)];
+            if (pre_tanh) {
+              v = make_float4(tanh_ool(v.x), tanh_ool(v.y), tanh_ool(v.z), tanh_ool(v.w));
+            } else {
+              v = make_float4(act_lin(v.x, pre_s), act_lin(v.y, pre_s), act_lin(v.z, pre_s), act_lin(v.w, pre_s));
+            }
+            __nv_bfloat162 lo2 = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 hi2 = __floats2bfloat162_rn(v.z, v.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+            const int jb = j4 >> 1;
+            *reinterpret_cast<uint2*>(dst + ((jb ^ ((t >> 1) & 3)) << 4) + ((j4 & 1) << 3)) = pk;
           }
-          ah[e] = make_float4(h[0], h[1], h[2], h[3]);
-          al[e] = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        if (!BF) {
+          // thread = tile row r (= TMEM lane): hi written back in place (smem, SW128 chunk
+          // j of row r lives at j ^ (r & 7)), lo stored to this stage's TMEM A columns
+          const int quarter = warp & 3;
+          const int r = quarter * 32 + lane;
+          float4* row = reinterpret_cast<float4*>(a_hi(s)) + r * 8;
+          const bool pre_tanh = p.pre_act == ACT_TANH;
+          const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+          float lo[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pj = j ^ (r & 7);
+            const float4 v = row[pj];
+            float x[4] = {v.x, v.y, v.z, v.w};
+            float h[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float a = pre_tanh ? tanh_ool(x[u]) : act_lin(x[u], pre_s);
+              h[u] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+              lo[4 * j + u] = a - h[u];
+            }
+            row[pj] = make_float4(h[0], h[1], h[2], h[3]);
+          }
+          tmem_st32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ALO_COL + 32 * s, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
         }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&xform[s]);
+        if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[2 * 256 + g] = clk();
       }
     }
-  } else {
-    // ===================== drain + epilogue (w6..w13) =====================
+  } else if (warp >= EP_WARP0) {
+    // ===================== drain + epilogue (w7..w14) =====================
     constexpr int COLS = BN / 2;
     const int quarter = warp & 3;
     const int half = (warp - EP_WARP0) >> 2;
@@ -378,23 +517,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool first = (kb / CK) == 0;
         const int b = c & 1;
         mbar_wait(&tfull[b], (c >> 1) & 1);
+        if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < COLS; cc += 16) {
-          uint32_t vm[16], vc[16];
-          if (p.debug & 4) {
+          uint32_t v[16];
+          tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);  // main chunk
+          tmem_wait_ld();
 #pragma unroll
-            for (int u = 0; u < 16; ++u) vm[u] = vc[u] = 0u;
-          } else {
-            tmem_ld16(lane_base + static_cast<uint32_t>(b * 2 * BN + cc), vm);
-            tmem_ld16(lane_base + static_cast<uint32_t>(b * 2 * BN + BN + cc), vc);
+          for (int u = 0; u < 16; ++u)
+            acc[cc + u] = first ? __uint_as_float(v[u]) : acc[cc + u] + __uint_as_float(v[u]);
+        }
+        if (!BF && kb == nk - 1) {  // the tile's corrections (complete with its last chunk)
+#pragma unroll
+          for (int cc = 0; cc < COLS; cc += 16) {
+            uint32_t v[16];
+            tmem_ld16(lane_base + CORR_COL + static_cast<uint32_t>(cc), v);
             tmem_wait_ld();
-          }
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const float x = __uint_as_float(vm[u]) + __uint_as_float(vc[u]);
-            acc[cc + u] = first ? x : acc[cc + u] + x;
+            for (int u = 0; u < 16; ++u) acc[cc + u] += __uint_as_float(v[u]);
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(corr_empty);
         }
         tc_fence_before();
         __syncwarp();
@@ -402,49 +547,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ++c;
       }
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
+      const bool trace = (p.debug & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
+      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
       if (p.debug & 8) continue;
       if (p.res) {
         mbar_wait(res_full, tcount & 1);
       } else if (tcount > 0) {
         mbar_wait(stg_free, (tcount - 1) & 1);
       }
+      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
       if (p.gate) {
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
           const int n = tc.n0 + col0 + u;
           const float a = acc[u] + sbias[n];
           const float gg = acc[u + 1] + sbias[n + 1];
-          stg[stg_off(r, (col0 + u) >> 1)] = tanhf(a) * (1.0f / (1.0f + expf(-gg)));
+          stg[stg_off(r, (col0 + u) >> 1)] = gate_ool(a, gg);
         }
-      } else {
+      } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
+        const float ps = slope_of(p.post_act, p.post_alpha);
+        const float rs = slope_of(p.res_act, p.res_alpha);
 #pragma unroll
-        for (int u = 0; u < COLS; u += 4) {
+        for (int u = 0; u < ((p.debug & 128) ? 0 : COLS); u += 4) {
           const int n = tc.n0 + col0 + u;
           const float4 bv = *reinterpret_cast<const float4*>(sbias + n);
           float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
           float4 o;
-          o.x = act_apply(acc[u] + bv.x, p.post_act, p.post_alpha);
-          o.y = act_apply(acc[u + 1] + bv.y, p.post_act, p.post_alpha);
-          o.z = act_apply(acc[u + 2] + bv.z, p.post_act, p.post_alpha);
-          o.w = act_apply(acc[u + 3] + bv.w, p.post_act, p.post_alpha);
+          o.x = act_lin(acc[u] + bv.x, ps);
+          o.y = act_lin(acc[u + 1] + bv.y, ps);
+          o.z = act_lin(acc[u + 2] + bv.z, ps);
+          o.w = act_lin(acc[u + 3] + bv.w, ps);
           if (p.res) {
             const float4 rv = *dst;
-            o.x += act_apply(rv.x, p.res_act, p.res_alpha);
-            o.y += act_apply(rv.y, p.res_act, p.res_alpha);
-            o.z += act_apply(rv.z, p.res_act, p.res_alpha);
-            o.w += act_apply(rv.w, p.res_act, p.res_alpha);
+            o.x += act_lin(rv.x, rs);
+            o.y += act_lin(rv.y, rs);
+            o.z += act_lin(rv.z, rs);
+            o.w += act_lin(rv.w, rs);
           }
           *dst = o;
         }
+      } else {  // tanh epilogues (unused by the five configs): out-of-line math
+#pragma unroll
+        for (int u = 0; u < COLS; ++u) {
+          const int n = tc.n0 + col0 + u;
+          float* dst = stg + stg_off(r, col0 + u);
+          float o = act_apply(acc[u] + sbias[n], p.post_act, p.post_alpha);
+          if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
+          *dst = o;
+        }
       }
+      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 2] = clk();
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(stg_written);
+      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 3] = clk();
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if ((p.debug & 32) && threadIdx.x == 0 && blockIdx.x < 256) g_tc_trace[8 * 256 + blockIdx.x] = clk();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
@@ -454,13 +616,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, int CK>
+template <int BN, int STAGES, int CK, bool BF>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES>;
+  using L = TcSmem<BN, STAGES, BF>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         L::BYTES);
     attr = true;
   }
   if (g_num_sms == 0) {
@@ -470,17 +633,27 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   }
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
-  conv_tc_kernel<BN, STAGES, CK><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  conv_tc_kernel<BN, STAGES, CK, BF><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 
 }  // namespace
 
+void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 10 * 256); }
+
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
+  if (p.bf16) {
+    switch (p.BN) {
+      case 32: launch_bn<32, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
   switch (p.BN) {
-    case 32: launch_bn<32, 4, 1>(map_a, map_w, map_out, map_res, p, st); break;
-    case 64: launch_bn<64, 3, 1>(map_a, map_w, map_out, map_res, p, st); break;
-    default: launch_bn<128, 2, 1>(map_a, map_w, map_out, map_res, p, st); break;
+    case 32: launch_bn<32, 4, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
+    case 64: launch_bn<64, 4, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
+    default: launch_bn<128, 3, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
   }
 }
 

@@ -41,6 +41,7 @@ struct TcParams {
   int res_f0;
   int res_act;
   float res_alpha;
+  int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
   int debug;  // experiments only (SC_TC_DEBUG): 1 skip transform math, 2 main MMA only, 4 skip drain loads
 };
 
@@ -48,5 +49,7 @@ struct TcParams {
 // map_res: residual rows (dims res_fstride x t_out x streams, base at res_f0); box 32 x R x G.
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st);
+
+void tc_trace_dump(long long* host);  // experiments: SC_TC_DEBUG & 32 timestamps
 
 }  // namespace scb

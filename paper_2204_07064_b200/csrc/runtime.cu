@@ -44,16 +44,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D fp32 tensor map with 128B swizzle (inner box = 32 floats = 128 bytes).
-CUtensorMap make_map3(const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
-                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+// 3-D tensor map (fp32 with 128B swizzle: inner box = 32 floats = 128 bytes; or bf16 with
+// 64B swizzle: inner box = 32 bf16 = 64 bytes).
+CUtensorMap make_map3(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2, bool bf16 = false) {
   CUtensorMap m;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {s1_bytes, s2_bytes};
   cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
-                           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                           const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(SC_ERR_CUDA_BASE, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -73,7 +75,7 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
   const int S = strided ? op.S : 1;
   const int cin_view = S * op.cin;
   const int bufC_view = S * bi.C;
-  bool ok = !tc_disabled() && precision == SC_PREC_FP32 && op.nout % 32 == 0 && op.nout <= 2048 &&
+  bool ok = !tc_disabled() && op.nout % 32 == 0 && op.nout <= 2048 &&
             cin_view >= 16 &&
             bufC_view % 4 == 0;
   if (strided) ok = ok && op.in_off == 0 && op.cin == bi.C && op.d == 1;
@@ -88,6 +90,7 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
   if (op.out_rstride % 4 != 0 || (op.res_buf >= 0 && (pg.bufs[op.res_buf].C % 4 != 0 || op.res_off % 4 != 0)))
     return;
   d.kernel = KERNEL_TC;
+  d.bf16 = precision == SC_PREC_BF16;
   d.view_S = S;
   d.cin_view = cin_view;
   d.cin_view_pad = static_cast<int>(round_up(cin_view, 32));
@@ -95,7 +98,9 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
   d.tap_rows = strided ? 1 : op.tap_step;
   const int64_t Kpad = static_cast<int64_t>(d.taps_view) * d.cin_view_pad;
   const int64_t N = op.nout;
-  wtc.assign(static_cast<size_t>(2 * N * Kpad), 0.f);
+  // fp32: [2 (hi, lo)][N][Kpad] floats; bf16: [N][Kpad] bf16 (round-to-nearest) packed in floats
+  wtc.assign(d.bf16 ? static_cast<size_t>((N * Kpad + 1) / 2) : static_cast<size_t>(2 * N * Kpad), 0.f);
+  uint16_t* wb = reinterpret_cast<uint16_t*>(wtc.data());
   for (int64_t n = 0; n < N; ++n)
     for (int q = 0; q < d.taps_view; ++q)
       for (int cv = 0; cv < cin_view; ++cv) {
@@ -107,10 +112,15 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
         } else {
           w = op.w[(static_cast<size_t>(q) * op.cin + cv) * N + n];
         }
-        const float hi = __builtin_bit_cast(float, __builtin_bit_cast(uint32_t, w) & 0xFFFFE000u);
         const size_t o = static_cast<size_t>(n) * Kpad + static_cast<size_t>(q) * d.cin_view_pad + cv;
-        wtc[o] = hi;
-        wtc[static_cast<size_t>(N * Kpad) + o] = w - hi;
+        if (d.bf16) {
+          const uint32_t u = __builtin_bit_cast(uint32_t, w);
+          wb[o] = static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);  // RN-even
+        } else {
+          const float hi = __builtin_bit_cast(float, __builtin_bit_cast(uint32_t, w) & 0xFFFFE000u);
+          wtc[o] = hi;
+          wtc[static_cast<size_t>(N * Kpad) + o] = w - hi;
+        }
       }
 }
 }  // namespace
@@ -176,8 +186,12 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
       const ConvOp& op = plan->prog.ops[i];
       d.wtc = plan->wmem + toff[i];
       const uint64_t Kpad = static_cast<uint64_t>(d.taps_view) * d.cin_view_pad;
-      d.map_w = make_map3(d.wtc, Kpad, op.nout, 2, Kpad * 4, static_cast<uint64_t>(op.nout) * Kpad * 4, 32,
-                          d.BN, 1);
+      if (d.bf16)
+        d.map_w = make_map3(d.wtc, Kpad, op.nout, 1, Kpad * 2, static_cast<uint64_t>(op.nout) * Kpad * 2, 32,
+                            d.BN, 1, true);
+      else
+        d.map_w = make_map3(d.wtc, Kpad, op.nout, 2, Kpad * 4, static_cast<uint64_t>(op.nout) * Kpad * 4, 32,
+                            d.BN, 1);
     }
   }
   plan->desc = plan->prog.describe();
@@ -349,7 +363,7 @@ std::string State::launch_name(int64_t F, int i) const {
   if (i >= 1 && i <= nops) {
     const ConvOp& op = plan->prog.ops[i - 1];
     return "op" + std::to_string(i - 1) + " " + op.name + " [" +
-           (plan->dops[i - 1].kernel == KERNEL_TC ? "tc" : "simt") + "]";
+           (plan->dops[i - 1].kernel == KERNEL_TC ? (plan->dops[i - 1].bf16 ? "tc-bf16" : "tc") : "simt") + "]";
   }
   if (i == nops + 1) return "egress";
   if (i == nops + 2 && n_desc > 0) return "carry";
@@ -374,6 +388,7 @@ const std::vector<TcLaunch>& State::tc_for(int64_t F) {
     const uint64_t rows_view = static_cast<uint64_t>((bi.cache + Tmax_in) / S);
     TcParams& p = v[i].p;
     p.BN = d.BN;
+    p.bf16 = d.bf16 ? 1 : 0;
     const int t_out = cp.t_out;
     if (t_out >= 128) {
       p.R = 128;
@@ -414,6 +429,8 @@ const std::vector<TcLaunch>& State::tc_for(int64_t F) {
     {
       const char* dbg = std::getenv("SC_TC_DEBUG");
       p.debug = dbg ? std::atoi(dbg) : 0;
+      const char* tr = std::getenv("SC_TC_TRACE_OP");
+      if (tr && std::atoi(tr) == static_cast<int>(i)) p.debug |= 32;
     }
     v[i].map_a = make_map3(buf_base[op.in_buf], bufC_view, rows_view, streams, bufC_view * 4,
                            static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,

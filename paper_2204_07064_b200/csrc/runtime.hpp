@@ -25,6 +25,7 @@ struct DevOp {
   float* wtc = nullptr;      // [2 (hi, lo)][nout][taps_view][cin_view_pad]
   CUtensorMap map_w{};
   int BN = 0;
+  bool bf16 = false;
   int view_S = 1;            // super-row factor of the input view (conv stride, or 1)
   int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
 };

@@ -65,6 +65,30 @@ def test_config_parity_fp32(cfg, streams, parts):
     assert err2 <= FP32_TOL
 
 
+# Separately stated bound for the bf16-operand / fp32-accumulate variant:
+# bf16 rounds each operand to 2^-9 relative, so per-layer errors are ~1e-3 of RMS and compound
+# over depth: normalized RMS error <= 1e-2, max |err| <= 1e-1 x RMS, correlation >= 0.9999.
+BF16_NRMSE = 1e-2
+BF16_MAX = 1e-1
+BF16_CORR = 0.9999
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,streams,parts", [(2, 2, [2048, 2048]), (4, 4, [1] * 8), (5, 2, [2048] * 8)],
+                         ids=["cfg2", "cfg4", "cfg5"])
+def test_config_parity_bf16(cfg, streams, parts):
+    m = configs.build(cfg, seed=cfg)
+    x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=cfg)
+    y_or = po.run(m, x, parts, "stream")
+    y_gpu, plan, _ = run_gpu(m, x, parts, precision="bf16")
+    err, rms = rel_err(y_gpu, y_or)
+    nrmse = float(np.sqrt(np.mean((y_gpu.astype(np.float64) - y_or) ** 2))) / rms
+    corr = float(np.corrcoef(y_gpu.ravel(), y_or.ravel())[0, 1])
+    assert nrmse <= BF16_NRMSE, f"cfg{cfg} bf16: nrmse {nrmse:.3e}"
+    assert err <= BF16_MAX, f"cfg{cfg} bf16: max err {err:.3e} x RMS"
+    assert corr >= BF16_CORR, corr
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg,parts_a,parts_b", [
     (2, [512, 1536, 2048], [2048, 256, 1792]),

@@ -10,8 +10,11 @@ from paper_2204_07064_b200.graph import Model
 from paper_2204_07064_b200.runtime import Plan, StreamState
 
 
+PREC = os.environ.get("SC_PREC", "fp32")
+
+
 def run(m, x, parts):
-    plan = Plan(m)
+    plan = Plan(m, precision=PREC)
     num, den, cout = plan.sink
     S = x.shape[0]
     st = StreamState(plan, S, max(parts))
