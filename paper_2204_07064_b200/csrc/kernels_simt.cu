@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvParams p) {
 }
 
 // ------------------------------------------------------------------------ ingest / egress
-__global__ void ingest_kernel(const IngestArgs a) {
+// Transposes run in 32-channel x 64-frame tiles: float4 loads/stores along the contiguous
+// axis on both sides (frame rows of C floats in the buffer, time rows of T floats outside).
+constexpr int TT = 64, TC = 32;
+
+__global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
   if (a.C == 1) {  // mono: contiguous copy per stream
     const int64_t total = static_cast<int64_t>(a.streams) * a.T;
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
@@ -148,28 +152,54 @@ __global__ void ingest_kernel(const IngestArgs a) {
     }
     return;
   }
-  __shared__ float tile[32][33];
-  const int ntt = (a.T + 31) / 32, ntc = (a.C + 31) / 32;
+  __shared__ float tile[TC][TT + 1];
+  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0);
+  const int ntt = (a.T + TT - 1) / TT, ntc = (a.C + TC - 1) / TC;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  const int tid = threadIdx.x;
   for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
     const int64_t s = tile_id / (ntt * ntc);
     const int rem = static_cast<int>(tile_id - s * ntt * ntc);
-    const int t0 = (rem / ntc) * 32, c0 = (rem % ntc) * 32;
-    for (int j = threadIdx.y; j < 32; j += 8) {
-      const int c = c0 + j, t = t0 + threadIdx.x;
-      tile[j][threadIdx.x] = (c < a.C && t < a.T) ? a.in[(s * a.C + c) * a.T + t] : 0.f;
+    const int t0 = (rem / ntc) * TT, c0 = (rem % ntc) * TC;
+    const bool full = vec && t0 + TT <= a.T && c0 + TC <= a.C;
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = tid + 256 * k;      // 512 float4 = 32 channel rows x 16
+        const int c = e >> 4, t4 = e & 15;
+        const float4 v = *reinterpret_cast<const float4*>(a.in + (s * a.C + c0 + c) * a.T + t0 + 4 * t4);
+        tile[c][4 * t4] = v.x;
+        tile[c][4 * t4 + 1] = v.y;
+        tile[c][4 * t4 + 2] = v.z;
+        tile[c][4 * t4 + 3] = v.w;
+      }
+    } else {
+      for (int e = tid; e < TC * TT; e += 256) {
+        const int c = e / TT, t = e % TT;
+        tile[c][t] = (c0 + c < a.C && t0 + t < a.T) ? a.in[(s * a.C + c0 + c) * a.T + t0 + t] : 0.f;
+      }
     }
     __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += 8) {
-      const int t = t0 + j, c = c0 + threadIdx.x;
-      if (t < a.T && c < a.C)
-        a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.C + c] = tile[threadIdx.x][j];
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = tid + 256 * k;      // 512 float4 = 64 frames x 8
+        const int t = e >> 3, c4 = e & 7;
+        const float4 v = make_float4(tile[4 * c4][t], tile[4 * c4 + 1][t], tile[4 * c4 + 2][t], tile[4 * c4 + 3][t]);
+        *reinterpret_cast<float4*>(a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + c0 + 4 * c4) = v;
+      }
+    } else {
+      for (int e = tid; e < TC * TT; e += 256) {
+        const int t = e / TC, c = e % TC;
+        if (t0 + t < a.T && c0 + c < a.C)
+          a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + c0 + c] = tile[c][t];
+      }
     }
     __syncthreads();
   }
 }
 
-__global__ void egress_kernel(const EgressArgs a) {
+__global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
   if (a.C == 1) {
     const int64_t total = static_cast<int64_t>(a.streams) * a.T;
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
@@ -180,25 +210,52 @@ __global__ void egress_kernel(const EgressArgs a) {
     }
     return;
   }
-  __shared__ float tile[32][33];
-  const int ntt = (a.T + 31) / 32, ntc = (a.C + 31) / 32;
+  __shared__ float tile[TC][TT + 1];
+  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0) && (a.fstride % 4 == 0) && (a.off % 4 == 0);
+  const int ntt = (a.T + TT - 1) / TT, ntc = (a.C + TC - 1) / TC;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  const int tid = threadIdx.x;
   for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
     const int64_t s = tile_id / (ntt * ntc);
     const int rem = static_cast<int>(tile_id - s * ntt * ntc);
-    const int t0 = (rem / ntc) * 32, c0 = (rem % ntc) * 32;
-    for (int j = threadIdx.y; j < 32; j += 8) {
-      const int t = t0 + j, c = c0 + threadIdx.x;
-      tile[j][threadIdx.x] =
-          (t < a.T && c < a.C)
-              ? act_apply(a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.fstride + a.off + c],
-                          a.act, a.alpha)
-              : 0.f;
+    const int t0 = (rem / ntc) * TT, c0 = (rem % ntc) * TC;
+    const bool full = vec && t0 + TT <= a.T && c0 + TC <= a.C;
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = tid + 256 * k;
+        const int t = e >> 3, c4 = e & 7;
+        const float4 v = *reinterpret_cast<const float4*>(
+            a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride + a.off + c0 + 4 * c4);
+        tile[4 * c4][t] = act_apply(v.x, a.act, a.alpha);
+        tile[4 * c4 + 1][t] = act_apply(v.y, a.act, a.alpha);
+        tile[4 * c4 + 2][t] = act_apply(v.z, a.act, a.alpha);
+        tile[4 * c4 + 3][t] = act_apply(v.w, a.act, a.alpha);
+      }
+    } else {
+      for (int e = tid; e < TC * TT; e += 256) {
+        const int t = e / TC, c = e % TC;
+        tile[c][t] = (t0 + t < a.T && c0 + c < a.C)
+                         ? act_apply(a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride +
+                                           a.off + c0 + c],
+                                     a.act, a.alpha)
+                         : 0.f;
+      }
     }
     __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += 8) {
-      const int c = c0 + j, t = t0 + threadIdx.x;
-      if (t < a.T && c < a.C) a.out[(s * a.C + c) * a.T + t] = tile[threadIdx.x][j];
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = tid + 256 * k;
+        const int c = e >> 4, t4 = e & 15;
+        const float4 v = make_float4(tile[c][4 * t4], tile[c][4 * t4 + 1], tile[c][4 * t4 + 2], tile[c][4 * t4 + 3]);
+        *reinterpret_cast<float4*>(a.out + (s * a.C + c0 + c) * a.T + t0 + 4 * t4) = v;
+      }
+    } else {
+      for (int e = tid; e < TC * TT; e += 256) {
+        const int c = e / TT, t = e % TT;
+        if (c0 + c < a.C && t0 + t < a.T) a.out[(s * a.C + c0 + c) * a.T + t0 + t] = tile[c][t];
+      }
     }
     __syncthreads();
   }
@@ -284,19 +341,19 @@ const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_k
 
 void launch_ingest(const IngestArgs& a, cudaStream_t st) {
   if (a.C == 1) {
-    ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), dim3(256, 1), 0, st>>>(a);
+    ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
   } else {
-    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + 31) / 32) * ((a.C + 31) / 32);
-    ingest_kernel<<<grid_for(tiles, 1), dim3(32, 8), 0, st>>>(a);
+    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + TT - 1) / TT) * ((a.C + TC - 1) / TC);
+    ingest_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
   }
 }
 
 void launch_egress(const EgressArgs& a, cudaStream_t st) {
   if (a.C == 1) {
-    egress_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), dim3(256, 1), 0, st>>>(a);
+    egress_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
   } else {
-    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + 31) / 32) * ((a.C + 31) / 32);
-    egress_kernel<<<grid_for(tiles, 1), dim3(32, 8), 0, st>>>(a);
+    const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + TT - 1) / TT) * ((a.C + TC - 1) / TC);
+    egress_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
   }
 }
 
