@@ -363,12 +363,14 @@ void build_graph(const sc_node* nodes, int n, const float* W, int64_t nW, int in
 
 // ---------------------------------------------------------------- execution
 struct StreamState {
-  std::vector<Sig> slot;  // per state index: cache [C][len]
+  std::vector<Sig> slot;      // per state index: cache [C][len]
+  std::vector<int64_t> n_in;  // per state index: input frames received (strided convs)
 };
 
 void init_state(const Graph& g, StreamState& st) {
   st.slot.clear();
   for (int i = 0; i < g.n_state; ++i) st.slot.emplace_back(g.state_C[i], g.state_len[i]);
+  st.n_in.assign(g.n_state, 0);
 }
 
 // Delay(d): streaming = ring of d samples; offline = zero-prepend + truncate
@@ -392,14 +394,25 @@ Sig run_prog(const Prog& prog, Sig x, StreamState* st, Mode mode, conv_fn_t fn) 
     switch (op.kind) {
       case OP_CONV: {
         const int64_t T = x.T;
-        const int64_t Tout = T / op.S;
+        int64_t Tout = T / op.S;
         Sig xin;
         if (mode == STREAM) {
-          // cached padding: xin = concat(cache, buf); cache = trailing L_total samples
-          // ("last N frames ... cached")
+          // cached padding: xin = concat(cache, buf); the cache keeps the trailing input
+          // samples the next output window starts at.  For a
+          // stride-S conv fed buffers that are not multiples of S (phase state, buffers below
+          // the compression ratio) the cache also holds the n_in mod S pending samples.
           Sig& cache = st->slot[op.state];
+          const int64_t n_prev = st->n_in[op.state];
+          const int64_t n_now = n_prev + T;
+          Tout = n_now / op.S - n_prev / op.S;
+          st->n_in[op.state] = n_now;
           xin = concat_time(cache, x);
-          cache = slice_time(xin, xin.T - op.P, op.P);
+          const int64_t keep = op.P + (n_now % op.S);
+          cache = slice_time(xin, xin.T - keep, keep);
+          if (Tout == 0) {
+            x = Sig(op.N, 0);
+            break;
+          }
         } else if (mode == OFFLINE_CAUSAL) {
           xin = pad_zeros(x, op.P, 0);  // causalized pad (L+R, 0)
         } else {
@@ -537,7 +550,11 @@ int oc_graph_info(const sc_node* nodes, int n, const float* W, int64_t nW, int i
 // x: [n_streams][in_C][T_total]; the per-stream signal is cut into consecutive buffers of
 // lengths `parts[0..n_parts)` (sum = T_total, each a multiple of the ratio) and the outputs
 // concatenated into y: [n_streams][out_C][T_total*sink].  mode: 0 stream, 1 offline of the
-// causalized graph (offline_run), 2 offline of the ORIGINAL graph.
+// causalized graph (offline_run), 2 offline of the ORIGINAL graph, 3 stream
+// with phase state: buffers need not be multiples of the compression ratio; every node emits
+// what its accumulated input allows and the per-call outputs are concatenated (the sink then
+// lags the input by up to ratio - buffer samples; the GPU emits the same stream delayed by a
+// fixed D, see sc_process).
 // conv_fn: NULL = oracle restatement; else a kernels.cpp-compatible conv (oracle/_ref).
 // threads: OpenMP threads across streams (SPEC.md:302,304 allow independent states to run
 // concurrently); 0 = runtime default.
@@ -549,9 +566,13 @@ int oc_run(const sc_node* nodes, int n, const float* W, int64_t nW, int in_C, in
     build_graph(nodes, n, W, nW, in_C, g);
     conv_fn_t fn = conv_fn ? reinterpret_cast<conv_fn_t>(conv_fn) : g_default_conv;
     int64_t sum = 0;
+    const bool phase = mode == 3;
+    if (phase) mode = 0;
     for (int p = 0; p < n_parts; ++p) {
-      if (parts[p] <= 0 || parts[p] % g.ratio != 0)
+      if (parts[p] <= 0 || (!phase && parts[p] % g.ratio != 0))
         throw OracleError(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer not multiple of ratio");
+      if (phase && (parts[p] * g.sink.num) % g.sink.den != 0)
+        throw OracleError(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer x sink rate not integral");
       sum += parts[p];
     }
     if (mode != 0) {

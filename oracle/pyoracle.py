@@ -161,7 +161,7 @@ def graph_info(model) -> dict:
                 out_channels=int(info[3]), latency_sink=int(info[4]), state_bytes=int(info[5]))
 
 
-MODES = {"stream": 0, "offline": 1, "offline_original": 2}
+MODES = {"stream": 0, "offline": 1, "offline_original": 2, "phase": 3}
 
 
 def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = False,

@@ -98,7 +98,8 @@ struct BufDesc {
   int64_t ritem0;   // prefix of C over the table (reset work items, per stream)
   int C;            // floats per frame
   int cache;        // cache frames
-  int rnum, rden;   // frames per input sample: a call of F input frames writes F*rnum/rden
+  int t;            // frames written this call (carry shift)
+  int pad_;
 };
 
 }  // namespace scb

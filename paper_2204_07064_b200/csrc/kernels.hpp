@@ -33,8 +33,7 @@ void launch_conv_simt(const ConvParams& p, cudaStream_t st);
 
 // Batched cache carry: for every buffer with cache > 0, frames [T, T+cache) -> [0, cache)
 // for every stream.  `items` = sum over buffers of streams*C (precomputed).
-void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, int64_t frames,
-                  cudaStream_t st);
+void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, cudaStream_t st);
 // Weights [N][M][K] -> [K][M][N].
 void launch_relayout_w(const float* w, int N, int M, int K, float* o, cudaStream_t st);
 // Zero the cache frames of the listed streams in every buffer.

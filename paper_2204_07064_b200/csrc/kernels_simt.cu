@@ -265,8 +265,7 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
 // One thread per (buffer, stream, channel column).  Frames move in ascending order in chunks
 // of 8 (all loads of a chunk before its stores): a chunk never reads a frame a previous
 // store wrote, because every load index f+T+u exceeds every earlier store index (T >= 1).
-__global__ void carry_kernel(const BufDesc* __restrict__ bufs, int nbuf, int streams,
-                             int64_t items, int64_t frames) {
+__global__ void carry_kernel(const BufDesc* __restrict__ bufs, int nbuf, int streams, int64_t items) {
   __shared__ BufDesc sb[64];
   for (int i = threadIdx.x; i < nbuf; i += blockDim.x) sb[i] = bufs[i];
   __syncthreads();
@@ -278,7 +277,7 @@ __global__ void carry_kernel(const BufDesc* __restrict__ bufs, int nbuf, int str
     const int64_t loc = g - d.item0;
     const int64_t s = loc / d.C;
     const int c = static_cast<int>(loc - s * d.C);
-    const int64_t T = frames * d.rnum / d.rden;
+    const int64_t T = d.t;
     float* col = d.base + s * d.sstride + c;
     const int64_t fs = d.C;
     int f = 0;
@@ -371,10 +370,9 @@ void launch_conv_simt(const ConvParams& p, cudaStream_t st) {
   }
 }
 
-void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, int64_t frames,
-                  cudaStream_t st) {
+void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, cudaStream_t st) {
   if (nbuf == 0 || items == 0) return;
-  carry_kernel<<<grid_for(items, 256), 256, 0, st>>>(d_bufs, nbuf, streams, items, frames);
+  carry_kernel<<<grid_for(items, 256), 256, 0, st>>>(d_bufs, nbuf, streams, items);
 }
 
 void launch_relayout_w(const float* w, int N, int M, int K, float* o, cudaStream_t st) {

@@ -204,9 +204,12 @@ State::~State() {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(plan->device);
-  for (auto& kv : graphs) {
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  for (auto& kv : plans) {
+    for (auto& g : kv.second->graphs) {
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+      if (g.second.graph) cudaGraphDestroy(g.second.graph);
+    }
+    if (kv.second->d_desc) cudaFree(kv.second->d_desc);
   }
   if (capture_stream) cudaStreamDestroy(capture_stream);
   if (mem) cudaFree(mem);
@@ -220,52 +223,63 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   if (plan->device < 0) fail(SC_ERR_INVALID_ARGUMENT, "plan was created host-only (device -1)");
   if (streams < 1) fail(SC_ERR_INVALID_ARGUMENT, "n_streams must be >= 1");
   if (max_frames < 1) fail(SC_ERR_INVALID_ARGUMENT, "max_frames must be >= 1");
-  if (max_frames % pg.ratio != 0)
+  if ((max_frames * pg.sink_rate.num) % pg.sink_rate.den != 0)
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "max_frames x sink rate is not an integer");
+  if (max_frames % pg.ratio != 0 && pg.ratio % max_frames != 0)
     fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO,
-         "max_frames " + std::to_string(max_frames) + " not a multiple of ratio " + std::to_string(pg.ratio));
+         "max_frames " + std::to_string(max_frames) + " is neither a multiple nor a divisor of the compression ratio " +
+             std::to_string(pg.ratio));
   auto st = std::make_unique<State>();
   st->plan = plan;
   st->streams = streams;
   st->max_frames = max_frames;
+  // Buffers shorter than the compression ratio need phase state: a stride-S reader keeps up
+  // to S-1 pending input frames (cache + S, still S-aligned) and the sink keeps a FIFO of up
+  // to (ratio - 1) x sink-rate frames (the fixed output lag).
+  st->phase_mode = max_frames % pg.ratio != 0;
+  st->cache.clear();
+  for (const BufferSpec& b : pg.bufs) st->cache.push_back(b.cache);
+  if (st->phase_mode) {
+    for (const ConvOp& op : pg.ops)
+      if (!op.convt && op.S > 1) st->cache[op.in_buf] = std::max(st->cache[op.in_buf], pg.bufs[op.in_buf].cache + op.S);
+    st->cache[pg.sink_buf] += (pg.ratio - 1) * pg.sink_rate.num / pg.sink_rate.den;
+  }
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
   int64_t total = 0;
   std::vector<int64_t> off;
-  for (const BufferSpec& b : pg.bufs) {
-    const int64_t T = max_frames * b.rate.num / b.rate.den;
-    const int64_t sstride = round_up((b.cache + T) * b.C, 32);
+  for (size_t i = 0; i < pg.bufs.size(); ++i) {
+    const BufferSpec& b = pg.bufs[i];
+    // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
+    const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
+    const int64_t sstride = round_up((st->cache[i] + T) * b.C, 32);
     st->buf_sstride.push_back(sstride);
     off.push_back(total);
     total += round_up(sstride * streams, 64);
-    st->cache_bytes_per_stream += b.cache * b.C * 4;
+    st->cache_bytes_per_stream += st->cache[i] * b.C * 4;
   }
   st->mem_bytes = total * 4;
   ck(cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256)), "cudaMalloc(state)");
   ck(cudaMemset(st->mem, 0, std::max<int64_t>(st->mem_bytes, 256)), "cudaMemset(state)");
   for (size_t i = 0; i < pg.bufs.size(); ++i) st->buf_base.push_back(st->mem + off[i]);
-  // carry / reset table: buffers with a cache
+  // reset table: buffers with a cache
   std::vector<BufDesc> desc;
-  int64_t items = 0, ritems = 0;
+  int64_t ritems = 0;
   for (size_t i = 0; i < pg.bufs.size(); ++i) {
     const BufferSpec& b = pg.bufs[i];
-    if (b.cache == 0) continue;
+    if (st->cache[i] == 0) continue;
     BufDesc d{};
     d.base = st->buf_base[i];
     d.sstride = st->buf_sstride[i];
-    d.item0 = items;
     d.ritem0 = ritems;
     d.C = b.C;
-    d.cache = static_cast<int>(b.cache);
-    d.rnum = static_cast<int>(b.rate.num);
-    d.rden = static_cast<int>(b.rate.den);
-    items += static_cast<int64_t>(streams) * b.C;
+    d.cache = static_cast<int>(st->cache[i]);
     ritems += b.C;
     desc.push_back(d);
   }
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
   st->n_desc = static_cast<int>(desc.size());
-  st->carry_items = items;
   st->reset_items = ritems;
   if (!desc.empty()) {
     ck(cudaMalloc(&st->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
@@ -274,122 +288,98 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   }
   ck(cudaMalloc(&st->d_ids, sizeof(int) * streams), "cudaMalloc(ids)");
   ck(cudaStreamCreateWithFlags(&st->capture_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  st->N.assign(pg.bufs.size(), 0);
   ck(cudaSetDevice(prev), "cudaSetDevice");
   return st;
 }
 
-ConvParams State::conv_params(size_t i, int64_t F) const {
+// Cumulative frames per buffer after one more call of F input samples: every op emits what
+// its accumulated input allows (stride S: floor(N_in / S); ConvT r: r N_in; else N_in).
+std::vector<int64_t> State::next_counts(int64_t F) const {
   const Program& pg = plan->prog;
-  const ConvOp& op = pg.ops[i];
-  const BufferSpec& bi = pg.bufs[op.in_buf];
-  const BufferSpec& bo = pg.bufs[op.out_buf];
-  const int64_t Tin = F * op.in_rate.num / op.in_rate.den;
-  ConvParams p{};
-  p.in = buf_base[op.in_buf];
-  p.in_sstride = buf_sstride[op.in_buf];
-  p.in_fstride = bi.C;
-  p.in_off = op.in_off;
-  p.cin = op.cin;
-  p.in_f0 = static_cast<int>(bi.cache - op.look);
-  p.row_step = op.row_step;
-  p.tap_step = op.tap_step;
-  p.taps = op.taps;
-  p.w = plan->dops[i].w;
-  p.bias = plan->dops[i].bias;
-  p.nout = op.nout;
-  p.out = buf_base[op.out_buf];
-  p.out_sstride = buf_sstride[op.out_buf];
-  p.out_base = bo.cache * bo.C;
-  p.out_rstride = op.out_rstride;
-  p.t_out = static_cast<int>(op.convt ? Tin : Tin / op.S);
-  p.streams = streams;
-  p.pre_act = op.pre_act;
-  p.pre_alpha = op.pre_alpha;
-  p.post_act = op.post_act;
-  p.post_alpha = op.post_alpha;
-  p.gate = op.gate ? 1 : 0;
-  if (op.res_buf >= 0) {
-    const BufferSpec& br = pg.bufs[op.res_buf];
-    p.res = buf_base[op.res_buf];
-    p.res_sstride = buf_sstride[op.res_buf];
-    p.res_fstride = br.C;
-    p.res_off = op.res_off;
-    p.res_f0 = static_cast<int>(br.cache - op.res_delay);
-    p.res_act = op.res_act;
-    p.res_alpha = op.res_alpha;
+  std::vector<int64_t> n(N);
+  n[0] = N[0] + F;
+  for (const ConvOp& op : pg.ops) {
+    const int64_t nin = n[op.in_buf];
+    n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? nin / op.S : nin);
   }
-  return p;
+  return n;
 }
 
-IngestArgs State::ingest_args(const float* in, int64_t F) const {
+CallPlan& State::call_plan(int64_t F) {
   const Program& pg = plan->prog;
-  IngestArgs a{};
-  a.in = in;
-  a.buf = buf_base[0];
-  a.sstride = buf_sstride[0];
-  a.C = pg.in_C;
-  a.T = static_cast<int>(F);
-  a.cache = static_cast<int>(pg.bufs[0].cache);
-  a.streams = streams;
-  return a;
-}
+  const std::vector<int64_t> n = next_counts(F);
+  const int64_t Fs = F * pg.sink_rate.num / pg.sink_rate.den;
+  const int sb = pg.sink_buf;
+  const int64_t D_ = (D < 0) ? lag_for(F) : D;
+  const int64_t row = (E - D_) - N[sb] + cache[sb];
+  if (E + Fs - D_ > n[sb] || row < 0)
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO,
+         "buffer length " + std::to_string(F) + " cannot continue this stream at lag " + std::to_string(D_) +
+             " (use one constant length below the compression ratio " + std::to_string(pg.ratio) + ")");
+  std::vector<int64_t> key;
+  key.push_back(F);
+  key.push_back(row);
+  for (size_t b = 0; b < n.size(); ++b) key.push_back(n[b] - N[b]);
+  for (const ConvOp& op : pg.ops) key.push_back(op.S > 1 && !op.convt ? N[op.in_buf] % op.S : 0);
+  auto it = plans.find(key);
+  if (it != plans.end()) return *it->second;
 
-EgressArgs State::egress_args(float* out, int64_t F) const {
-  const Program& pg = plan->prog;
-  const BufferSpec& b = pg.bufs[pg.sink_buf];
-  EgressArgs a{};
-  a.buf = buf_base[pg.sink_buf];
-  a.sstride = buf_sstride[pg.sink_buf];
-  a.fstride = b.C;
-  a.off = pg.sink_off;
-  a.C = pg.sink_C;
-  a.T = static_cast<int>(F * pg.sink_rate.num / pg.sink_rate.den);
-  a.cache = static_cast<int>(b.cache);
-  a.streams = streams;
-  a.act = pg.sink_act;
-  a.alpha = pg.sink_alpha;
-  a.out = out;
-  return a;
-}
-
-int State::launches(int64_t F) const {
-  (void)F;
-  return 2 + static_cast<int>(plan->prog.ops.size()) + (n_desc > 0 ? 1 : 0);
-}
-
-std::string State::launch_name(int64_t F, int i) const {
-  const int nops = static_cast<int>(plan->prog.ops.size());
-  if (i == 0) return "ingest";
-  if (i >= 1 && i <= nops) {
-    const ConvOp& op = plan->prog.ops[i - 1];
-    return "op" + std::to_string(i - 1) + " " + op.name + " [" +
-           (plan->dops[i - 1].kernel == KERNEL_TC ? (plan->dops[i - 1].bf16 ? "tc-bf16" : "tc") : "simt") + "]";
+  auto cp = std::make_unique<CallPlan>();
+  cp->F = F;
+  cp->egress_row = row;
+  cp->egress_T = Fs;
+  for (size_t b = 0; b < n.size(); ++b) cp->T.push_back(n[b] - N[b]);
+  for (const ConvOp& op : pg.ops) {
+    cp->pend.push_back(op.S > 1 && !op.convt ? N[op.in_buf] % op.S : 0);
+    cp->t_out.push_back(op.convt ? cp->T[op.in_buf] : cp->T[op.out_buf]);
   }
-  if (i == nops + 1) return "egress";
-  if (i == nops + 2 && n_desc > 0) return "carry";
-  (void)F;
-  return "";
-}
-
-const std::vector<TcLaunch>& State::tc_for(int64_t F) {
-  auto it = tc_launches.find(F);
-  if (it != tc_launches.end()) return it->second;
-  const Program& pg = plan->prog;
-  std::vector<TcLaunch> v(pg.ops.size());
+  for (size_t b = 0; b < pg.bufs.size(); ++b)
+    if (cache[b] > static_cast<int64_t>(buf_sstride[b] / pg.bufs[b].C) - cp->T[b])
+      fail(SC_ERR_INVALID_ARGUMENT, "buffer length exceeds max_frames");
+  // carry table: shift each cached buffer by this call's new frames
+  std::vector<BufDesc> desc;
+  int64_t items = 0;
+  for (size_t i = 0; i < pg.bufs.size(); ++i) {
+    const BufferSpec& b = pg.bufs[i];
+    if (cache[i] == 0 || cp->T[i] == 0) continue;
+    BufDesc d{};
+    d.base = buf_base[i];
+    d.sstride = buf_sstride[i];
+    d.item0 = items;
+    d.C = b.C;
+    d.cache = static_cast<int>(cache[i]);
+    d.t = static_cast<int>(cp->T[i]);
+    items += static_cast<int64_t>(streams) * b.C;
+    desc.push_back(d);
+  }
+  if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
+  cp->n_desc = static_cast<int>(desc.size());
+  cp->carry_items = items;
+  if (!desc.empty()) {
+    ck(cudaMalloc(&cp->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
+    ck(cudaMemcpy(cp->d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice),
+       "cudaMemcpy(desc)");
+  }
+  // tensor-core launches (tensor maps depend on the tile geometry and the pending offset)
+  cp->tc.resize(pg.ops.size());
   for (size_t i = 0; i < pg.ops.size(); ++i) {
     const DevOp& d = plan->dops[i];
-    if (d.kernel != KERNEL_TC) continue;
+    if (d.kernel != KERNEL_TC || cp->t_out[i] == 0) continue;
     const ConvOp& op = pg.ops[i];
     const BufferSpec& bi = pg.bufs[op.in_buf];
-    const ConvParams cp = conv_params(i, F);
-    const int64_t Tmax_in = max_frames * bi.rate.num / bi.rate.den;
+    const ConvParams c = conv_params(i, *cp);
     const int S = d.view_S;
+    // window start frame; super-rows are anchored at base_off so that it is S-aligned
+    const int64_t f0 = c.in_f0;
+    const int64_t base_off = f0 % S;
     const uint64_t bufC_view = static_cast<uint64_t>(bi.C) * S;
-    const uint64_t rows_view = static_cast<uint64_t>((bi.cache + Tmax_in) / S);
-    TcParams& p = v[i].p;
+    const int64_t frames_avail = buf_sstride[op.in_buf] / bi.C - base_off;
+    const uint64_t rows_view = static_cast<uint64_t>(frames_avail / S);
+    TcParams& p = cp->tc[i].p;
     p.BN = d.BN;
     p.bf16 = d.bf16 ? 1 : 0;
-    const int t_out = cp.t_out;
+    const int t_out = c.t_out;
     if (t_out >= 128) {
       p.R = 128;
       p.G = 1;
@@ -404,75 +394,189 @@ const std::vector<TcLaunch>& State::tc_for(int64_t F) {
     p.cblocks = d.cin_view_pad / 32;
     p.n_kblocks = d.taps_view * p.cblocks;
     p.a_c0 = S > 1 ? 0 : op.in_off;
-    p.a_row0 = static_cast<int>((bi.cache - op.look) / S);
+    p.a_row0 = static_cast<int>((f0 - base_off) / S);
     p.a_tap_rows = d.tap_rows;
-    p.pre_act = cp.pre_act;
-    p.pre_alpha = cp.pre_alpha;
-    p.post_act = cp.post_act;
-    p.post_alpha = cp.post_alpha;
-    p.gate = cp.gate;
-    p.nout = cp.nout;
+    p.pre_act = c.pre_act;
+    p.pre_alpha = c.pre_alpha;
+    p.post_act = c.post_act;
+    p.post_alpha = c.post_alpha;
+    p.gate = c.gate;
+    p.nout = c.nout;
     p.t_out = t_out;
     p.streams = streams;
-    p.bias = cp.bias;
-    p.out = cp.out;
-    p.out_sstride = cp.out_sstride;
-    p.out_base = cp.out_base;
-    p.out_rstride = cp.out_rstride;
-    p.res = cp.res;
-    p.res_sstride = cp.res_sstride;
-    p.res_fstride = cp.res_fstride;
-    p.res_off = cp.res_off;
-    p.res_f0 = cp.res_f0;
-    p.res_act = cp.res_act;
-    p.res_alpha = cp.res_alpha;
+    p.bias = c.bias;
+    p.out = c.out;
+    p.out_sstride = c.out_sstride;
+    p.out_base = c.out_base;
+    p.out_rstride = c.out_rstride;
+    p.res = c.res;
+    p.res_sstride = c.res_sstride;
+    p.res_fstride = c.res_fstride;
+    p.res_off = c.res_off;
+    p.res_f0 = c.res_f0;
+    p.res_act = c.res_act;
+    p.res_alpha = c.res_alpha;
     {
       const char* dbg = std::getenv("SC_TC_DEBUG");
       p.debug = dbg ? std::atoi(dbg) : 0;
       const char* tr = std::getenv("SC_TC_TRACE_OP");
       if (tr && std::atoi(tr) == static_cast<int>(i)) p.debug |= 32;
     }
-    v[i].map_a = make_map3(buf_base[op.in_buf], bufC_view, rows_view, streams, bufC_view * 4,
-                           static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
-                           static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
+    cp->tc[i].map_a = make_map3(buf_base[op.in_buf] + base_off * bi.C, bufC_view, rows_view, streams,
+                                bufC_view * 4, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
+                                static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
     // output rows start at out_base; rows >= t_out and streams >= n_streams are clipped by TMA
-    v[i].map_out = make_map3(cp.out + cp.out_base, static_cast<uint64_t>(cp.out_rstride),
-                             static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(cp.out_rstride) * 4,
-                             static_cast<uint64_t>(cp.out_sstride) * 4, 32, static_cast<uint32_t>(p.R),
-                             static_cast<uint32_t>(p.G));
-    if (cp.res) {
-      v[i].map_res = make_map3(cp.res + static_cast<int64_t>(cp.res_f0) * cp.res_fstride,
-                               static_cast<uint64_t>(cp.res_fstride), static_cast<uint64_t>(t_out), streams,
-                               static_cast<uint64_t>(cp.res_fstride) * 4,
-                               static_cast<uint64_t>(cp.res_sstride) * 4, 32, static_cast<uint32_t>(p.R),
-                               static_cast<uint32_t>(p.G));
+    cp->tc[i].map_out = make_map3(c.out + c.out_base, static_cast<uint64_t>(c.out_rstride),
+                                  static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(c.out_rstride) * 4,
+                                  static_cast<uint64_t>(c.out_sstride) * 4, 32, static_cast<uint32_t>(p.R),
+                                  static_cast<uint32_t>(p.G));
+    if (c.res) {
+      cp->tc[i].map_res = make_map3(c.res + static_cast<int64_t>(c.res_f0) * c.res_fstride,
+                                    static_cast<uint64_t>(c.res_fstride), static_cast<uint64_t>(t_out), streams,
+                                    static_cast<uint64_t>(c.res_fstride) * 4,
+                                    static_cast<uint64_t>(c.res_sstride) * 4, 32, static_cast<uint32_t>(p.R),
+                                    static_cast<uint32_t>(p.G));
     } else {
-      v[i].map_res = v[i].map_out;  // unused
+      cp->tc[i].map_res = cp->tc[i].map_out;  // unused
     }
   }
-  return tc_launches.emplace(F, std::move(v)).first->second;
+  return *plans.emplace(key, std::move(cp)).first->second;
 }
 
-void State::enqueue(const float* in, float* out, int64_t F, cudaStream_t s, cudaEvent_t* ev) {
+ConvParams State::conv_params(size_t i, const CallPlan& cp) const {
+  const Program& pg = plan->prog;
+  const ConvOp& op = pg.ops[i];
+  const BufferSpec& bi = pg.bufs[op.in_buf];
+  const BufferSpec& bo = pg.bufs[op.out_buf];
+  ConvParams p{};
+  p.in = buf_base[op.in_buf];
+  p.in_sstride = buf_sstride[op.in_buf];
+  p.in_fstride = bi.C;
+  p.in_off = op.in_off;
+  p.cin = op.cin;
+  p.in_f0 = static_cast<int>(cache[op.in_buf] - op.look - cp.pend[i]);
+  p.row_step = op.row_step;
+  p.tap_step = op.tap_step;
+  p.taps = op.taps;
+  p.w = plan->dops[i].w;
+  p.bias = plan->dops[i].bias;
+  p.nout = op.nout;
+  p.out = buf_base[op.out_buf];
+  p.out_sstride = buf_sstride[op.out_buf];
+  p.out_base = cache[op.out_buf] * bo.C;
+  p.out_rstride = op.out_rstride;
+  p.t_out = static_cast<int>(cp.t_out[i]);
+  p.streams = streams;
+  p.pre_act = op.pre_act;
+  p.pre_alpha = op.pre_alpha;
+  p.post_act = op.post_act;
+  p.post_alpha = op.post_alpha;
+  p.gate = op.gate ? 1 : 0;
+  if (op.res_buf >= 0) {
+    const BufferSpec& br = pg.bufs[op.res_buf];
+    p.res = buf_base[op.res_buf];
+    p.res_sstride = buf_sstride[op.res_buf];
+    p.res_fstride = br.C;
+    p.res_off = op.res_off;
+    p.res_f0 = static_cast<int>(cache[op.res_buf] - op.res_delay);
+    p.res_act = op.res_act;
+    p.res_alpha = op.res_alpha;
+  }
+  return p;
+}
+
+IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
+  const Program& pg = plan->prog;
+  IngestArgs a{};
+  a.in = in;
+  a.buf = buf_base[0];
+  a.sstride = buf_sstride[0];
+  a.C = pg.in_C;
+  a.T = static_cast<int>(cp.F);
+  a.cache = static_cast<int>(cache[0]);
+  a.streams = streams;
+  return a;
+}
+
+EgressArgs State::egress_args(float* out, const CallPlan& cp) const {
+  const Program& pg = plan->prog;
+  const BufferSpec& b = pg.bufs[pg.sink_buf];
+  EgressArgs a{};
+  a.buf = buf_base[pg.sink_buf];
+  a.sstride = buf_sstride[pg.sink_buf];
+  a.fstride = b.C;
+  a.off = pg.sink_off;
+  a.C = pg.sink_C;
+  a.T = static_cast<int>(cp.egress_T);
+  a.cache = static_cast<int>(cp.egress_row);
+  a.streams = streams;
+  a.act = pg.sink_act;
+  a.alpha = pg.sink_alpha;
+  a.out = out;
+  return a;
+}
+
+int State::launches(int64_t F) {
+  CallPlan& cp = call_plan(F);
+  int n = 2 + (cp.n_desc > 0 ? 1 : 0);
+  for (int64_t t : cp.t_out) n += t > 0 ? 1 : 0;
+  return n;
+}
+
+std::string State::launch_name(int64_t F, int i) {
+  CallPlan& cp = call_plan(F);
+  int k = 0;
+  if (i == k++) return "ingest";
+  for (size_t j = 0; j < plan->prog.ops.size(); ++j) {
+    if (cp.t_out[j] == 0) continue;
+    if (i == k++) {
+      const ConvOp& op = plan->prog.ops[j];
+      const DevOp& d = plan->dops[j];
+      return "op" + std::to_string(j) + " " + op.name + " [" +
+             (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc") : "simt") + "]";
+    }
+  }
+  if (i == k++) return "egress";
+  if (cp.n_desc > 0 && i == k++) return "carry";
+  return "";
+}
+
+void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, cudaEvent_t* ev) {
   int e = 0;
-  const std::vector<TcLaunch>& tcl = tc_for(F);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
-  launch_ingest(ingest_args(in, F), s);
+  launch_ingest(ingest_args(in, cp), s);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
+    if (cp.t_out[i] == 0) continue;
     if (plan->dops[i].kernel == KERNEL_TC) {
-      launch_conv_tc(tcl[i].map_a, plan->dops[i].map_w, tcl[i].map_out, tcl[i].map_res, tcl[i].p, s);
+      const TcLaunch& t = cp.tc[i];
+      launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
     } else {
-      launch_conv_simt(conv_params(i, F), s);
+      launch_conv_simt(conv_params(i, cp), s);
     }
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
-  launch_egress(egress_args(out, F), s);
+  launch_egress(egress_args(out, cp), s);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
-  if (n_desc > 0) {
-    launch_carry(d_desc, n_desc, streams, carry_items, F, s);
+  if (cp.n_desc > 0) {
+    launch_carry(cp.d_desc, cp.n_desc, streams, cp.carry_items, s);
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
+}
+
+void State::check_frames(int64_t F) const {
+  const Program& pg = plan->prog;
+  if (F <= 0) fail(SC_ERR_INVALID_ARGUMENT, "frames must be positive");
+  if ((F * pg.sink_rate.num) % pg.sink_rate.den != 0)
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO,
+         "buffer length " + std::to_string(F) + " times the sink rate is not an integer");
+  if (F % pg.ratio != 0 && (!phase_mode || pg.ratio % F != 0))
+    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer length " + std::to_string(F) +
+                                                  " is neither a multiple nor a divisor of the compression ratio " +
+                                                  std::to_string(pg.ratio));
+  if (F > max_frames)
+    fail(SC_ERR_INVALID_ARGUMENT, "buffer length " + std::to_string(F) + " exceeds max_frames " +
+                                      std::to_string(max_frames));
 }
 
 void State::profile(const float* in, float* out, int64_t F, int steps, float* ms, cudaStream_t s) {
@@ -482,33 +586,30 @@ void State::profile(const float* in, float* out, int64_t F, int steps, float* ms
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
   const int n = launches(F);
+  for (int i = 0; i < n; ++i) ms[i] = 0.f;
   std::vector<cudaEvent_t> ev(static_cast<size_t>(n + 1) * steps);
   for (auto& e : ev) ck(cudaEventCreate(&e), "EventCreate");
-  for (int k = 0; k < steps; ++k) enqueue(in, out, F, s, ev.data() + static_cast<size_t>(k) * (n + 1));
+  int done = 0;
+  for (int k = 0; k < steps; ++k) {
+    CallPlan& cp = call_plan(F);
+    const bool same = launches(F) == n;
+    enqueue(in, out, cp, s, same ? ev.data() + static_cast<size_t>(k) * (n + 1) : nullptr);
+    advance(F, cp);
+    if (same) ++done;
+  }
   ck(cudaGetLastError(), "launch");
   ck(cudaStreamSynchronize(s), "StreamSynchronize");
-  for (int i = 0; i < n; ++i) ms[i] = 0.f;
-  for (int k = 0; k < steps; ++k)
+  for (int k = 0; k < steps; ++k) {
     for (int i = 0; i < n; ++i) {
       float t = 0.f;
-      ck(cudaEventElapsedTime(&t, ev[static_cast<size_t>(k) * (n + 1) + i],
-                              ev[static_cast<size_t>(k) * (n + 1) + i + 1]),
-         "EventElapsedTime");
-      ms[i] += t / steps;
+      if (cudaEventElapsedTime(&t, ev[static_cast<size_t>(k) * (n + 1) + i],
+                               ev[static_cast<size_t>(k) * (n + 1) + i + 1]) == cudaSuccess && done > 0)
+        ms[i] += t / done;
     }
+  }
+  cudaGetLastError();  // events of skipped steps were never recorded
   for (auto& e : ev) cudaEventDestroy(e);
   ck(cudaSetDevice(prev), "cudaSetDevice");
-}
-
-void State::check_frames(int64_t F) const {
-  if (F <= 0) fail(SC_ERR_INVALID_ARGUMENT, "frames must be positive");
-  if (F % plan->prog.ratio != 0)
-    fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer length " + std::to_string(F) +
-                                                  " is not a multiple of the compression ratio " +
-                                                  std::to_string(plan->prog.ratio));
-  if (F > max_frames)
-    fail(SC_ERR_INVALID_ARGUMENT, "buffer length " + std::to_string(F) + " exceeds max_frames " +
-                                      std::to_string(max_frames));
 }
 
 void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
@@ -517,78 +618,98 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  CallPlan& cp = call_plan(F);
   if (!use_graphs) {
-    enqueue(in, out, F, s, nullptr);
+    enqueue(in, out, cp, s, nullptr);
     ck(cudaGetLastError(), "launch");
-    ck(cudaSetDevice(prev), "cudaSetDevice");
-    return;
-  }
-  const auto key = std::make_tuple(F, in, out);
-  auto it = graphs.find(key);
-  if (it == graphs.end()) {
-    // reuse the least recently used graph of this length once 8 pointer pairs exist
-    int same = 0;
-    auto lru = graphs.end();
-    for (auto jt = graphs.begin(); jt != graphs.end(); ++jt) {
-      if (std::get<0>(jt->first) != F) continue;
-      ++same;
-      if (lru == graphs.end() || jt->second.last_use < lru->second.last_use) lru = jt;
-    }
-    GraphEntry g;
-    if (same >= 8) {
-      g = lru->second;
-      graphs.erase(lru);
-      g.ia = ingest_args(in, F);
-      g.ea = egress_args(out, F);
-      void* a1[] = {&g.ia};
-      cudaKernelNodeParams kp = g.ingest_params;
-      kp.kernelParams = a1;
-      kp.extra = nullptr;
-      ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
-      void* a2[] = {&g.ea};
-      kp = g.egress_params;
-      kp.kernelParams = a2;
-      kp.extra = nullptr;
-      ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
-    } else {
-      ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
-      enqueue(in, out, F, capture_stream, nullptr);
-      cudaError_t le = cudaGetLastError();
-      cudaGraph_t graph = nullptr;
-      cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);
-      ck(le, "launch (capture)");
-      ck(ee, "EndCapture");
-      g.graph = graph;
-      size_t n = 0;
-      ck(cudaGraphGetNodes(graph, nullptr, &n), "GraphGetNodes");
-      std::vector<cudaGraphNode_t> nodes(n);
-      ck(cudaGraphGetNodes(graph, nodes.data(), &n), "GraphGetNodes");
-      for (cudaGraphNode_t nd : nodes) {
-        cudaGraphNodeType ty;
-        ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
-        if (ty != cudaGraphNodeTypeKernel) continue;
-        cudaKernelNodeParams kp;
-        ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-        if (kp.func == ingest_kernel_ptr()) {
-          g.ingest_node = nd;
-          g.ingest_params = kp;
-        } else if (kp.func == egress_kernel_ptr()) {
-          g.egress_node = nd;
-          g.egress_params = kp;
+  } else {
+    const auto key = std::make_pair(in, out);
+    auto it = cp.graphs.find(key);
+    if (it == cp.graphs.end()) {
+      // reuse the least recently used graph once 8 pointer pairs exist
+      GraphEntry g;
+      if (cp.graphs.size() >= 8) {
+        auto lru = cp.graphs.begin();
+        for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
+          if (jt->second.last_use < lru->second.last_use) lru = jt;
+        g = lru->second;
+        cp.graphs.erase(lru);
+        g.ia = ingest_args(in, cp);
+        g.ea = egress_args(out, cp);
+        void* a1[] = {&g.ia};
+        cudaKernelNodeParams kp = g.ingest_params;
+        kp.kernelParams = a1;
+        kp.extra = nullptr;
+        ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
+        void* a2[] = {&g.ea};
+        kp = g.egress_params;
+        kp.kernelParams = a2;
+        kp.extra = nullptr;
+        ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
+      } else {
+        ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+        enqueue(in, out, cp, capture_stream, nullptr);
+        cudaError_t le = cudaGetLastError();
+        cudaGraph_t graph = nullptr;
+        cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);
+        ck(le, "launch (capture)");
+        ck(ee, "EndCapture");
+        g.graph = graph;
+        size_t n = 0;
+        ck(cudaGraphGetNodes(graph, nullptr, &n), "GraphGetNodes");
+        std::vector<cudaGraphNode_t> nodes(n);
+        ck(cudaGraphGetNodes(graph, nodes.data(), &n), "GraphGetNodes");
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType ty;
+          ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
+          if (ty != cudaGraphNodeTypeKernel) continue;
+          cudaKernelNodeParams kp;
+          ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
+          if (kp.func == ingest_kernel_ptr()) {
+            g.ingest_node = nd;
+            g.ingest_params = kp;
+          } else if (kp.func == egress_kernel_ptr()) {
+            g.egress_node = nd;
+            g.egress_params = kp;
+          }
         }
+        if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
+        ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
+        ck(cudaGraphUpload(g.exec, s), "GraphUpload");
+        g.ia = ingest_args(in, cp);
+        g.ea = egress_args(out, cp);
       }
-      if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
-      ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
-      ck(cudaGraphUpload(g.exec, s), "GraphUpload");
-      g.ia = ingest_args(in, F);
-      g.ea = egress_args(out, F);
+      it = cp.graphs.emplace(key, g).first;
     }
-    it = graphs.emplace(key, g).first;
+    it->second.last_use = ++use_clock;
+    ck(cudaGraphLaunch(it->second.exec, s), "GraphLaunch");
   }
-  GraphEntry& g = it->second;
-  g.last_use = ++use_clock;
-  ck(cudaGraphLaunch(g.exec, s), "GraphLaunch");
+  advance(F, cp);
   ck(cudaSetDevice(prev), "cudaSetDevice");
+}
+
+// Sink lag for a constant buffer length F from the current position: the largest shortfall
+// E_k - N_sink_k over one period of calls (0 when F is a multiple of the ratio).
+int64_t State::lag_for(int64_t F) const {
+  const Program& pg = plan->prog;
+  const int64_t Fs = F * pg.sink_rate.num / pg.sink_rate.den;
+  int64_t P = pg.ratio / std::__gcd(F, pg.ratio);
+  State* self = const_cast<State*>(this);
+  const std::vector<int64_t> saveN = N;
+  int64_t e = E, lag = 0;
+  for (int64_t k = 0; k < P; ++k) {
+    self->N = next_counts(F);
+    e += Fs;
+    lag = std::max(lag, e - N[pg.sink_buf]);
+  }
+  self->N = saveN;
+  return lag;
+}
+
+void State::advance(int64_t F, const CallPlan& cp) {
+  if (D < 0) D = lag_for(F);
+  N = next_counts(F);
+  E += cp.egress_T;
 }
 
 void State::reset(const int* ids, int n_ids, cudaStream_t s) {
@@ -597,6 +718,9 @@ void State::reset(const int* ids, int n_ids, cudaStream_t s) {
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
   if (!ids) {
     ck(cudaMemsetAsync(mem, 0, mem_bytes, s), "cudaMemsetAsync");
+    std::fill(N.begin(), N.end(), 0);
+    E = 0;
+    D = -1;
   } else {
     if (n_ids < 0 || n_ids > streams) fail(SC_ERR_INVALID_ARGUMENT, "bad id count");
     for (int i = 0; i < n_ids; ++i)

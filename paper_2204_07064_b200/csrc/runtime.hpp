@@ -57,6 +57,23 @@ struct TcLaunch {
   TcParams p{};
 };
 
+// One call's launch geometry.  Calls whose buffer length F is a multiple of the compression
+// ratio all share one CallPlan; shorter buffers cycle through a period of CallPlans (phase
+// state: a layer fires only when its input holds enough new frames).
+struct CallPlan {
+  int64_t F = 0;
+  std::vector<int64_t> T;     // new frames per buffer this call
+  std::vector<int64_t> pend;  // per op: input frames pending (not yet consumed) before the call
+  std::vector<int64_t> t_out; // per op: output rows this call (0: op skipped)
+  int64_t egress_row = 0;     // first sink-buffer row emitted this call
+  int64_t egress_T = 0;       // sink frames emitted this call
+  BufDesc* d_desc = nullptr;  // carry table (per-buffer shift T)
+  int n_desc = 0;
+  int64_t carry_items = 0;
+  std::vector<TcLaunch> tc;
+  std::map<std::pair<const float*, float*>, GraphEntry> graphs;
+};
+
 struct State {
   const Plan* plan = nullptr;
   int streams = 0;
@@ -66,27 +83,34 @@ struct State {
   int64_t cache_bytes_per_stream = 0;
   std::vector<float*> buf_base;
   std::vector<int64_t> buf_sstride;
-  BufDesc* d_desc = nullptr;
+  BufDesc* d_desc = nullptr;  // reset table (all cached buffers)
   int n_desc = 0;
-  int64_t carry_items = 0, reset_items = 0;
+  int64_t reset_items = 0;
   int* d_ids = nullptr;
   bool use_graphs = true;
   cudaStream_t capture_stream = nullptr;
-  // graphs keyed by (frames, in, out): replaying a graph whose I/O pointers match needs no
-  // parameter update (an updated exec graph is re-uploaded on its next launch)
-  std::map<std::tuple<int64_t, const float*, float*>, GraphEntry> graphs;
   uint64_t use_clock = 0;
-  std::map<int64_t, std::vector<TcLaunch>> tc_launches;  // per call length, per op
+  // stream position (all streams advance in lockstep)
+  std::vector<int64_t> N;     // cumulative frames written per buffer
+  int64_t E = 0;              // cumulative sink frames emitted
+  int64_t D = -1;             // sink lag in sink frames (fixed by the first call after reset)
+  std::map<std::vector<int64_t>, std::unique_ptr<CallPlan>> plans;
+  bool phase_mode = false;     // created for buffers shorter than the compression ratio
+  std::vector<int64_t> cache;  // per-buffer cache frames of this state
 
-  ConvParams conv_params(size_t op, int64_t frames) const;
-  const std::vector<TcLaunch>& tc_for(int64_t frames);
-  IngestArgs ingest_args(const float* in, int64_t frames) const;
-  EgressArgs egress_args(float* out, int64_t frames) const;
+  int64_t lag_for(int64_t F) const;
+  void advance(int64_t F, const CallPlan& cp);
+
+  std::vector<int64_t> next_counts(int64_t F) const;
+  CallPlan& call_plan(int64_t F);
+  ConvParams conv_params(size_t op, const CallPlan& cp) const;
+  IngestArgs ingest_args(const float* in, const CallPlan& cp) const;
+  EgressArgs egress_args(float* out, const CallPlan& cp) const;
   void check_frames(int64_t frames) const;
-  void enqueue(const float* in, float* out, int64_t frames, cudaStream_t s, cudaEvent_t* ev);
+  void enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, cudaEvent_t* ev);
   void profile(const float* in, float* out, int64_t frames, int steps, float* ms, cudaStream_t s);
-  int launches(int64_t frames) const;
-  std::string launch_name(int64_t frames, int i) const;
+  int launches(int64_t frames);
+  std::string launch_name(int64_t frames, int i);
   void process(const float* in, float* out, int64_t frames, cudaStream_t s);
   void reset(const int* ids, int n_ids, cudaStream_t s);
   ~State();
