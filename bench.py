@@ -287,10 +287,16 @@ def main():
         oi = int(dom_name.split()[0][2:])
         flops = 2.0 * op_macs[oi] * frames * streams
         achieved = flops / (dom_ms / 1e3) / 1e12
+        # the fp32-accurate path issues 3 tf32 MMAs per product at half the bf16 rate:
+        # its tensor-core ceiling is peak_bf16 / 6 (algorithmic FLOPs)
+        ceil = pk["bf16"] / 6.0 if (args.precision == "fp32" and "[tc]" in dom_name) else pk["bf16"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16"], "traffic": None, "kernel": dom_name,
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms_prof,
                 "peak_source": f"{pk['src']} bf16 dense (burst; MEASURED_PEAKS.json)",
+                "path_ceiling": ceil, "frac_of_path_ceiling": achieved / ceil,
+                "path_ceiling_note": "3xTF32 = 3 tf32 MMAs (half bf16 rate) per fp32 product"
+                if ceil != pk["bf16"] else "bf16 kind::f16 MMA",
                 "flops_per_launch": flops}
         tfile = ROOT / "profiles" / "traffic.json"
         if tfile.exists():

@@ -1,0 +1,229 @@
+// streamconv_b200.hpp — C++ cached-module API over the C-ABI (header-only).
+//
+// The host-side mirror of the reference's streaming interface: cached modules (SPEC.md
+// graph_ir node kinds) are appended to a Sequential stack, compiled into a
+// Plan (causalize) and run for a batch of independent streams
+// (stream_runtime).  Errors are rethrown as streamconv::b200::Error carrying
+// the reference ErrCode name (error.hpp:8-70).
+//
+//   streamconv::b200::Sequential m(128);
+//   m.residual([](auto& br) { br.leaky_relu(0.2f).conv(CachedConv1d{128, 128, 3, 1, 9}); });
+//   streamconv::b200::Plan plan(m);                 // device 0
+//   streamconv::b200::StreamBatch st(plan, 256, 2048);
+//   st.process_buffer(d_in, d_out, 2048, stream);
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "streamconv_b200.h"
+
+namespace streamconv {
+namespace b200 {
+
+class Error : public std::runtime_error {
+ public:
+  Error(int status, const std::string& msg) : std::runtime_error(msg), status_(status) {}
+  int status() const noexcept { return status_; }
+  std::string code() const { return sc_status_name(status_); }  // e.g. "ChannelMismatch"
+
+ private:
+  int status_;
+};
+
+inline void check(int st) {
+  if (st != SC_OK) throw Error(st, sc_last_error());
+}
+
+// ---- cached modules -------------------------------------------------------------------
+// Padding: {-1, -1} selects the centered (non-causal, trained) padding; the plan causalizes.
+struct PaddingSpec {
+  int64_t left = -1, right = -1;
+};
+
+struct CachedConv1d {  // conv1d(pad(x,(L,R)), k, stride, dilation)   kernels.cpp:73-104
+  int in_channels, out_channels, taps, stride = 1, dilation = 1;
+  PaddingSpec padding{};
+  std::vector<float> weights;  // [n][m][k] (tensor.hpp:52-88); empty = zeros
+  std::vector<float> bias;     // [n]; empty = zeros
+};
+
+struct CachedConvTranspose1d {  // zero_upsample(stride) + conv1d
+  int in_channels, out_channels, taps, stride;
+  PaddingSpec padding{};
+  std::vector<float> weights;  // conv-form kernel [n][m][k]
+  std::vector<float> bias;
+};
+
+class Sequential {
+ public:
+  explicit Sequential(int in_channels) : in_channels_(in_channels), channels_(in_channels) {}
+
+  int in_channels() const { return in_channels_; }
+  int channels() const { return channels_; }
+  const std::vector<sc_node>& nodes() const { return nodes_; }
+  const std::vector<float>& weights() const { return weights_; }
+
+  Sequential& conv(const CachedConv1d& c) {
+    PaddingSpec p = c.padding;
+    if (p.left < 0) {
+      const int64_t tot = c.stride == 1 ? static_cast<int64_t>(c.taps - 1) * c.dilation : c.taps - 1;
+      p = {(tot + 1) / 2, tot / 2};
+    }
+    sc_node n = base(SC_NODE_CONV);
+    n.in_channels = c.in_channels;
+    n.out_channels = c.out_channels;
+    n.taps = c.taps;
+    n.stride = c.stride;
+    n.dilation = c.dilation;
+    n.pad_left = p.left;
+    n.pad_right = p.right;
+    n.weight_offset = add_weights(c.weights, c.bias, c.out_channels, c.in_channels, c.taps);
+    nodes_.push_back(n);
+    channels_ = c.out_channels;
+    return *this;
+  }
+
+  Sequential& conv_transpose(const CachedConvTranspose1d& c) {
+    PaddingSpec p = c.padding;
+    if (p.left < 0) p = {c.taps / 2, (c.taps - 1) / 2};
+    sc_node n = base(SC_NODE_CONVT);
+    n.in_channels = c.in_channels;
+    n.out_channels = c.out_channels;
+    n.taps = c.taps;
+    n.stride = c.stride;
+    n.pad_left = p.left;
+    n.pad_right = p.right;
+    n.weight_offset = add_weights(c.weights, c.bias, c.out_channels, c.in_channels, c.taps);
+    nodes_.push_back(n);
+    channels_ = c.out_channels;
+    return *this;
+  }
+
+  // activation (kernels.cpp:119-128); the reference default alpha is 0.01f (kernels.hpp:32)
+  Sequential& leaky_relu(float alpha = 0.01f) { return act(SC_ACT_LEAKY_RELU, alpha); }
+  Sequential& tanh() { return act(SC_ACT_TANH, 0.f); }
+
+  // Fanout -> branch -> Sum(branch, Delay_A(skip)), A from branch_alignment
+  Sequential& residual(const std::function<void(Sequential&)>& branch) {
+    nodes_.push_back(base(SC_NODE_RES_BEGIN));
+    const int c0 = channels_;
+    branch(*this);
+    if (channels_ != c0) throw Error(SC_ERR_CHANNEL_MISMATCH, "ChannelMismatch: residual branch changes channels");
+    nodes_.push_back(base(SC_NODE_RES_END));
+    return *this;
+  }
+
+  Sequential& gate() {  // y = tanh(x[:C/2]) * sigmoid(x[C/2:])
+    nodes_.push_back(base(SC_NODE_GATE));
+    channels_ /= 2;
+    return *this;
+  }
+
+  Sequential& slice(int begin, int count) {
+    sc_node n = base(SC_NODE_SLICE);
+    n.slice_begin = begin;
+    n.slice_count = count;
+    nodes_.push_back(n);
+    channels_ = count;
+    return *this;
+  }
+
+  // PQMF analysis / synthesis (builder-defined, sc_pqmf_filters)
+  Sequential& pqmf_analysis(int bands = 16, int taps = 256) {
+    std::vector<float> ana(static_cast<size_t>(bands) * taps + bands), syn(static_cast<size_t>(bands) * taps + 1);
+    check(sc_pqmf_filters(bands, taps, ana.data(), syn.data(), nullptr));
+    CachedConv1d c{1, bands, taps, bands, 1, {taps - bands, 0}, {}, {}};
+    c.weights.assign(ana.begin(), ana.begin() + static_cast<size_t>(bands) * taps);
+    c.bias.assign(bands, 0.f);
+    return conv(c);
+  }
+  Sequential& pqmf_synthesis(int bands = 16, int taps = 256) {
+    std::vector<float> ana(static_cast<size_t>(bands) * taps + bands), syn(static_cast<size_t>(bands) * taps + 1);
+    check(sc_pqmf_filters(bands, taps, ana.data(), syn.data(), nullptr));
+    CachedConvTranspose1d c{bands, 1, taps, bands, {taps - 1, 0}, {}, {}};
+    c.weights.assign(syn.begin(), syn.begin() + static_cast<size_t>(bands) * taps);
+    c.bias.assign(1, 0.f);
+    return conv_transpose(c);
+  }
+
+ private:
+  static sc_node base(int kind) {
+    sc_node n{};
+    n.kind = kind;
+    n.stride = 1;
+    n.dilation = 1;
+    return n;
+  }
+  Sequential& act(int kind, float alpha) {
+    sc_node n = base(SC_NODE_ACT);
+    n.act = kind;
+    n.alpha = alpha;
+    nodes_.push_back(n);
+    return *this;
+  }
+  int64_t add_weights(const std::vector<float>& w, const std::vector<float>& b, int N, int M, int K) {
+    const int64_t off = static_cast<int64_t>(weights_.size());
+    const size_t nw = static_cast<size_t>(N) * M * K;
+    if (!w.empty() && w.size() != nw)
+      throw Error(SC_ERR_INVALID_ARGUMENT, "InvalidArgument: kernel weight count does not match shape");
+    if (!b.empty() && b.size() != static_cast<size_t>(N))
+      throw Error(SC_ERR_INVALID_ARGUMENT, "InvalidArgument: kernel bias count does not match out_channels");
+    if (w.empty()) weights_.resize(weights_.size() + nw, 0.f); else weights_.insert(weights_.end(), w.begin(), w.end());
+    if (b.empty()) weights_.resize(weights_.size() + N, 0.f); else weights_.insert(weights_.end(), b.begin(), b.end());
+    return off;
+  }
+
+  int in_channels_, channels_;
+  std::vector<sc_node> nodes_;
+  std::vector<float> weights_;
+};
+
+// ---- plan + stream batch --------------------------------------------------------------
+class Plan {
+ public:
+  explicit Plan(const Sequential& m, int device = 0, int precision = SC_PREC_FP32) {
+    check(sc_plan_create(m.nodes().data(), static_cast<int32_t>(m.nodes().size()), m.weights().data(),
+                         static_cast<int64_t>(m.weights().size()), m.in_channels(), precision, device, &p_));
+  }
+  ~Plan() { sc_plan_destroy(p_); }
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  int64_t ratio() const { int64_t r = 0; check(sc_plan_ratio(p_, &r)); return r; }
+  int64_t latency() const { int64_t r = 0; check(sc_plan_latency(p_, &r)); return r; }
+  int64_t state_bytes() const { int64_t r = 0; check(sc_plan_state_bytes(p_, &r)); return r; }
+  void sink(int64_t* num, int64_t* den, int32_t* channels) const { check(sc_plan_sink_rate(p_, num, den, channels)); }
+  const sc_plan* get() const { return p_; }
+
+ private:
+  sc_plan* p_ = nullptr;
+};
+
+class StreamBatch {  // StreamState for n independent streams
+ public:
+  StreamBatch(const Plan& plan, int n_streams, int64_t max_frames) {
+    check(sc_state_create(plan.get(), n_streams, max_frames, &s_));
+  }
+  ~StreamBatch() { sc_state_destroy(s_); }
+  StreamBatch(const StreamBatch&) = delete;
+  StreamBatch& operator=(const StreamBatch&) = delete;
+
+  // process_buffer for every stream; device pointers, async on `stream`
+  void process_buffer(const float* d_in, float* d_out, int64_t frames, void* stream = nullptr) {
+    check(sc_process(s_, d_in, d_out, frames, stream));
+  }
+  void reset(void* stream = nullptr) { check(sc_state_reset(s_, nullptr, 0, stream)); }
+  void reset(const std::vector<int32_t>& ids, void* stream = nullptr) {
+    check(sc_state_reset(s_, ids.data(), static_cast<int32_t>(ids.size()), stream));
+  }
+
+ private:
+  sc_state* s_ = nullptr;
+};
+
+}  // namespace b200
+}  // namespace streamconv

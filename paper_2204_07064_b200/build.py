@@ -66,6 +66,26 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
+CPP_TEST = ROOT / "tests" / "cpp" / "test_modules.cpp"
+CPP_BIN = OBJ / "test_modules"
+
+
+def build_cpp_tests(verbose: bool = False) -> Path:
+    """The C++ cached-module API test (include/streamconv_b200.hpp), linked to the library."""
+    if CPP_BIN.exists() and CPP_BIN.stat().st_mtime >= max(CPP_TEST.stat().st_mtime, LIB.stat().st_mtime,
+                                                            _headers_mtime()):
+        return CPP_BIN
+    cmd = ["/usr/bin/g++", "-std=c++17", "-O2", "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
+           str(CPP_TEST), "-o", str(CPP_BIN), "-L", str(LIB.parent), "-lstreamconv_b200",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN/../lib", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
+    return CPP_BIN
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Test infrastructure: oracle/build/liboracle.so and (when /root/reference exists)
     oracle/_ref/libref_streamconv.so.  Never linked into the library above."""
@@ -78,4 +98,5 @@ def build_oracle(verbose: bool = False) -> None:
 
 if __name__ == "__main__":
     print(build(verbose=True))
+    build_cpp_tests(verbose=True)
     build_oracle(verbose=True)

@@ -20,6 +20,7 @@ def built():
     from paper_2204_07064_b200 import build as B
     if os.environ.get("SC_SKIP_BUILD") != "1":
         B.build()
+        B.build_cpp_tests()
         B.build_oracle()
     return True
 

@@ -220,3 +220,12 @@ def test_phase_state_short_buffers(cfg, B):
     assert np.all(y_gpu[..., :D] == 0.0)
     err, rms = rel_err(y_gpu[..., D:], y_ref[..., :total - D])
     assert err <= FP32_TOL, f"cfg{cfg} B={B}: {err:.3e}"
+
+
+@pytest.mark.gpu
+def test_cpp_cached_module_api_gpu():
+    """The C++ API streams a residual stack; split buffers are bit-identical to one buffer."""
+    import subprocess
+    from paper_2204_07064_b200 import build as B
+    r = subprocess.run([str(B.CPP_BIN), "gpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "OK gpu" in r.stdout, r.stdout + r.stderr

@@ -135,3 +135,12 @@ def test_pqmf_filters_design():
     k = 3
     hk = 2 * h * np.cos((2 * k + 1) * np.pi / 32 * (n - 127.5) + (-1) ** k * np.pi / 4)
     np.testing.assert_allclose(ana[k * 256:(k + 1) * 256], hk[::-1].astype(np.float32), atol=1e-7)
+
+
+def test_cpp_cached_module_api_host():
+    """include/streamconv_b200.hpp (C++ cached-module API) builds plans host-only."""
+    import subprocess
+    from paper_2204_07064_b200 import build as B
+    exe = B.build_cpp_tests()
+    r = subprocess.run([str(exe), "host"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "OK host" in r.stdout, r.stdout + r.stderr
