@@ -159,6 +159,16 @@ SC_API int sc_state_cache_bytes(const sc_state* state, int64_t* bytes_per_stream
  * frames must be a positive multiple of sc_plan_ratio and <= max_frames.  Asynchronous on
  * `stream`; the steady-state launch sequence is replayed from a cached CUDA graph.        */
 SC_API int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t frames, void* stream);
+/* Same call with HOST buffers (the reference's process_buffer takes host SignalTensors):
+ * h_in / h_out as above but in host memory — pinned (cudaHostAlloc/cudaHostRegister) for
+ * asynchronous copies.  The H2D copy, the compute and the D2H copy run on three internal
+ * streams with two device slots, so consecutive calls overlap each other's transfers.  The
+ * H2D is ordered after the work already queued on `stream`; call sc_process_host_wait to
+ * order `stream` after the last call's D2H (then synchronize it before reading h_out).  As
+ * with cudaMemcpyAsync, h_in must not be overwritten before its copy has run.            */
+SC_API int sc_process_host(sc_state* state, const float* h_in, float* h_out, int64_t frames,
+                           void* stream);
+SC_API int sc_process_host_wait(sc_state* state, void* stream);
 /* Number of kernels one sc_process launches (for launch accounting). */
 SC_API int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n);
 /* Measurement: run `steps` calls WITHOUT graph replay with CUDA events between launches;

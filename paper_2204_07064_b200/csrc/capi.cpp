@@ -191,6 +191,20 @@ int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t frames,
   });
 }
 
+int sc_process_host(sc_state* state, const float* h_in, float* h_out, int64_t frames, void* stream) {
+  return guard([&] {
+    need(state != nullptr, "null state");
+    state->s->process_host(h_in, h_out, frames, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sc_process_host_wait(sc_state* state, void* stream) {
+  return guard([&] {
+    need(state != nullptr, "null state");
+    state->s->host_wait(static_cast<cudaStream_t>(stream));
+  });
+}
+
 int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n) {
   return guard([&] {
     need(state && n, "null argument");

@@ -212,6 +212,17 @@ State::~State() {
     if (kv.second->d_desc) cudaFree(kv.second->d_desc);
   }
   if (capture_stream) cudaStreamDestroy(capture_stream);
+  for (int k = 0; k < 2; ++k) {
+    if (io_in[k]) cudaFree(io_in[k]);
+    if (io_out[k]) cudaFree(io_out[k]);
+    if (ev_entry[k]) cudaEventDestroy(ev_entry[k]);
+    if (ev_h2d[k]) cudaEventDestroy(ev_h2d[k]);
+    if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
+    if (ev_d2h[k]) cudaEventDestroy(ev_d2h[k]);
+  }
+  if (s_h2d) cudaStreamDestroy(s_h2d);
+  if (s_comp) cudaStreamDestroy(s_comp);
+  if (s_d2h) cudaStreamDestroy(s_d2h);
   if (mem) cudaFree(mem);
   if (d_desc) cudaFree(d_desc);
   if (d_ids) cudaFree(d_ids);
@@ -685,6 +696,65 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
     ck(cudaGraphLaunch(it->second.exec, s), "GraphLaunch");
   }
   advance(F, cp);
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+}
+
+// Host-buffer call: the step's input is copied H2D on its own stream, processed on the
+// state's compute stream and copied back D2H on a third stream, with two device slots so
+// call k+1's H2D and call k-1's D2H overlap call k's compute.  The H2D is ordered after the
+// work already on `s` (entry event); host_wait(s) orders `s` after the last call's D2H.
+void State::process_host(const float* h_in, float* h_out, int64_t F, cudaStream_t s) {
+  check_frames(F);
+  if (!h_in || !h_out) fail(SC_ERR_INVALID_ARGUMENT, "null host pointer");
+  const Program& pg = plan->prog;
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  const int64_t in_f = static_cast<int64_t>(streams) * pg.in_C * max_frames;
+  const int64_t out_f = static_cast<int64_t>(streams) * pg.sink_C * (max_frames * pg.sink_rate.num / pg.sink_rate.den);
+  if (!s_comp) {
+    ck(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaMalloc(&io_in[k], sizeof(float) * in_f), "cudaMalloc(io)");
+      ck(cudaMalloc(&io_out[k], sizeof(float) * std::max<int64_t>(out_f, 1)), "cudaMalloc(io)");
+      ck(cudaEventCreateWithFlags(&ev_entry[k], cudaEventDisableTiming), "EventCreate");
+      ck(cudaEventCreateWithFlags(&ev_h2d[k], cudaEventDisableTiming), "EventCreate");
+      ck(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming), "EventCreate");
+      ck(cudaEventCreateWithFlags(&ev_d2h[k], cudaEventDisableTiming), "EventCreate");
+    }
+    io_in_floats = in_f;
+    io_out_floats = out_f;
+  }
+  const int k = static_cast<int>(host_calls & 1);
+  const size_t in_bytes = sizeof(float) * static_cast<size_t>(streams) * pg.in_C * F;
+  const size_t out_bytes =
+      sizeof(float) * static_cast<size_t>(streams) * pg.sink_C * (F * pg.sink_rate.num / pg.sink_rate.den);
+  ck(cudaEventRecord(ev_entry[k], s), "EventRecord");
+  ck(cudaStreamWaitEvent(s_h2d, ev_entry[k], 0), "StreamWaitEvent");
+  if (host_calls >= 2) ck(cudaStreamWaitEvent(s_h2d, ev_comp[k], 0), "StreamWaitEvent");  // slot k read
+  ck(cudaMemcpyAsync(io_in[k], h_in, in_bytes, cudaMemcpyHostToDevice, s_h2d), "H2D");
+  ck(cudaEventRecord(ev_h2d[k], s_h2d), "EventRecord");
+  ck(cudaStreamWaitEvent(s_comp, ev_h2d[k], 0), "StreamWaitEvent");
+  if (host_calls >= 2) ck(cudaStreamWaitEvent(s_comp, ev_d2h[k], 0), "StreamWaitEvent");  // slot k drained
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+  process(io_in[k], io_out[k], F, s_comp);
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  ck(cudaEventRecord(ev_comp[k], s_comp), "EventRecord");
+  ck(cudaStreamWaitEvent(s_d2h, ev_comp[k], 0), "StreamWaitEvent");
+  ck(cudaMemcpyAsync(h_out, io_out[k], out_bytes, cudaMemcpyDeviceToHost, s_d2h), "D2H");
+  ck(cudaEventRecord(ev_d2h[k], s_d2h), "EventRecord");
+  ++host_calls;
+  ck(cudaSetDevice(prev), "cudaSetDevice");
+}
+
+void State::host_wait(cudaStream_t s) {
+  if (host_calls == 0) return;
+  int prev = 0;
+  ck(cudaGetDevice(&prev), "cudaGetDevice");
+  ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  ck(cudaStreamWaitEvent(s, ev_d2h[(host_calls - 1) & 1], 0), "StreamWaitEvent");
   ck(cudaSetDevice(prev), "cudaSetDevice");
 }
 

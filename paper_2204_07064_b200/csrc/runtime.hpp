@@ -112,6 +112,15 @@ struct State {
   int launches(int64_t frames);
   std::string launch_name(int64_t frames, int i);
   void process(const float* in, float* out, int64_t frames, cudaStream_t s);
+  // host-buffer path: H2D / compute / D2H on three streams, double-buffered across calls
+  void process_host(const float* h_in, float* h_out, int64_t frames, cudaStream_t s);
+  void host_wait(cudaStream_t s);
+  float* io_in[2] = {nullptr, nullptr};
+  float* io_out[2] = {nullptr, nullptr};
+  int64_t io_in_floats = 0, io_out_floats = 0;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_entry[2] = {}, ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  int64_t host_calls = 0;
   void reset(const int* ids, int n_ids, cudaStream_t s);
   ~State();
 };

@@ -27,6 +27,14 @@ def _stream_handle(stream) -> int:
     return int(stream)
 
 
+def _hptr(t) -> int:
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return int(t)
+
+
 def _ptr(t) -> int:
     if hasattr(t, "data_ptr"):
         return t.data_ptr()
@@ -125,6 +133,16 @@ class StreamState:
         """x: device [n_streams][in_C][frames] fp32, y: device [n_streams][out_C][out_frames]."""
         check(lib().sc_process(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
                                C.c_void_p(_stream_handle(stream))))
+
+    def process_host(self, x, y, frames: int, stream=None) -> None:
+        """Host-buffer process_buffer (pinned host memory for overlap): x/y host arrays or
+        pinned torch CPU tensors with the same layouts as process_buffer."""
+        check(lib().sc_process_host(self._h, C.c_void_p(_hptr(x)), C.c_void_p(_hptr(y)), frames,
+                                    C.c_void_p(_stream_handle(stream))))
+
+    def host_wait(self, stream=None) -> None:
+        """Order `stream` after the last process_host call's device->host copy."""
+        check(lib().sc_process_host_wait(self._h, C.c_void_p(_stream_handle(stream))))
 
     def reset(self, stream_ids=None, stream=None) -> None:
         if stream_ids is None:

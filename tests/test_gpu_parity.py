@@ -229,3 +229,22 @@ def test_cpp_cached_module_api_gpu():
     from paper_2204_07064_b200 import build as B
     r = subprocess.run([str(B.CPP_BIN), "gpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "OK gpu" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_process_host_matches_device():
+    """sc_process_host (pinned host buffers, pipelined copies) == sc_process on device."""
+    m = configs.build(3, seed=9)
+    x = configs.batch_input(3, range(3), 16, 512 * 4, seed=9)
+    y_dev, plan, _ = run_gpu(m, x, [512] * 4)
+    st = StreamState(plan, 3, 512)
+    outs = []
+    hy = [torch.empty((3, 16, 512)).pin_memory() for _ in range(4)]
+    for k in range(4):
+        hx = torch.from_numpy(np.ascontiguousarray(x[:, :, 512 * k:512 * (k + 1)])).pin_memory()
+        st.process_host(hx, hy[k], 512)
+        outs.append(hy[k])
+    st.host_wait()
+    torch.cuda.synchronize()
+    y_host = torch.cat(outs, 2).numpy()
+    assert np.array_equal(y_host, y_dev)
