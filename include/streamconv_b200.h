@@ -94,7 +94,14 @@ typedef struct sc_node {
   int64_t weight_offset; /* CONV/CONVT: float offset of weights[N][M][K] then bias[N] */
   int32_t slice_begin;   /* SLICE */
   int32_t slice_count;   /* SLICE */
+  int32_t hint;          /* enum sc_hint: structure the planner may exploit (verified) */
 } sc_node;
+
+/* Planner hints.  SC_HINT_PQMF marks a CONV / CONVT node whose weights are a cosine-modulated
+ * filter bank (sc_pqmf_filters): the plan factors them into the polyphase + modulation form
+ * (5x fewer MACs) after checking the factorisation reproduces every weight to 1e-6, and
+ * otherwise runs the node as a generic conv.  Results are unaffected beyond fp32 rounding. */
+enum sc_hint { SC_HINT_NONE = 0, SC_HINT_PQMF = 1 };
 
 /* arithmetic variants of the dense path */
 enum sc_precision {

@@ -139,7 +139,9 @@ class Sequential {
     CachedConv1d c{1, bands, taps, bands, 1, {taps - bands, 0}, {}, {}};
     c.weights.assign(ana.begin(), ana.begin() + static_cast<size_t>(bands) * taps);
     c.bias.assign(bands, 0.f);
-    return conv(c);
+    conv(c);
+    nodes_.back().hint = SC_HINT_PQMF;
+    return *this;
   }
   Sequential& pqmf_synthesis(int bands = 16, int taps = 256) {
     std::vector<float> ana(static_cast<size_t>(bands) * taps + bands), syn(static_cast<size_t>(bands) * taps + 1);
@@ -147,7 +149,9 @@ class Sequential {
     CachedConvTranspose1d c{bands, 1, taps, bands, {taps - 1, 0}, {}, {}};
     c.weights.assign(syn.begin(), syn.begin() + static_cast<size_t>(bands) * taps);
     c.bias.assign(1, 0.f);
-    return conv_transpose(c);
+    conv_transpose(c);
+    nodes_.back().hint = SC_HINT_PQMF;
+    return *this;
   }
 
  private:

@@ -23,6 +23,7 @@ ERR_NAMES = [
 NODE_CONV, NODE_CONVT, NODE_ACT, NODE_RES_BEGIN, NODE_RES_END, NODE_GATE, NODE_SLICE = range(7)
 ACT_IDENTITY, ACT_TANH, ACT_LEAKY_RELU = range(3)
 PREC_FP32, PREC_BF16 = 0, 1
+HINT_NONE, HINT_PQMF = 0, 1
 
 
 class StreamconvError(RuntimeError):
@@ -45,7 +46,7 @@ class SCNode(C.Structure):
         ("taps", C.c_int32), ("stride", C.c_int32), ("dilation", C.c_int32),
         ("pad_left", C.c_int64), ("pad_right", C.c_int64), ("act", C.c_int32),
         ("alpha", C.c_float), ("weight_offset", C.c_int64), ("slice_begin", C.c_int32),
-        ("slice_count", C.c_int32),
+        ("slice_count", C.c_int32), ("hint", C.c_int32),
     ]
 
 

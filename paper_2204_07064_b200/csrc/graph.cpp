@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <sstream>
 
 #include "program.hpp"
@@ -19,6 +21,135 @@ namespace scb {
 namespace {
 
 int64_t delay_for_stride(int64_t S, int64_t R, int64_t Dc) { return (S - ((R + Dc) % S)) % S; }
+
+// ---- PQMF fast form (SC_HINT_PQMF): factor the cosine-modulated filter-bank weights.
+// analysis (stride-M conv, 1 -> M, K taps): W[n][j], j = B*a + b (B = 2M): the modulation of
+// band n repeats with period 2M in the tap index, so W[n][B a + b] = S[a][b] * Cm[n][b].
+bool factor_pqmf_analysis(ConvOp& op, int M, int K) {
+  const int B = 2 * M;
+  if (K % B != 0 || op.cin != 1 || op.nout != M || op.taps != K) return false;
+  const int A = K / B;
+  auto W = [&](int n, int j) { return static_cast<double>(op.w[static_cast<size_t>(j) * M + n]); };
+  double wmax = 0;
+  for (float v : op.w) wmax = std::max(wmax, std::fabs(static_cast<double>(v)));
+  std::vector<float> S(static_cast<size_t>(A) * B), Cm(static_cast<size_t>(M) * B);
+  for (int b = 0; b < B; ++b) {
+    int as = 0, ns = 0;
+    double best = -1;
+    for (int a = 0; a < A; ++a)
+      for (int n = 0; n < M; ++n)
+        if (std::fabs(W(n, B * a + b)) > best) best = std::fabs(W(n, B * a + b)), as = a, ns = n;
+    if (best <= 0) return false;
+    for (int n = 0; n < M; ++n) Cm[static_cast<size_t>(n) * B + b] = static_cast<float>(W(n, B * as + b) / W(ns, B * as + b));
+    for (int a = 0; a < A; ++a) S[static_cast<size_t>(a) * B + b] = static_cast<float>(W(ns, B * a + b));
+  }
+  for (int n = 0; n < M; ++n)
+    for (int a = 0; a < A; ++a)
+      for (int b = 0; b < B; ++b) {
+        const double rec = static_cast<double>(S[static_cast<size_t>(a) * B + b]) * Cm[static_cast<size_t>(n) * B + b];
+        if (std::fabs(rec - W(n, B * a + b)) > 1e-6 * wmax) return false;
+      }
+  op.pqmf = 1;
+  op.pq_A = A;
+  op.pq_B = B;
+  op.pq_M = M;
+  op.pq_S.swap(S);
+  op.pq_C.swap(Cm);
+  return true;
+}
+
+// synthesis (polyphase ConvT M -> 1, r = M, Q taps over input frames): the weight vector over
+// the M bands of every (q, phase) pair is proportional to one of <= 2M modulation vectors.
+bool factor_pqmf_synthesis(ConvOp& op, int M) {
+  const int Q = op.taps;
+  if (op.cin != M || op.nout != M) return false;
+  auto W = [&](int q, int c, int ph) { return static_cast<double>(op.w[(static_cast<size_t>(q) * M + c) * M + ph]); };
+  double wmax = 0;
+  for (float v : op.w) wmax = std::max(wmax, std::fabs(static_cast<double>(v)));
+  std::vector<std::vector<double>> cls;  // normalized class vectors
+  std::vector<int> idx(static_cast<size_t>(Q) * M, -1);
+  std::vector<float> sval(static_cast<size_t>(Q) * M, 0.f);
+  for (int q = 0; q < Q; ++q)
+    for (int ph = 0; ph < M; ++ph) {
+      int cm = 0;
+      for (int c = 1; c < M; ++c)
+        if (std::fabs(W(q, c, ph)) > std::fabs(W(q, cm, ph))) cm = c;
+      const double piv = W(q, cm, ph);
+      if (std::fabs(piv) <= 1e-30) continue;  // all-zero column: any class, s = 0 (idx stays -1)
+      std::vector<double> v(M);
+      for (int c = 0; c < M; ++c) v[c] = W(q, c, ph) / piv;
+      int found = -1;
+      for (size_t k = 0; k < cls.size() && found < 0; ++k) {
+        // proportional up to sign: compare v with cls[k] scaled by its value at cm
+        const double sc = cls[k][cm];
+        if (std::fabs(sc) < 1e-3) continue;
+        bool ok = true;
+        for (int c = 0; c < M && ok; ++c) ok = std::fabs(cls[k][c] / sc - v[c]) <= 1e-5;
+        if (ok) found = static_cast<int>(k);
+      }
+      if (found < 0) {
+        cls.push_back(v);
+        found = static_cast<int>(cls.size()) - 1;
+        if (cls.size() > static_cast<size_t>(4 * M)) return false;
+      }
+      idx[static_cast<size_t>(q) * M + ph] = found;
+      sval[static_cast<size_t>(q) * M + ph] = static_cast<float>(piv / cls[found][cm]);
+    }
+  if (cls.empty()) return false;
+  // Canonical class order: with the cosine modulation the class of (q, phase) depends on q
+  // only through q mod P (P = 2 for a 2M-periodic modulation) and, for a symmetric prototype,
+  // on the phase only up to the mirror phase <-> M-1-phase.  Renumber the classes so that
+  // class(q, phase) = (q mod P) * Mh + (mirror ? min(phase, M-1-phase) : phase), which lets
+  // the kernel index them statically (and, mirrored, use each loaded class value twice).
+  for (int cand = 0; cand < 6 && !op.pq_period; ++cand) {
+    const int P = (cand % 3 == 0) ? 1 : (cand % 3 == 1) ? 2 : 4;
+    const bool mirror = cand < 3;
+    const int Mh = mirror ? M / 2 : M;
+    if (Q % P != 0 || (mirror && M % 2) || cls.size() != static_cast<size_t>(P) * Mh) continue;
+    auto slot_of = [&](int q, int ph) { return (q % P) * Mh + (mirror ? std::min(ph, M - 1 - ph) : ph); };
+    std::vector<int> perm(cls.size(), -1), inv(cls.size(), -1);  // old class <-> canonical slot
+    bool ok = true;
+    for (int q = 0; q < Q && ok; ++q)
+      for (int ph = 0; ph < M && ok; ++ph) {
+        const int old = idx[static_cast<size_t>(q) * M + ph];
+        if (old < 0) continue;
+        const int slot = slot_of(q, ph);
+        if (perm[old] < 0 && inv[slot] < 0) perm[old] = slot, inv[slot] = old;
+        ok = perm[old] == slot && inv[slot] == old;
+      }
+    for (size_t k = 0; k < perm.size() && ok; ++k) ok = perm[k] >= 0;
+    if (!ok) continue;
+    std::vector<std::vector<double>> c2(cls.size());
+    for (size_t k = 0; k < cls.size(); ++k) c2[perm[k]] = cls[k];
+    cls.swap(c2);
+    for (int q = 0; q < Q; ++q)
+      for (int ph = 0; ph < M; ++ph) {
+        int& v = idx[static_cast<size_t>(q) * M + ph];
+        v = v < 0 ? slot_of(q, ph) : perm[v];
+      }
+    op.pq_period = P;
+    op.pq_mirror = mirror ? 1 : 0;
+  }
+  for (int& v : idx) v = std::max(v, 0);
+  std::vector<float> R(cls.size() * M);
+  for (size_t k = 0; k < cls.size(); ++k)
+    for (int c = 0; c < M; ++c) R[k * M + c] = static_cast<float>(cls[k][c]);
+  for (int q = 0; q < Q; ++q)
+    for (int ph = 0; ph < M; ++ph)
+      for (int c = 0; c < M; ++c) {
+        const size_t i = static_cast<size_t>(q) * M + ph;
+        const double rec = static_cast<double>(sval[i]) * R[static_cast<size_t>(idx[i]) * M + c];
+        if (std::fabs(rec - W(q, c, ph)) > 1e-6 * wmax) return false;
+      }
+  op.pqmf = 2;
+  op.pq_A = Q;
+  op.pq_B = static_cast<int>(cls.size());
+  op.pq_M = M;
+  op.pq_S.swap(sval);
+  op.pq_C.swap(R);
+  op.pq_idx.swap(idx);
+  return true;
+}
 
 struct Value {
   int buf = 0;
@@ -173,6 +304,15 @@ struct Lowerer {
       op.macs_per_sample = static_cast<double>(M) * N * K / S;  // per input frame
       std::snprintf(nm, sizeof nm, "conv%s %d->%d K%d d%d", S > 1 ? ("/" + std::to_string(S)).c_str() : "",
                     (int)M, (int)N, (int)K, nd.dilation);
+    }
+    if (nd.hint == SC_HINT_PQMF) {
+      if (convt && nd.out_channels == 1 && nd.stride == nd.in_channels) factor_pqmf_synthesis(op, nd.in_channels);
+      if (!convt && nd.in_channels == 1 && nd.stride == nd.out_channels && op.look == Ptot)
+        factor_pqmf_analysis(op, nd.out_channels, nd.taps);
+      if (op.pqmf) std::snprintf(nm, sizeof nm, "pqmf-%s %d bands K%d", convt ? "synthesis" : "analysis",
+                                 convt ? nd.in_channels : nd.out_channels, (int)K);
+      if (op.pqmf == 2 && op.pq_period) std::snprintf(nm + std::strlen(nm), sizeof nm - std::strlen(nm), " P%d%s", op.pq_period,
+                                              op.pq_mirror ? "m" : "");
     }
     op.name = nm;
     // scale per-input-frame MACs to per-input-SAMPLE of the model

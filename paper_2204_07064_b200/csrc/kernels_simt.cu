@@ -275,9 +275,26 @@ __global__ void carry_kernel(const BufDesc* __restrict__ bufs, int nbuf, int str
     while (b + 1 < nbuf && sb[b + 1].item0 <= g) ++b;
     const BufDesc d = sb[b];
     const int64_t loc = g - d.item0;
+    const int64_t T = d.t;
+    if ((d.C & 3) == 0) {  // float4 column groups: 16 B per thread, 512 B per warp and row
+      const int G = d.C >> 2;
+      const int64_t s = loc / G;
+      const int c4 = static_cast<int>(loc - s * G);
+      float4* col = reinterpret_cast<float4*>(d.base + s * d.sstride) + c4;
+      const int64_t fs = G;
+      int f = 0;
+      for (; f + 8 <= d.cache; f += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = col[(f + u + T) * fs];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) col[(f + u) * fs] = v[u];
+      }
+      for (; f < d.cache; ++f) col[f * fs] = col[(f + T) * fs];
+      continue;
+    }
     const int64_t s = loc / d.C;
     const int c = static_cast<int>(loc - s * d.C);
-    const int64_t T = d.t;
     float* col = d.base + s * d.sstride + c;
     const int64_t fs = d.C;
     int f = 0;

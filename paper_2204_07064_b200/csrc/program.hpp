@@ -35,6 +35,14 @@ struct ConvOp {
   int res_buf = -1, res_off = 0, res_act = ACT_ID;
   int64_t res_delay = 0;
   float res_alpha = 0.f;
+  // PQMF fast form (hint verified): 1 = analysis, 2 = synthesis; constants below
+  int pqmf = 0;
+  int pq_A = 0, pq_B = 0, pq_M = 0;  // analysis: A prototype phases x B = 2M modulation rows
+  std::vector<float> pq_S;           // analysis [A][B]; synthesis s(q, phi) [Q][M]
+  std::vector<float> pq_C;           // analysis Cm [M][B]; synthesis R [classes][M]
+  std::vector<int> pq_idx;           // synthesis class of (q, phi) [Q][M]
+  int pq_period = 0;                 // synthesis canonical classes (graph.cpp); 0: irregular
+  int pq_mirror = 0;
   std::vector<float> w;      // [taps][cin][nout]  (polyphase / gate-interleaved)
   std::vector<float> bias;   // [nout]
   Rate in_rate;              // frames of the input buffer per input sample

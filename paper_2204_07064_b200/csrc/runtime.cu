@@ -62,6 +62,11 @@ CUtensorMap make_map3(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, u
   return m;
 }
 
+bool pqmf_disabled() {
+  const char* e = std::getenv("SC_DISABLE_PQMF");
+  return e && std::atoi(e) != 0;
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("SC_DISABLE_TC");
   return e && std::atoi(e) != 0;
@@ -157,8 +162,35 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
   plan->dops.assign(nops, DevOp{});
   std::vector<std::vector<float>> wtc(nops);
   for (size_t i = 0; i < nops; ++i) plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i]);
+  // PQMF fast form: the factor arrays (S, C, class index as float) follow the op's blob slots
+  std::vector<std::vector<float>> pqv(nops);
+  for (size_t i = 0; i < nops; ++i) {
+    const ConvOp& op = plan->prog.ops[i];
+    DevOp& d = plan->dops[i];
+    if (!op.pqmf || d.kernel != KERNEL_SIMT || pqmf_disabled() || op.gate || op.res_buf >= 0) continue;
+    const BufferSpec& bi = plan->prog.bufs[op.in_buf];
+    const BufferSpec& bo = plan->prog.bufs[op.out_buf];
+    // one output row = M contiguous floats: an M-band frame (analysis) or M mono samples (synthesis)
+    if (op.out_rstride != op.nout || op.nout != op.pq_M || bo.C != (op.pqmf == 1 ? op.pq_M : 1)) continue;
+    if (op.pqmf == 1) {
+      if (!pqmf_fast_shape(1, op.pq_M, op.pq_A, op.pq_B) || bi.C != 1 || op.row_step != op.pq_M || op.tap_step != 1)
+        continue;
+      d.kernel = KERNEL_PQMF_ANA;
+    } else {
+      if (!pqmf_fast_shape(2, op.pq_M, op.pq_A, op.pq_B, op.pq_period, op.pq_mirror) || op.row_step != 1 || op.tap_step != 1) continue;
+      d.kernel = KERNEL_PQMF_SYN;
+      d.pq_classes = op.pq_B;
+    }
+    auto& v = pqv[i];
+    const size_t nS = round_up(static_cast<int64_t>(op.pq_S.size()), 64);
+    const size_t nC = round_up(static_cast<int64_t>(op.pq_C.size()), 64);
+    v.assign(nS + nC + op.pq_idx.size(), 0.f);
+    std::copy(op.pq_S.begin(), op.pq_S.end(), v.begin());
+    std::copy(op.pq_C.begin(), op.pq_C.end(), v.begin() + nS);
+    for (size_t k = 0; k < op.pq_idx.size(); ++k) v[nS + nC + k] = static_cast<float>(op.pq_idx[k]);
+  }
   int64_t total = 0;
-  std::vector<int64_t> woff, boff, toff;
+  std::vector<int64_t> woff, boff, toff, qoff;
   for (size_t i = 0; i < nops; ++i) {
     const ConvOp& op = plan->prog.ops[i];
     woff.push_back(total);
@@ -167,6 +199,8 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
     total += round_up(static_cast<int64_t>(op.bias.size()), 64);
     toff.push_back(total);
     total += round_up(static_cast<int64_t>(wtc[i].size()), 64);
+    qoff.push_back(total);
+    total += round_up(static_cast<int64_t>(pqv[i].size()), 64);
   }
   std::vector<float> host(static_cast<size_t>(std::max<int64_t>(total, 1)), 0.f);
   for (size_t i = 0; i < nops; ++i) {
@@ -174,6 +208,7 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
     std::memcpy(host.data() + woff[i], op.w.data(), op.w.size() * sizeof(float));
     std::memcpy(host.data() + boff[i], op.bias.data(), op.bias.size() * sizeof(float));
     if (!wtc[i].empty()) std::memcpy(host.data() + toff[i], wtc[i].data(), wtc[i].size() * sizeof(float));
+    if (!pqv[i].empty()) std::memcpy(host.data() + qoff[i], pqv[i].data(), pqv[i].size() * sizeof(float));
   }
   ck(cudaMalloc(&plan->wmem, host.size() * sizeof(float)), "cudaMalloc(weights)");
   ck(cudaMemcpy(plan->wmem, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice),
@@ -182,6 +217,12 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
     DevOp& d = plan->dops[i];
     d.w = plan->wmem + woff[i];
     d.bias = plan->wmem + boff[i];
+    if (d.kernel == KERNEL_PQMF_ANA || d.kernel == KERNEL_PQMF_SYN) {
+      const ConvOp& op = plan->prog.ops[i];
+      d.pq_S = plan->wmem + qoff[i];
+      d.pq_C = d.pq_S + round_up(static_cast<int64_t>(op.pq_S.size()), 64);
+      d.pq_idx = d.pq_C + round_up(static_cast<int64_t>(op.pq_C.size()), 64);
+    }
     if (d.kernel == KERNEL_TC) {
       const ConvOp& op = plan->prog.ops[i];
       d.wtc = plan->wmem + toff[i];
@@ -361,7 +402,7 @@ CallPlan& State::call_plan(int64_t F) {
     d.C = b.C;
     d.cache = static_cast<int>(cache[i]);
     d.t = static_cast<int>(cp->T[i]);
-    items += static_cast<int64_t>(streams) * b.C;
+    items += static_cast<int64_t>(streams) * ((b.C % 4 == 0) ? b.C / 4 : b.C);  // float4 groups
     desc.push_back(d);
   }
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
@@ -496,6 +537,34 @@ ConvParams State::conv_params(size_t i, const CallPlan& cp) const {
   return p;
 }
 
+PqmfParams State::pqmf_params(size_t i, const CallPlan& cp) const {
+  const ConvParams c = conv_params(i, cp);
+  const DevOp& d = plan->dops[i];
+  PqmfParams p{};
+  p.in = c.in;
+  p.in_sstride = c.in_sstride;
+  p.in_fstride = c.in_fstride;
+  p.in_off = c.in_off;
+  p.in_f0 = c.in_f0;
+  p.S = d.pq_S;
+  p.C = d.pq_C;
+  p.idx = d.pq_idx;
+  p.bias = c.bias;
+  p.nclass = d.pq_classes;
+  p.period = plan->prog.ops[i].pq_period;
+  p.mirror = plan->prog.ops[i].pq_mirror;
+  p.out = c.out;
+  p.out_sstride = c.out_sstride;
+  p.out_base = c.out_base;
+  p.t_out = c.t_out;
+  p.streams = c.streams;
+  p.pre_act = c.pre_act;
+  p.pre_alpha = c.pre_alpha;
+  p.post_act = c.post_act;
+  p.post_alpha = c.post_alpha;
+  return p;
+}
+
 IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
   const Program& pg = plan->prog;
   IngestArgs a{};
@@ -544,7 +613,8 @@ std::string State::launch_name(int64_t F, int i) {
       const ConvOp& op = plan->prog.ops[j];
       const DevOp& d = plan->dops[j];
       return "op" + std::to_string(j) + " " + op.name + " [" +
-             (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc") : "simt") + "]";
+             (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
+              : d.kernel == KERNEL_SIMT ? "simt" : "pqmf") + "]";
     }
   }
   if (i == k++) return "egress";
@@ -562,6 +632,8 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     if (plan->dops[i].kernel == KERNEL_TC) {
       const TcLaunch& t = cp.tc[i];
       launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
+    } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {
+      launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_params(i, cp), s);
     } else {
       launch_conv_simt(conv_params(i, cp), s);
     }

@@ -10,12 +10,13 @@
 #include <vector>
 
 #include "kernels.hpp"
+#include "kernels_pqmf.hpp"
 #include "kernels_tc.hpp"
 #include "program.hpp"
 
 namespace scb {
 
-enum KernelKind { KERNEL_SIMT = 0, KERNEL_TC = 1 };
+enum KernelKind { KERNEL_SIMT = 0, KERNEL_TC = 1, KERNEL_PQMF_ANA = 2, KERNEL_PQMF_SYN = 3 };
 
 struct DevOp {
   float* w = nullptr;
@@ -28,6 +29,11 @@ struct DevOp {
   bool bf16 = false;
   int view_S = 1;            // super-row factor of the input view (conv stride, or 1)
   int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
+  // PQMF fast form (kernel == KERNEL_PQMF_*): factor arrays inside the weight blob
+  float* pq_S = nullptr;
+  float* pq_C = nullptr;
+  float* pq_idx = nullptr;
+  int pq_classes = 0;
 };
 
 struct Plan {
@@ -104,6 +110,7 @@ struct State {
   std::vector<int64_t> next_counts(int64_t F) const;
   CallPlan& call_plan(int64_t F);
   ConvParams conv_params(size_t op, const CallPlan& cp) const;
+  PqmfParams pqmf_params(size_t op, const CallPlan& cp) const;
   IngestArgs ingest_args(const float* in, const CallPlan& cp) const;
   EgressArgs egress_args(float* out, const CallPlan& cp) const;
   void check_frames(int64_t frames) const;

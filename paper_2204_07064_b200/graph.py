@@ -63,7 +63,7 @@ class Model:
     def _node(self, kind, **kw) -> dict:
         nd = dict(kind=kind, in_channels=0, out_channels=0, taps=0, stride=1, dilation=1,
                   pad_left=0, pad_right=0, act=0, alpha=0.0, weight_offset=0, slice_begin=0,
-                  slice_count=0)
+                  slice_count=0, hint=0)
         nd.update(kw)
         self.nodes.append(nd)
         return nd
@@ -141,6 +141,7 @@ class Model:
         w = ana[: bands * taps].reshape(bands, 1, taps)
         self.conv(1, bands, taps, stride=bands, padding=(taps - bands, 0), weight=w,
                   bias=np.zeros(bands, np.float32))
+        self.nodes[-1]["hint"] = _abi.HINT_PQMF
         return self
 
     def pqmf_synthesis(self, bands: int = 16, taps: int = 256) -> "Model":
@@ -148,6 +149,7 @@ class Model:
         w = syn[: bands * taps].reshape(1, bands, taps)
         self.conv_transpose(bands, 1, taps, stride=bands, padding=(taps - 1, 0), weight=w,
                             bias=np.zeros(1, np.float32))
+        self.nodes[-1]["hint"] = _abi.HINT_PQMF
         return self
 
     # ---- C-ABI form

@@ -160,6 +160,10 @@ class StreamState:
         check(lib().sc_process_launches(self._h, frames, C.byref(n)))
         return n.value
 
+    def launch_names(self, frames: int):
+        """Names of the launches one call of `frames` enqueues ("op<i> <op> [tc|tc-bf16|simt|pqmf]")."""
+        return [lib().sc_launch_name(self._h, frames, i).decode() for i in range(self.launches(frames))]
+
     def profile(self, x, y, frames: int, steps: int = 3, stream=None):
         """Per-launch mean device ms over `steps` un-graphed calls (CUDA events between
         launches on the launching stream).  Returns [(name, ms)]."""

@@ -248,3 +248,46 @@ def test_process_host_matches_device():
     torch.cuda.synchronize()
     y_host = torch.cat(outs, 2).numpy()
     assert np.array_equal(y_host, y_dev)
+
+
+def _pqmf_model():
+    from paper_2204_07064_b200.graph import Model
+    m = Model(in_channels=1)
+    m.pqmf_analysis(16, 256)
+    m.leaky_relu(0.2)
+    m.pqmf_synthesis(16, 256)
+    return m
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [[4096, 4096], [16, 4080, 2048, 2048], [256] * 12])
+def test_pqmf_fast_form_vs_oracle(parts):
+    """The polyphase / cosine-modulation PQMF kernels (kernels_pqmf.cu) against the oracle's
+    plain convolutions, across ragged buffer partitions."""
+    m = _pqmf_model()
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((3, 1, sum(parts))).astype(np.float32)
+    y, plan, st = run_gpu(m, x, parts)
+    names = st.launch_names(parts[0])
+    assert any("pqmf-analysis" in n and n.endswith("[pqmf]") for n in names), names
+    assert any("pqmf-synthesis" in n and n.endswith("[pqmf]") for n in names), names
+    ref = po.run(m, x, parts=parts)
+    err, rms = rel_err(y, ref)
+    assert err <= FP32_TOL, (err, rms)
+
+
+@pytest.mark.gpu
+def test_pqmf_fast_form_selected_in_rave_configs(monkeypatch):
+    """cfg4 / cfg5 run their PQMF ops on the fast kernels; the generic conv path
+    (SC_DISABLE_PQMF=1) gives the same outputs within the fp32 tolerance."""
+    for cfg, parts in ((4, [1] * 4), (5, [2048] * 2)):
+        model = configs.build(cfg, seed=cfg)
+        x = configs.batch_input(cfg, range(2), model.in_channels, sum(parts), seed=3)
+        y_fast, _, st = run_gpu(model, x, parts)
+        assert any(n.endswith("[pqmf]") for n in st.launch_names(parts[0]))
+        monkeypatch.setenv("SC_DISABLE_PQMF", "1")
+        y_gen, _, st2 = run_gpu(model, x, parts)
+        monkeypatch.delenv("SC_DISABLE_PQMF")
+        assert not any(n.endswith("[pqmf]") for n in st2.launch_names(parts[0]))
+        err, rms = rel_err(y_fast, y_gen)
+        assert err <= 2 * FP32_TOL, (cfg, err, rms)
