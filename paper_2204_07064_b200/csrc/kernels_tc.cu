@@ -10,16 +10,16 @@
 // operand x is split x = hi + lo with hi = x & 0xffffe000 (exactly representable in tf32) and
 // lo = x - hi (exact in fp32), and D += A_lo W_hi + A_hi W_lo + A_hi W_hi (the dropped A_lo W_lo
 // term is ~2^-22 relative).  Weight hi/lo planes are prepared once at plan time; the
-// activation split (and the fused pre-activation LeakyReLU/tanh) is done in shared memory by
-// the transform warps between the TMA landing and the MMA issue — elementwise, so it is
-// oblivious to the 128B swizzle.
+// activation split (and the fused pre-activation LeakyReLU/tanh) is done by the transform
+// warps between the TMA landing and the MMA issue, which store A hi / lo into TMEM: all three
+// MMAs take A from TMEM, so the only shared-memory operand traffic is the weight tile (shared
+// memory bandwidth, not the tensor core, bounded the all-smem form).
 //
 // The tensor core accumulates in fp32 with truncation, so long K loops drift (measured: ~4e-5
 // x RMS per layer at K=384..1536).  The MMA therefore accumulates only CK K-blocks (a chunk)
-// into one of two TMEM buffers — the main A_hi W_hi product and the two small correction
-// products in separate accumulators — and the drain warps add each chunk into fp32
-// registers with round-to-nearest adds (fixed order, independent of T and of the stream
-// count), which keeps the path at FFMA-level accuracy at any depth.
+// into one of two TMEM buffers, and the drain warps add each chunk into fp32 registers with
+// round-to-nearest adds (fixed order, independent of T and of the stream count), which keeps
+// the path at FFMA-level accuracy at any depth.
 //
 // Persistent: grid = #SMs, static tile striding; the TMA/transform/MMA pipeline runs across
 // tile boundaries and the drain/epilogue of tile t overlaps the MMAs of tile t+1.
@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels_tc.hpp"
 
@@ -40,7 +41,7 @@ namespace scb {
 
 namespace {
 
-__device__ long long g_tc_trace[10 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
+__device__ long long g_tc_trace[12 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
 
 __device__ __forceinline__ long long clk() { return clock64(); }  // SM cycles (per-SM counter)
 
@@ -81,6 +82,24 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_w(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                              int c2) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
@@ -159,6 +178,39 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+// Warp-collective forms: the whole warp runs the issue loop in uniform control flow (so the
+// descriptors live in uniform registers) and elect.sync picks the one issuing lane.  Issuing
+// from a lane-0-only branch instead costs an R2UR waterfall per tcgen05.mma (~80 cycles).
+__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -171,6 +223,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
         "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -190,8 +253,8 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
   return v;
 }
 
-// fp32 (3xTF32) stage: A (raw -> hi, in place) | W hi | W lo, K-major SW128 (32 fp32/row);
-//                      A lo goes to TMEM (the correction MMA reads A from TMEM).
+// fp32 (3xTF32) stage: A raw | W hi | W lo, K-major SW128 (32 fp32/row); A hi / lo go to
+//                      TMEM (per-stage columns).
 // bf16 stage:          A raw fp32 (SW128) | A bf16 (SW64, 32 bf16/row) | W bf16 (SW64).
 template <int BN, int STAGES, bool BF = false>
 struct TcSmem {
@@ -264,7 +327,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* stg_written = bars + 3 * STAGES + 5;
   uint64_t* stg_free = bars + 3 * STAGES + 6;
   uint64_t* corr_empty = bars + 3 * STAGES + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 8);
+  uint64_t* aempty = bars + 3 * STAGES + 8;  // [<= STAGES] TMEM A slots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 8);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * L::STAGE + L::STAGING + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
@@ -278,14 +342,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int nk = p.n_kblocks;
   const int n_tiles_n = (p.nout + BN - 1) / BN;
   const int n_tiles = p.m_tiles * n_tiles_n;
-  // fp32: main x2 (chunk double buffer) | corr (whole tile) | A lo x STAGES (32 cols each)
+  // fp32: main x2 (chunk double buffer) | corr (whole tile) | A ring of TS slots, each A hi
+  //       (32 cols) + A lo (32 cols), decoupled from the shared-memory stages
   // bf16: main x2
-  constexpr uint32_t COLS_USED = BF ? 2 * BN : 3 * BN + 32 * STAGES;
+  constexpr int TS = BF ? 1 : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
+  static_assert(BF || TS >= 2, "TMEM A ring needs two slots");
+  constexpr uint32_t COLS_USED = BF ? 2 * BN : 3 * BN + 64 * TS;
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
   constexpr uint32_t CORR_COL = 2 * BN;
-  constexpr uint32_t ALO_COL = 3 * BN;
+  constexpr uint32_t A_COL = 3 * BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -301,6 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
     mbar_init(corr_empty, 8);
+    for (int a = 0; a < STAGES; ++a) mbar_init(&aempty[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -327,8 +395,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
+    // ===================== TMA producer (whole warp, one elected lane issues) =====================
+    {
       const uint32_t bytes = static_cast<uint32_t>(BK * 4 * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
       int g = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -336,24 +404,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[4 * 256 + g] = clk();
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
           const int q = kb / p.cblocks;
           const int cb = kb - q * p.cblocks;
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[0 * 256 + g] = clk();
-          mbar_expect_tx(&full[s], bytes);
-          tma_load_3d(&tmap_a, &full[s], a_hi(s), p.a_c0 + cb * BK, p.a_row0 + tc.i0 + q * p.a_tap_rows, tc.s0);
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
+          mbar_expect_tx_w(&full[s], bytes);
+          tma_load_3d_w(&tmap_a, &full[s], a_hi(s), p.a_c0 + cb * BK, p.a_row0 + tc.i0 + q * p.a_tap_rows, tc.s0);
           if (BF) {
-            tma_load_3d(&tmap_w, &full[s], b_bf(s), kb * BK, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_bf(s), kb * BK, tc.n0, 0);
           } else {
-            tma_load_3d(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
-            tma_load_3d(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (whole warp, one elected lane issues) =====================
+    {
+      const uint32_t tbase = warp_uniform(tmem_base);
       // c_format F32 | a,b format TF32 (2) or BF16 (1) | N >> 3 | M >> 4
       const uint32_t fmt = BF ? 1u : 2u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -367,41 +436,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
           if (chunk_first && c >= 2) mbar_wait(&tempty[b], ((c >> 1) + 1) & 1);
           mbar_wait(&xform[s], (g / STAGES) & 1);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256) g_tc_trace[3 * 256 + g] = clk();
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
           tc_fence_after();
-          const uint32_t dmain = tmem_base + static_cast<uint32_t>(b * BN);
+          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
           if (BF) {
             const uint32_t ab = smem_u32(a_bf(s)), bb = smem_u32(b_bf(s));
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes along the 64B row
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16(dmain, sw64_desc(ab + kk * 32), sw64_desc(bb + kk * 32), idesc, acc0);
+              mma_bf16_w(dmain, sw64_desc(ab + kk * 32), sw64_desc(bb + kk * 32), idesc, acc0);
             }
           } else {
-            const uint32_t ah = smem_u32(a_hi(s));
+            // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
+            // shared-memory operand traffic is the weight tile (A never re-read from smem)
             const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-            const uint32_t dcorr = tmem_base + CORR_COL;
-            const uint32_t alo = tmem_base + ALO_COL + 32 * s;
+            const uint32_t ahi = tbase + A_COL + 64 * (g % TS);
+            const uint32_t alo = ahi + 32;
+            const uint32_t dcorr = tbase + CORR_COL;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 32 bytes along the swizzled row
+            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_tf32(dmain, sw128_desc(ah + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+              if (!(p.debug & 1024)) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
             }
-            // corrections accumulate over the whole tile in one buffer (2^-10 of the signal: its
-            // own truncation is negligible); wait until the drain has read the previous tile's
+            // corrections accumulate over the whole tile in their own buffer (2^-10 of the
+            // signal: their truncation is negligible, and the main chunk keeps 4 accumulation
+            // steps); wait until the drain has read the previous tile's
             if (kb == 0 && tcount > 0) mbar_wait(corr_empty, (tcount - 1) & 1);
             if (!(p.debug & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) {
                 const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-                mma_tf32_ts(dcorr, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
-                mma_tf32(dcorr, sw128_desc(ah + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+                mma_tf32_ts_w(dcorr, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+                mma_tf32_ts_w(dcorr, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
               }
             }
+            mma_commit_w(&aempty[g % TS]);
           }
-          mma_commit(&empty[s]);
+          mma_commit_w(&empty[s]);
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
-            mma_commit(&tfull[b]);
+            mma_commit_w(&tfull[b]);
             ++c;
           }
         }
@@ -464,30 +538,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             *reinterpret_cast<uint2*>(dst + ((jb ^ ((t >> 1) & 3)) << 4) + ((j4 & 1) << 3)) = pk;
           }
         }
-        if (!BF) {
-          // thread = tile row r (= TMEM lane): hi written back in place (smem, SW128 chunk
-          // j of row r lives at j ^ (r & 7)), lo stored to this stage's TMEM A columns
+        if (!BF && !(p.debug & 512)) {
+          // thread = tile row r (= TMEM lane): SW128 chunk j of row r lives at j ^ (r & 7); hi
+          // and lo go to this stage's TMEM A columns (the MMAs read A from TMEM)
           const int quarter = warp & 3;
           const int r = quarter * 32 + lane;
-          float4* row = reinterpret_cast<float4*>(a_hi(s)) + r * 8;
+          const float4* row = reinterpret_cast<const float4*>(a_hi(s)) + r * 8;
           const bool pre_tanh = p.pre_act == ACT_TANH;
           const float pre_s = slope_of(p.pre_act, p.pre_alpha);
-          float lo[32];
+          float hi[32], lo[32];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int pj = j ^ (r & 7);
-            const float4 v = row[pj];
-            float x[4] = {v.x, v.y, v.z, v.w};
-            float h[4];
+            const float4 v = row[j ^ (r & 7)];
+            const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const float a = pre_tanh ? tanh_ool(x[u]) : act_lin(x[u], pre_s);
-              h[u] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-              lo[4 * j + u] = a - h[u];
+              hi[4 * j + u] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+              lo[4 * j + u] = a - hi[4 * j + u];
             }
-            row[pj] = make_float4(h[0], h[1], h[2], h[3]);
           }
-          tmem_st32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ALO_COL + 32 * s, lo);
+          const int a = g % TS;
+          if (g >= TS) mbar_wait(&aempty[a], ((g / TS) + 1) & 1);  // MMAs of g - TS done
+          tc_fence_after();
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 64 * a;
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
@@ -520,12 +596,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
 #pragma unroll
-        for (int cc = 0; cc < COLS; cc += 16) {
-          uint32_t v[16];
-          tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);  // main chunk
+        for (int cc = 0; cc < ((p.debug & 256) ? 0 : COLS); cc += (COLS >= 32 ? 32 : 16)) {  // main chunk
+          uint32_t v[32];
+          if (COLS >= 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
+          else tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);
           tmem_wait_ld();
 #pragma unroll
-          for (int u = 0; u < 16; ++u)
+          for (int u = 0; u < (COLS >= 32 ? 32 : 16); ++u)
             acc[cc + u] = first ? __uint_as_float(v[u]) : acc[cc + u] + __uint_as_float(v[u]);
         }
         if (!BF && kb == nk - 1) {  // the tile's corrections (complete with its last chunk)
@@ -544,6 +621,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
+        if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
         ++c;
       }
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
@@ -638,7 +716,7 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
 
 }  // namespace
 
-void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 10 * 256); }
+void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 12 * 256); }
 
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
@@ -647,6 +725,27 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
       case 32: launch_bn<32, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
       case 64: launch_bn<64, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
       default: launch_bn<128, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
+  static int ck = -1;
+  if (ck < 0) {
+    const char* e = std::getenv("SC_TC_CK");
+    ck = e ? std::atoi(e) : 1;
+  }
+  if (ck == 2) {
+    switch (p.BN) {
+      case 32: launch_bn<32, 4, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 4, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 3, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
+  if (ck == 4) {
+    switch (p.BN) {
+      case 32: launch_bn<32, 4, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 4, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 3, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;
   }
