@@ -315,7 +315,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const TcParams p) {
   using L = TcSmem<BN, STAGES, BF>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by an offset from the __shared__ array (not integer pointer math), so
+  // the compiler keeps the shared address space: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stg = reinterpret_cast<float*>(smem + STAGES * L::STAGE);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE + L::STAGING);
   uint64_t* full = bars;
@@ -596,7 +598,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
 #pragma unroll
-        for (int cc = 0; cc < ((p.debug & 256) ? 0 : COLS); cc += (COLS >= 32 ? 32 : 16)) {  // main chunk
+        for (int cc = 0; cc < COLS; cc += (COLS >= 32 ? 32 : 16)) {  // main chunk, 32 columns per wait
           uint32_t v[32];
           if (COLS >= 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
           else tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float ps = slope_of(p.post_act, p.post_alpha);
         const float rs = slope_of(p.res_act, p.res_alpha);
 #pragma unroll
-        for (int u = 0; u < ((p.debug & 128) ? 0 : COLS); u += 4) {
+        for (int u = 0; u < COLS; u += 4) {
           const int n = tc.n0 + col0 + u;
           const float4 bv = *reinterpret_cast<const float4*>(sbias + n);
           float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
