@@ -201,6 +201,16 @@ __device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a, uint64_t
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -210,6 +220,15 @@ __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
       : "memory");
 }
 __device__ __forceinline__ uint32_t warp_uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -259,8 +278,7 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 template <int BN, int STAGES, bool BF = false>
 struct TcSmem {
   static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
-  static constexpr uint32_t A_BF = BM * BK * 2;
-  static constexpr uint32_t STAGE = BF ? A_TILE + A_BF + B_TILE : A_TILE + 2 * B_TILE;
+  static constexpr uint32_t STAGE = BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
   static constexpr uint32_t BYTES = STAGES * STAGE + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
 };
@@ -336,8 +354,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
   auto b_hi = [&](int s) { return smem + s * L::STAGE + A_TILE; };
   auto b_lo = [&](int s) { return smem + s * L::STAGE + A_TILE + L::B_TILE; };
-  auto a_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
-  auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE + L::A_BF; };
+  auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -347,14 +364,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // fp32: main x2 (chunk double buffer) | corr (whole tile) | A ring of TS slots, each A hi
   //       (32 cols) + A lo (32 cols), decoupled from the shared-memory stages
   // bf16: main x2
-  constexpr int TS = BF ? 1 : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
-  static_assert(BF || TS >= 2, "TMEM A ring needs two slots");
-  constexpr uint32_t COLS_USED = BF ? 2 * BN : 3 * BN + 64 * TS;
+  // bf16: main x2 | A ring of STAGES slots, 16 cols each (32 bf16 per row, two per column)
+  constexpr int TS = BF ? STAGES : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
+  static_assert(TS >= 2, "TMEM A ring needs two slots");
+  constexpr uint32_t COLS_USED = BF ? 2 * BN + 16 * TS : 3 * BN + 64 * TS;
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
   constexpr uint32_t CORR_COL = 2 * BN;
-  constexpr uint32_t A_COL = 3 * BN;
+  constexpr uint32_t A_COL = BF ? 2 * BN : 3 * BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -442,12 +460,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
           if (BF) {
-            const uint32_t ab = smem_u32(a_bf(s)), bb = smem_u32(b_bf(s));
+            // A (bf16 pairs) from this stage's TMEM columns, W from shared memory
+            const uint32_t bb = smem_u32(b_bf(s));
+            const uint32_t at = tbase + A_COL + 16 * (g % TS);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 32 bytes along the 64B row
+            for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 8 TMEM columns / 32 bytes of the 64B row
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16_w(dmain, sw64_desc(ab + kk * 32), sw64_desc(bb + kk * 32), idesc, acc0);
+              mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, acc0);
             }
+            mma_commit_w(&aempty[g % TS]);
           } else {
             // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
             // shared-memory operand traffic is the weight tile (A never re-read from smem)
@@ -517,15 +538,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&full[s], (g / STAGES) & 1);
         if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[1 * 256 + g] = clk();
         if (BF) {
-          // fp32 row t (SW128: 16B chunk j at j ^ (t & 7)) -> bf16 row t (SW64: 16B chunk jb at
-          // jb ^ ((t >> 1) & 3)), pre-activation fused
-          const float4* src = reinterpret_cast<const float4*>(a_hi(s)) + t * 8;
-          uint8_t* dst = a_bf(s) + t * 64;
+          // thread = tile row r (= TMEM lane): fp32 SW128 row (16B chunk j at j ^ (r & 7)) ->
+          // pre-activation -> bf16 pairs (low half = even k) -> this stage's TMEM A columns
+          const int quarter = warp & 3;
+          const int r = quarter * 32 + lane;
+          const float4* row = reinterpret_cast<const float4*>(a_hi(s)) + r * 8;
           const bool pre_tanh = p.pre_act == ACT_TANH;
           const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+          uint32_t pk[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            float4 v = src[j4 ^ (t & 7)];
+            float4 v = row[j4 ^ (r & 7)];
             if (pre_tanh) {
               v = make_float4(tanh_ool(v.x), tanh_ool(v.y), tanh_ool(v.z), tanh_ool(v.w));
             } else {
@@ -533,12 +556,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             __nv_bfloat162 lo2 = __floats2bfloat162_rn(v.x, v.y);
             __nv_bfloat162 hi2 = __floats2bfloat162_rn(v.z, v.w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t*>(&lo2);
-            pk.y = *reinterpret_cast<uint32_t*>(&hi2);
-            const int jb = j4 >> 1;
-            *reinterpret_cast<uint2*>(dst + ((jb ^ ((t >> 1) & 3)) << 4) + ((j4 & 1) << 3)) = pk;
+            pk[2 * j4] = *reinterpret_cast<uint32_t*>(&lo2);
+            pk[2 * j4 + 1] = *reinterpret_cast<uint32_t*>(&hi2);
           }
+          const int a = g % TS;
+          if (g >= TS) mbar_wait(&aempty[a], ((g / TS) + 1) & 1);  // MMAs of g - TS done
+          tc_fence_after();
+          tmem_st16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 16 * a, pk);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
         }
         if (!BF && !(p.debug & 512)) {
           // thread = tile row r (= TMEM lane): SW128 chunk j of row r lives at j ^ (r & 7); hi
@@ -724,9 +750,9 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
   if (p.bf16) {
     switch (p.BN) {
-      case 32: launch_bn<32, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 4, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 32: launch_bn<32, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;
   }
