@@ -6,10 +6,11 @@ no Python or CPU fallback — if the shared library is missing, `lib()` raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libstreamconv_b200.so"
+LIB_PATH = Path(os.environ["SC_LIB_PATH"]) if os.environ.get("SC_LIB_PATH") else PKG / "lib" / "libstreamconv_b200.so"
 
 # streamconv::ErrCode (proj/include/streamconv/error.hpp:8-29); status = 1 + ordinal
 ERR_NAMES = [
