@@ -239,6 +239,7 @@ def main():
            for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
+    launched0 = st.launch_total()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             if flush is not None:
@@ -248,6 +249,7 @@ def main():
             evs[k][1].record(stream)
         torch.cuda.synchronize()
     barrier()
+    gpu_launches = st.launch_total() - launched0  # exact: counted by the library per call
     ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), dev)
     total_streams = args.total_streams or streams * ws
     value = total_streams * out_call * args.steps / (ms / 1e3)
@@ -337,7 +339,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": in_bytes,
                     "d2h_bytes_per_step": out_bytes},
-            "gpu_launches": st.launches(frames) * args.steps,
+            "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "profile_ms": {n: round(t, 4) for n, t in prof},
         }

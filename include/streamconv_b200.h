@@ -176,8 +176,12 @@ SC_API int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t 
 SC_API int sc_process_host(sc_state* state, const float* h_in, float* h_out, int64_t frames,
                            void* stream);
 SC_API int sc_process_host_wait(sc_state* state, void* stream);
-/* Number of kernels one sc_process launches (for launch accounting). */
+/* Launch slots of one sc_process call (profile layout): carry (wrap-around calls only, see
+ * DESIGN.md §3 strips), ingest, one per firing op, egress. */
 SC_API int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n);
+/* Kernels launched so far by this state (eager, graph-replayed or profiled calls): the exact
+ * launch count of a timed region is the difference of two readings. */
+SC_API int sc_state_launch_total(const sc_state* state, int64_t* total);
 /* Measurement: run `steps` calls WITHOUT graph replay with CUDA events between launches;
  * ms_per_launch[i] = mean device time of launch i (sc_process_launches entries).          */
 SC_API int sc_state_profile(sc_state* state, const float* d_in, float* d_out, int64_t frames,

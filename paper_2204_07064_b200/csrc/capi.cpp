@@ -212,6 +212,13 @@ int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n) {
   });
 }
 
+int sc_state_launch_total(const sc_state* state, int64_t* total) {
+  return guard([&] {
+    need(state && total, "null argument");
+    *total = state->s->launched;
+  });
+}
+
 int sc_state_profile(sc_state* state, const float* d_in, float* d_out, int64_t frames, int32_t steps,
                      float* ms_per_launch, void* stream) {
   return guard([&] {

@@ -299,20 +299,39 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
-  int64_t total = 0;
-  std::vector<int64_t> off;
-  for (size_t i = 0; i < pg.bufs.size(); ++i) {
-    const BufferSpec& b = pg.bufs[i];
-    // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
-    const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
-    const int64_t sstride = round_up((st->cache[i] + T) * b.C, 32);
-    st->buf_sstride.push_back(sstride);
-    off.push_back(total);
-    total += round_up(sstride * streams, 64);
-    st->cache_bytes_per_stream += st->cache[i] * b.C * 4;
+  // strip length: k calls' frames after the cache (phase mode keeps k = 1: bursts vary).
+  // Strips pay off when the carry moves a lot of bytes (many streams x large caches); small
+  // states keep k = 1 (one CallPlan / graph per buffer length).
+  {
+    int64_t cache_floats = 0;
+    for (size_t i = 0; i < pg.bufs.size(); ++i) cache_floats += st->cache[i] * pg.bufs[i].C;
+    const bool big = cache_floats * 4 * static_cast<int64_t>(streams) >= (int64_t{256} << 20);
+    const char* e = std::getenv("SC_STRIP_K");
+    st->strip_k = st->phase_mode ? 1 : std::max(1, e ? std::atoi(e) : (big ? 4 : 1));
   }
-  st->mem_bytes = total * 4;
-  ck(cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256)), "cudaMalloc(state)");
+  std::vector<int64_t> off;
+  for (;;) {
+    int64_t total = 0;
+    off.clear();
+    st->buf_sstride.clear();
+    st->cache_bytes_per_stream = 0;
+    for (size_t i = 0; i < pg.bufs.size(); ++i) {
+      const BufferSpec& b = pg.bufs[i];
+      // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
+      const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
+      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T) * b.C, 32);
+      st->buf_sstride.push_back(sstride);
+      off.push_back(total);
+      total += round_up(sstride * streams, 64);
+      st->cache_bytes_per_stream += st->cache[i] * b.C * 4;
+    }
+    st->mem_bytes = total * 4;
+    const cudaError_t e = cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256));
+    if (e == cudaSuccess) break;
+    cudaGetLastError();
+    if (st->strip_k == 1) ck(e, "cudaMalloc(state)");
+    st->strip_k /= 2;  // not enough memory for this strip length: halve it (k = 1: carry every call)
+  }
   ck(cudaMemset(st->mem, 0, std::max<int64_t>(st->mem_bytes, 256)), "cudaMemset(state)");
   for (size_t i = 0; i < pg.bufs.size(); ++i) st->buf_base.push_back(st->mem + off[i]);
   // reset table: buffers with a cache
@@ -333,6 +352,9 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
   st->n_desc = static_cast<int>(desc.size());
   st->reset_items = ritems;
+  st->reset_desc = desc;
+  st->pos.assign(pg.bufs.size(), 0);
+  st->carry_slot = !desc.empty();
   if (!desc.empty()) {
     ck(cudaMalloc(&st->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
     ck(cudaMemcpy(st->d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice),
@@ -369,15 +391,25 @@ CallPlan& State::call_plan(int64_t F) {
     fail(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO,
          "buffer length " + std::to_string(F) + " cannot continue this stream at lag " + std::to_string(D_) +
              " (use one constant length below the compression ratio " + std::to_string(pg.ratio) + ")");
+  // strip positions: a buffer whose cache + new frames would run past its strip wraps first
+  // (its cache moves to the strip start: the carry, once per strip_k calls)
+  std::vector<int64_t> pw(pos);
+  for (size_t b = 0; b < n.size(); ++b) {
+    const int64_t cap = buf_sstride[b] / pg.bufs[b].C;
+    if (pos[b] + cache[b] + (n[b] - N[b]) > cap) pw[b] = 0;
+  }
   std::vector<int64_t> key;
   key.push_back(F);
   key.push_back(row);
   for (size_t b = 0; b < n.size(); ++b) key.push_back(n[b] - N[b]);
   for (const ConvOp& op : pg.ops) key.push_back(op.S > 1 && !op.convt ? N[op.in_buf] % op.S : 0);
+  for (size_t b = 0; b < n.size(); ++b) key.push_back(pos[b]);
   auto it = plans.find(key);
   if (it != plans.end()) return *it->second;
 
   auto cp = std::make_unique<CallPlan>();
+  cp->pos = pw;
+  for (size_t b = 0; b < n.size(); ++b) cp->base.push_back(buf_base[b] + pw[b] * pg.bufs[b].C);
   cp->F = F;
   cp->egress_row = row;
   cp->egress_T = Fs;
@@ -389,25 +421,27 @@ CallPlan& State::call_plan(int64_t F) {
   for (size_t b = 0; b < pg.bufs.size(); ++b)
     if (cache[b] > static_cast<int64_t>(buf_sstride[b] / pg.bufs[b].C) - cp->T[b])
       fail(SC_ERR_INVALID_ARGUMENT, "buffer length exceeds max_frames");
-  // carry table: shift each cached buffer by this call's new frames
+  // carry table (runs first): wrapped buffers move their cache from row pos to the strip start
   std::vector<BufDesc> desc;
   int64_t items = 0;
   for (size_t i = 0; i < pg.bufs.size(); ++i) {
     const BufferSpec& b = pg.bufs[i];
-    if (cache[i] == 0 || cp->T[i] == 0) continue;
+    if (cache[i] == 0 || pw[i] == pos[i]) continue;
     BufDesc d{};
     d.base = buf_base[i];
     d.sstride = buf_sstride[i];
     d.item0 = items;
     d.C = b.C;
     d.cache = static_cast<int>(cache[i]);
-    d.t = static_cast<int>(cp->T[i]);
+    d.t = static_cast<int>(pos[i]);
     items += static_cast<int64_t>(streams) * ((b.C % 4 == 0) ? b.C / 4 : b.C);  // float4 groups
     desc.push_back(d);
   }
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
   cp->n_desc = static_cast<int>(desc.size());
   cp->carry_items = items;
+  cp->n_launch = 2 + (desc.empty() ? 0 : 1);
+  for (int64_t t : cp->t_out) cp->n_launch += t > 0 ? 1 : 0;
   if (!desc.empty()) {
     ck(cudaMalloc(&cp->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
     ck(cudaMemcpy(cp->d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice),
@@ -426,7 +460,7 @@ CallPlan& State::call_plan(int64_t F) {
     const int64_t f0 = c.in_f0;
     const int64_t base_off = f0 % S;
     const uint64_t bufC_view = static_cast<uint64_t>(bi.C) * S;
-    const int64_t frames_avail = buf_sstride[op.in_buf] / bi.C - base_off;
+    const int64_t frames_avail = buf_sstride[op.in_buf] / bi.C - cp->pos[op.in_buf] - base_off;
     const uint64_t rows_view = static_cast<uint64_t>(frames_avail / S);
     TcParams& p = cp->tc[i].p;
     p.BN = d.BN;
@@ -474,7 +508,7 @@ CallPlan& State::call_plan(int64_t F) {
       const char* tr = std::getenv("SC_TC_TRACE_OP");
       if (tr && std::atoi(tr) == static_cast<int>(i)) p.debug |= 32;
     }
-    cp->tc[i].map_a = make_map3(buf_base[op.in_buf] + base_off * bi.C, bufC_view, rows_view, streams,
+    cp->tc[i].map_a = make_map3(cp->base[op.in_buf] + base_off * bi.C, bufC_view, rows_view, streams,
                                 bufC_view * 4, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
                                 static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
     // output rows start at out_base; rows >= t_out and streams >= n_streams are clipped by TMA
@@ -501,7 +535,7 @@ ConvParams State::conv_params(size_t i, const CallPlan& cp) const {
   const BufferSpec& bi = pg.bufs[op.in_buf];
   const BufferSpec& bo = pg.bufs[op.out_buf];
   ConvParams p{};
-  p.in = buf_base[op.in_buf];
+  p.in = cp.base[op.in_buf];
   p.in_sstride = buf_sstride[op.in_buf];
   p.in_fstride = bi.C;
   p.in_off = op.in_off;
@@ -513,7 +547,7 @@ ConvParams State::conv_params(size_t i, const CallPlan& cp) const {
   p.w = plan->dops[i].w;
   p.bias = plan->dops[i].bias;
   p.nout = op.nout;
-  p.out = buf_base[op.out_buf];
+  p.out = cp.base[op.out_buf];
   p.out_sstride = buf_sstride[op.out_buf];
   p.out_base = cache[op.out_buf] * bo.C;
   p.out_rstride = op.out_rstride;
@@ -526,7 +560,7 @@ ConvParams State::conv_params(size_t i, const CallPlan& cp) const {
   p.gate = op.gate ? 1 : 0;
   if (op.res_buf >= 0) {
     const BufferSpec& br = pg.bufs[op.res_buf];
-    p.res = buf_base[op.res_buf];
+    p.res = cp.base[op.res_buf];
     p.res_sstride = buf_sstride[op.res_buf];
     p.res_fstride = br.C;
     p.res_off = op.res_off;
@@ -569,7 +603,7 @@ IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
   const Program& pg = plan->prog;
   IngestArgs a{};
   a.in = in;
-  a.buf = buf_base[0];
+  a.buf = cp.base[0];
   a.sstride = buf_sstride[0];
   a.C = pg.in_C;
   a.T = static_cast<int>(cp.F);
@@ -582,7 +616,7 @@ EgressArgs State::egress_args(float* out, const CallPlan& cp) const {
   const Program& pg = plan->prog;
   const BufferSpec& b = pg.bufs[pg.sink_buf];
   EgressArgs a{};
-  a.buf = buf_base[pg.sink_buf];
+  a.buf = cp.base[pg.sink_buf];
   a.sstride = buf_sstride[pg.sink_buf];
   a.fstride = b.C;
   a.off = pg.sink_off;
@@ -598,7 +632,7 @@ EgressArgs State::egress_args(float* out, const CallPlan& cp) const {
 
 int State::launches(int64_t F) {
   CallPlan& cp = call_plan(F);
-  int n = 2 + (cp.n_desc > 0 ? 1 : 0);
+  int n = 2 + (carry_slot ? 1 : 0);
   for (int64_t t : cp.t_out) n += t > 0 ? 1 : 0;
   return n;
 }
@@ -606,6 +640,7 @@ int State::launches(int64_t F) {
 std::string State::launch_name(int64_t F, int i) {
   CallPlan& cp = call_plan(F);
   int k = 0;
+  if (carry_slot && i == k++) return "carry";
   if (i == k++) return "ingest";
   for (size_t j = 0; j < plan->prog.ops.size(); ++j) {
     if (cp.t_out[j] == 0) continue;
@@ -618,13 +653,16 @@ std::string State::launch_name(int64_t F, int i) {
     }
   }
   if (i == k++) return "egress";
-  if (cp.n_desc > 0 && i == k++) return "carry";
   return "";
 }
 
 void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, cudaEvent_t* ev) {
   int e = 0;
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  if (carry_slot) {  // wrapped buffers first move their cache to the strip start
+    if (cp.n_desc > 0) launch_carry(cp.d_desc, cp.n_desc, streams, cp.carry_items, s);
+    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  }
   launch_ingest(ingest_args(in, cp), s);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
@@ -641,10 +679,6 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
   }
   launch_egress(egress_args(out, cp), s);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
-  if (cp.n_desc > 0) {
-    launch_carry(cp.d_desc, cp.n_desc, streams, cp.carry_items, s);
-    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
-  }
 }
 
 void State::check_frames(int64_t F) const {
@@ -677,6 +711,7 @@ void State::profile(const float* in, float* out, int64_t F, int steps, float* ms
     CallPlan& cp = call_plan(F);
     const bool same = launches(F) == n;
     enqueue(in, out, cp, s, same ? ev.data() + static_cast<size_t>(k) * (n + 1) : nullptr);
+    launched += cp.n_launch;
     advance(F, cp);
     if (same) ++done;
   }
@@ -705,6 +740,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   if (!use_graphs) {
     enqueue(in, out, cp, s, nullptr);
     ck(cudaGetLastError(), "launch");
+    launched += cp.n_launch;
   } else {
     const auto key = std::make_pair(in, out);
     auto it = cp.graphs.find(key);
@@ -766,6 +802,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
     }
     it->second.last_use = ++use_clock;
     ck(cudaGraphLaunch(it->second.exec, s), "GraphLaunch");
+    launched += cp.n_launch;
   }
   advance(F, cp);
   ck(cudaSetDevice(prev), "cudaSetDevice");
@@ -851,6 +888,7 @@ int64_t State::lag_for(int64_t F) const {
 void State::advance(int64_t F, const CallPlan& cp) {
   if (D < 0) D = lag_for(F);
   N = next_counts(F);
+  for (size_t b = 0; b < pos.size(); ++b) pos[b] = cp.pos[b] + cp.T[b];
   E += cp.egress_T;
 }
 
@@ -861,6 +899,7 @@ void State::reset(const int* ids, int n_ids, cudaStream_t s) {
   if (!ids) {
     ck(cudaMemsetAsync(mem, 0, mem_bytes, s), "cudaMemsetAsync");
     std::fill(N.begin(), N.end(), 0);
+    std::fill(pos.begin(), pos.end(), 0);
     E = 0;
     D = -1;
   } else {
@@ -869,6 +908,15 @@ void State::reset(const int* ids, int n_ids, cudaStream_t s) {
       if (ids[i] < 0 || ids[i] >= streams) fail(SC_ERR_INVALID_ARGUMENT, "stream id out of range");
     if (n_ids > 0) {
       ck(cudaMemcpyAsync(d_ids, ids, sizeof(int) * n_ids, cudaMemcpyHostToDevice, s), "copy ids");
+      // the caches currently start at each buffer's strip position
+      std::vector<BufDesc> desc(reset_desc);
+      for (BufDesc& d : desc) {
+        const size_t b = static_cast<size_t>(std::find(buf_base.begin(), buf_base.end(), d.base) - buf_base.begin());
+        d.base += pos[b] * d.C;
+      }
+      if (!desc.empty())
+        ck(cudaMemcpyAsync(d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice, s),
+           "copy reset table");
       launch_reset_streams(d_desc, n_desc, d_ids, n_ids, reset_items, s);
       ck(cudaGetLastError(), "reset launch");
       // the host id array may be reused by the caller after return

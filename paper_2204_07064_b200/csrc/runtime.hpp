@@ -73,9 +73,12 @@ struct CallPlan {
   std::vector<int64_t> t_out; // per op: output rows this call (0: op skipped)
   int64_t egress_row = 0;     // first sink-buffer row emitted this call
   int64_t egress_T = 0;       // sink frames emitted this call
-  BufDesc* d_desc = nullptr;  // carry table (per-buffer shift T)
+  std::vector<int64_t> pos;   // per buffer: strip row where this call's cache starts
+  std::vector<float*> base;   // per buffer: buf_base + pos * C (this call's frame 0 = cache start)
+  BufDesc* d_desc = nullptr;  // carry table (wrapped buffers: cache moved to the strip start)
   int n_desc = 0;
   int64_t carry_items = 0;
+  int n_launch = 0;           // kernels one call of this plan launches
   std::vector<TcLaunch> tc;
   std::map<std::pair<const float*, float*>, GraphEntry> graphs;
 };
@@ -103,6 +106,13 @@ struct State {
   std::map<std::vector<int64_t>, std::unique_ptr<CallPlan>> plans;
   bool phase_mode = false;     // created for buffers shorter than the compression ratio
   std::vector<int64_t> cache;  // per-buffer cache frames of this state
+  // Strips: each buffer holds cache + strip_k x T frames per stream; successive calls slide
+  // the cache start by T instead of copying the cache back (carry only on wrap-around).
+  int strip_k = 1;
+  bool carry_slot = false;     // some buffer has a cache: profile layouts carry a carry slot
+  int64_t launched = 0;        // kernels launched by this state (eager, captured or replayed)
+  std::vector<int64_t> pos;    // per buffer: strip row of the cache start for the next call
+  std::vector<BufDesc> reset_desc;  // host copy of the reset table (bases at strip start)
 
   int64_t lag_for(int64_t F) const;
   void advance(int64_t F, const CallPlan& cp);

@@ -160,6 +160,12 @@ class StreamState:
         check(lib().sc_process_launches(self._h, frames, C.byref(n)))
         return n.value
 
+    def launch_total(self) -> int:
+        """Kernels this state has launched so far (sc_state_launch_total)."""
+        n = C.c_int64()
+        check(lib().sc_state_launch_total(self._h, C.byref(n)))
+        return n.value
+
     def launch_names(self, frames: int):
         """Names of the launches one call of `frames` enqueues ("op<i> <op> [tc|tc-bf16|simt|pqmf]")."""
         return [lib().sc_launch_name(self._h, frames, i).decode() for i in range(self.launches(frames))]

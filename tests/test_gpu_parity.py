@@ -291,3 +291,39 @@ def test_pqmf_fast_form_selected_in_rave_configs(monkeypatch):
         assert not any(n.endswith("[pqmf]") for n in st2.launch_names(parts[0]))
         err, rms = rel_err(y_fast, y_gen)
         assert err <= 2 * FP32_TOL, (cfg, err, rms)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,streams,parts", [(2, 3, [512] * 7), (5, 2, [2048] * 5), (3, 2, [4096, 4096, 8192, 4096])],
+                         ids=["cfg2", "cfg5", "cfg3-ragged"])
+def test_strips_match_oracle(monkeypatch, cfg, streams, parts):
+    """Strip buffers (the cache start slides by T per call, carry only on
+    wrap-around) give the oracle's stream output, bit-identical to the carry-every-call state."""
+    m = configs.build(cfg, seed=cfg)
+    x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=11)
+    monkeypatch.setenv("SC_STRIP_K", "3")
+    y3, _, _ = run_gpu(m, x, parts)
+    monkeypatch.setenv("SC_STRIP_K", "1")
+    y1, _, _ = run_gpu(m, x, parts)
+    assert np.array_equal(y3, y1)
+    if cfg != 5:  # cfg5's oracle parity needs the long warmed-up run of test_config_parity_fp32
+        y_or = po.run(m, x, parts, "stream")
+        err, rms = rel_err(y3, y_or)
+        assert err <= FP32_TOL, (err, rms)
+
+
+@pytest.mark.gpu
+def test_strips_reset_subset(monkeypatch):
+    """Subset reset while the caches sit mid-strip zeroes the live cache rows."""
+    monkeypatch.setenv("SC_STRIP_K", "4")
+    m = configs.build(2, seed=5)
+    x = configs.batch_input(2, range(3), 128, 2048, seed=5)
+    plan = Plan(m)
+    st = StreamState(plan, 3, 512)
+    y_fresh, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan)
+    for k in range(3):  # 3 calls: cache start at row 3 T of the strip
+        run_gpu(m, x, [512], plan=plan, state=st)
+    st.reset([2])
+    y2, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan, state=st)
+    assert np.array_equal(y2[2], y_fresh[2])
+    assert not np.array_equal(y2[0], y_fresh[0])
