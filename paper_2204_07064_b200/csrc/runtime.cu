@@ -86,9 +86,10 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
   if (strided) ok = ok && op.in_off == 0 && op.cin == bi.C && op.d == 1;
   if (!ok) return;
   if (op.gate) {
-    // the output tile (BN/2 columns) must be a whole 32-column TMA box
+    // the output tile (BN/2 columns) is stored as 32-column TMA boxes clipped at the buffer
+    // width: a partial box is only allowed as the last (and only) one
     if (op.nout > 64 && op.nout % 64 != 0) return;
-    d.BN = (op.nout % 128 == 0) ? 128 : 64;
+    d.BN = (op.nout % 128 == 0) ? 128 : (op.nout % 64 == 0) ? 64 : 32;
   } else {
     d.BN = (op.nout % 128 == 0) ? 128 : (op.nout % 64 == 0) ? 64 : 32;
   }
