@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // bf16: main x2
   // bf16: main x2 | A ring of STAGES slots, 16 cols each (32 bf16 per row, two per column)
   constexpr int TS = BF ? STAGES : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
+  static_assert(4 * STAGES + 9 <= 128, "barrier area");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
   constexpr uint32_t COLS_USED = BF ? 2 * BN + 16 * TS : 3 * BN + 64 * TS;
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
@@ -726,6 +727,7 @@ template <int BN, int STAGES, int CK, bool BF>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
   using L = TcSmem<BN, STAGES, BF>;
+  static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -748,38 +750,19 @@ void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, siz
 
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
+  // <BN, STAGES, CK (K-blocks per drained chunk), bf16>: as many stages as shared memory
+  // holds next to the staging tile (narrow tiles are TMA-latency bound, not MMA bound)
   if (p.bf16) {
     switch (p.BN) {
-      case 32: launch_bn<32, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 32: launch_bn<32, 10, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 8, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
       default: launch_bn<128, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;
   }
-  static int ck = -1;
-  if (ck < 0) {
-    const char* e = std::getenv("SC_TC_CK");
-    ck = e ? std::atoi(e) : 1;
-  }
-  if (ck == 2) {
-    switch (p.BN) {
-      case 32: launch_bn<32, 4, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 4, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 3, 2, false>(map_a, map_w, map_out, map_res, p, st); break;
-    }
-    return;
-  }
-  if (ck == 4) {
-    switch (p.BN) {
-      case 32: launch_bn<32, 4, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 4, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 3, 4, false>(map_a, map_w, map_out, map_res, p, st); break;
-    }
-    return;
-  }
   switch (p.BN) {
-    case 32: launch_bn<32, 4, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
-    case 64: launch_bn<64, 4, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
+    case 32: launch_bn<32, 8, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
+    case 64: launch_bn<64, 5, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
     default: launch_bn<128, 3, 1, false>(map_a, map_w, map_out, map_res, p, st); break;
   }
 }
