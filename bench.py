@@ -307,8 +307,12 @@ def main():
             except Exception:
                 pass
     total_flops = 2.0 * plan.macs_per_sample * frames * streams
-    step_roof_ms = max(total_flops / (pk["bf16_sus"] * 1e12),
-                       (in_bytes + out_bytes + streams * (st.cache_bytes * 2)) / (pk["hbm"] * 1e9)) * 1e3
+    step_bytes_min = in_bytes + out_bytes + streams * (st.cache_bytes * 2)
+    step_roof_ms = max(total_flops / (pk["bf16_sus"] * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
+    # the same bound with this precision's tensor ceiling: 3xTF32 issues 3 tf32 MMAs (half
+    # the bf16 rate) per fp32 product, so its ceiling is bf16_sustained / 6
+    path_tf = pk["bf16_sus"] / 6.0 if args.precision == "fp32" else pk["bf16_sus"]
+    step_path_ms = max(total_flops / (path_tf * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -335,7 +339,9 @@ def main():
             "roofline": roof,
             "step_roofline": {"ms": step_roof_ms, "frac": step_roof_ms / (ms / args.steps),
                               "flops_per_step": total_flops,
-                              "note": "whole-step bound max(F/P_bf16_sustained, bytes/HBM)"},
+                              "path_ms": step_path_ms, "frac_of_path_ceiling": step_path_ms / (ms / args.steps),
+                              "note": "whole-step bound max(F/P_bf16_sustained, bytes/HBM); path_ms uses "
+                                      "the precision's tensor ceiling (3xTF32: P_bf16_sustained / 6)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": in_bytes,
                     "d2h_bytes_per_step": out_bytes},
