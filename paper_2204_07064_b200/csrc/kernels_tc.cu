@@ -191,6 +191,16 @@ __device__ __forceinline__ void mma_tf32_ts_w(uint32_t d_tmem, uint32_t a_tmem, 
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_tf32_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
@@ -275,12 +285,26 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 // fp32 (3xTF32) stage: A raw | W hi | W lo, K-major SW128 (32 fp32/row); A hi / lo go to
 //                      TMEM (per-stage columns).
 // bf16 stage:          A raw fp32 (SW128) | A bf16 (SW64, 32 bf16/row) | W bf16 (SW64).
-template <int BN, int STAGES, bool BF = false>
+// window stage (WIN, fp32, narrow tiles): the ring holds only W hi | W lo; two window slots
+// hold the 128 + halo input rows of one 32-channel block as A hi and A lo (SW128), computed
+// once and read by the SS-MMAs of every tap at a row offset (q x tap_rows x 128 B: the
+// swizzle follows absolute address bits, so a descriptor may start at any 128 B row —
+// tools/desc_rowshift_test.cu).
+// The window kernels' weight region (112 KB) holds either a ring of K-slab tiles or, when
+// the layer's whole weight (hi + lo) fits, all of it — loaded once per CTA (p.wres).
+constexpr int WIN_ROWS = 144;  // 128 + halo (<= 16)
+constexpr uint32_t WREG = 112 * 1024;
+template <int BN, int STAGES, bool BF = false, bool WIN = false>
 struct TcSmem {
   static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
-  static constexpr uint32_t STAGE = BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
+  static constexpr uint32_t STAGE = WIN ? 2 * B_TILE : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
+  static constexpr int AST = WIN ? 2 : 0;
+  static constexpr uint32_t WIN_SLOT = 2 * WIN_ROWS * BK * 4;  // hi + lo
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
-  static constexpr uint32_t BYTES = STAGES * STAGE + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
+  static constexpr uint32_t WBYTES = WIN ? WREG : STAGES * STAGE;
+  static constexpr uint32_t BYTES =
+      WBYTES + AST * WIN_SLOT + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
+  static_assert(!WIN || STAGES * STAGE <= WREG, "window ring fits the weight region");
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
@@ -326,35 +350,43 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
   return tc;
 }
 
-template <int BN, int STAGES, int CK, bool BF>
+template <int BN, int STAGES, int CK, bool BF, bool WIN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
-  using L = TcSmem<BN, STAGES, BF>;
+  using L = TcSmem<BN, STAGES, BF, WIN>;
+  static_assert(!(WIN && BF), "window kernels are fp32");
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by an offset from the __shared__ array (not integer pointer math), so
   // the compiler keeps the shared address space: LDS/STS instead of generic LD/ST
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* stg = reinterpret_cast<float*>(smem + STAGES * L::STAGE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE + L::STAGING);
+  uint8_t* wins = smem + L::WBYTES;
+  float* stg = reinterpret_cast<float*>(wins + L::AST * L::WIN_SLOT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wins + L::AST * L::WIN_SLOT + L::STAGING);
   uint64_t* full = bars;
   uint64_t* xform = bars + STAGES;
   uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* tfull = bars + 3 * STAGES;       // [2]
-  uint64_t* tempty = bars + 3 * STAGES + 2;  // [2]
   uint64_t* res_full = bars + 3 * STAGES + 4;
   uint64_t* stg_written = bars + 3 * STAGES + 5;
   uint64_t* stg_free = bars + 3 * STAGES + 6;
-  uint64_t* corr_empty = bars + 3 * STAGES + 7;
   uint64_t* aempty = bars + 3 * STAGES + 8;  // [<= STAGES] TMEM A slots
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 8);
-  float* sbias = reinterpret_cast<float*>(smem + STAGES * L::STAGE + L::STAGING + 1024);  // <= 2048 floats
+  uint64_t* wa_full = bars + 4 * STAGES + 8;    // [2] window rows landed (WIN)
+  uint64_t* wa_ready = bars + 4 * STAGES + 10;  // [2] window hi / lo written (WIN)
+  uint64_t* wa_empty = bars + 4 * STAGES + 12;  // [2] window read by the last tap's MMAs (WIN)
+  uint64_t* tfull = bars + 4 * STAGES + 14;   // [NB] main chunk accumulated
+  uint64_t* tempty = bars + 4 * STAGES + 22;  // [NB] main chunk drained
+  uint64_t* corr_empty = bars + 4 * STAGES + 30;  // [NC] correction accumulator drained
+  uint64_t* wres_full = bars + 4 * STAGES + 32;   // resident weights landed (WIN && p.wres)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 33);
+  float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
-  auto b_hi = [&](int s) { return smem + s * L::STAGE + A_TILE; };
-  auto b_lo = [&](int s) { return smem + s * L::STAGE + A_TILE + L::B_TILE; };
+  auto b_hi = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE); };
+  auto b_lo = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE) + L::B_TILE; };
   auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
+  auto win_hi = [&](int sa) { return wins + sa * L::WIN_SLOT; };
+  auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + WIN_ROWS * BK * 4; };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -366,14 +398,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // bf16: main x2
   // bf16: main x2 | A ring of STAGES slots, 16 cols each (32 bf16 per row, two per column)
   constexpr int TS = BF ? STAGES : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
-  static_assert(4 * STAGES + 9 <= 128, "barrier area");
+  static_assert(4 * STAGES + 34 <= 128, "barrier area");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
-  constexpr uint32_t COLS_USED = BF ? 2 * BN + 16 * TS : 3 * BN + 64 * TS;
+  // chunk accumulators: as many as TMEM holds (<= 8) so the MMAs run ahead of a tile-boundary
+  // epilogue; fp32 window tiles also double-buffer the correction accumulator per tile
+  constexpr int NC = (!BF && WIN) ? 2 : 1;
+  constexpr int OTHER = BF ? 16 * TS : WIN ? NC * BN : BN + 64 * TS;
+  constexpr int NB = (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
+  static_assert(NB >= 2, "two chunk accumulators");
+  constexpr uint32_t COLS_USED = NB * BN + OTHER;
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
-  constexpr uint32_t CORR_COL = 2 * BN;
-  constexpr uint32_t A_COL = BF ? 2 * BN : 3 * BN;
+  constexpr uint32_t CORR_COL = NB * BN;
+  constexpr uint32_t A_COL = BF ? NB * BN : NB * BN + BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -381,15 +419,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&xform[s], 4);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8);
     }
+    for (int b = 0; b < NC; ++b) mbar_init(&corr_empty[b], 8);
+    mbar_init(wres_full, 1);
     mbar_init(res_full, 1);
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
-    mbar_init(corr_empty, 8);
     for (int a = 0; a < STAGES; ++a) mbar_init(&aempty[a], 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&wa_full[a], 1);
+      mbar_init(&wa_ready[a], 4);
+      mbar_init(&wa_empty[a], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -415,7 +459,131 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (WIN && warp == 0) {
+    // ===================== TMA producer, window mode =====================
+    // per 32-channel block: the 128 + halo input rows once (window slot), then per tap the
+    // weight hi / lo tiles into the W ring
+    const int taps = nk / p.cblocks;
+    const uint32_t a_bytes = static_cast<uint32_t>(BK * 4 * (p.R + p.halo));
+    if (p.wres) {  // whole weight resident: slab kb = cb * taps + q at slot kb
+      mbar_expect_tx_w(wres_full, static_cast<uint32_t>(nk) * 2 * L::B_TILE);
+      for (int cb = 0; cb < p.cblocks; ++cb)
+        for (int q = 0; q < taps; ++q) {
+          const int kb = cb * taps + q, kw = (q * p.cblocks + cb) * BK;
+          tma_load_3d_w(&tmap_w, wres_full, b_hi(kb), kw, 0, 0);
+          tma_load_3d_w(&tmap_w, wres_full, b_lo(kb), kw, 0, 1);
+        }
+    }
+    int g = 0, u = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+        const int sa = u & 1;
+        if (u >= 2) mbar_wait(&wa_empty[sa], ((u >> 1) + 1) & 1);
+        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
+        mbar_expect_tx_w(&wa_full[sa], a_bytes);
+        tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
+        if (p.wres) continue;
+        for (int q = 0; q < taps; ++q, ++g) {
+          const int s = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          const int kw = (q * p.cblocks + cb) * BK;
+          mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
+          tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
+          tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
+        }
+      }
+    }
+  } else if (WIN && warp == 1) {
+    // ===================== MMA issuer, window mode (SS-MMAs at a per-tap row offset) ========
+    const uint32_t tbase = warp_uniform(tmem_base);
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                           (static_cast<uint32_t>(BM >> 4) << 24);
+    const int taps = nk / p.cblocks;
+    int g = 0, c = 0, tcount = 0, u = 0;
+    if (p.wres) mbar_wait(wres_full, 0);
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+        const int sa = u & 1;
+        mbar_wait(&wa_ready[sa], (u >> 1) & 1);
+        tc_fence_after();
+        const uint32_t wh = smem_u32(win_hi(sa)), wl = smem_u32(win_lo(sa));
+        for (int q = 0; q < taps; ++q, ++g) {
+          const int kb = cb * taps + q;
+          const int s = g % STAGES;
+          const int b = c % NB;
+          const bool chunk_first = (kb % CK) == 0;
+          const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
+          if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+          if (!p.wres) mbar_wait(&full[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+          const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
+          const int ws = p.wres ? kb : s;
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+          const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+          }
+          const int cbuf = tcount % NC;
+          const uint32_t dcorr = tbase + CORR_COL + static_cast<uint32_t>(cbuf * BN);
+          if (kb == 0 && tcount >= NC) mbar_wait(&corr_empty[cbuf], ((tcount / NC) + 1) & 1);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_w(dcorr, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+            mma_tf32_w(dcorr, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+          }
+          if (!p.wres) mma_commit_w(&empty[s]);
+          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
+          if (chunk_last) {
+            mma_commit_w(&tfull[b]);
+            ++c;
+          }
+        }
+        mma_commit_w(&wa_empty[sa]);
+      }
+    }
+  } else if (WIN && warp >= XF_WARP0 && warp < EP_WARP0) {
+    // ===================== transform, window mode: hi in place, lo to the lo window ==========
+    const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
+    const bool pre_tanh = p.pre_act == ACT_TANH;
+    const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+    const int rows = p.R + p.halo;
+    int u = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+        const int sa = u & 1;
+        mbar_wait(&wa_full[sa], (u >> 1) & 1);
+        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
+        float4* hrow = reinterpret_cast<float4*>(win_hi(sa));
+        float4* lrow = reinterpret_cast<float4*>(win_lo(sa));
+        for (int w = t; w < rows; w += 128) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pj = w * 8 + (j ^ (w & 7));
+            const float4 v = hrow[pj];
+            const float x[4] = {v.x, v.y, v.z, v.w};
+            float h[4], l[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float y = pre_tanh ? tanh_ool(x[k]) : act_lin(x[k], pre_s);
+              h[k] = __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
+              l[k] = y - h[k];
+            }
+            hrow[pj] = make_float4(h[0], h[1], h[2], h[3]);
+            lrow[pj] = make_float4(l[0], l[1], l[2], l[3]);
+          }
+        }
+        fence_proxy_async();  // generic smem writes -> read by the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wa_ready[sa]);
+        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[2 * 256 + u] = clk();
+      }
+    }
+  } else if (warp == 0) {
     // ===================== TMA producer (whole warp, one elected lane issues) =====================
     {
       const uint32_t bytes = static_cast<uint32_t>(BK * 4 * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
@@ -452,10 +620,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
-          const int b = c & 1;
+          const int b = c % NB;
           const bool chunk_first = (kb % CK) == 0;
           const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
-          if (chunk_first && c >= 2) mbar_wait(&tempty[b], ((c >> 1) + 1) & 1);
+          if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
           mbar_wait(&xform[s], (g / STAGES) & 1);
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
           tc_fence_after();
@@ -485,7 +653,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // corrections accumulate over the whole tile in their own buffer (2^-10 of the
             // signal: their truncation is negligible, and the main chunk keeps 4 accumulation
             // steps); wait until the drain has read the previous tile's
-            if (kb == 0 && tcount > 0) mbar_wait(corr_empty, (tcount - 1) & 1);
+            if (kb == 0 && tcount > 0) mbar_wait(&corr_empty[0], (tcount - 1) & 1);
             if (!(p.debug & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) {
@@ -620,8 +788,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
         if (!chunk_last) continue;
         const bool first = (kb / CK) == 0;
-        const int b = c & 1;
-        mbar_wait(&tfull[b], (c >> 1) & 1);
+        const int b = c % NB;
+        mbar_wait(&tfull[b], (c / NB) & 1);
         if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
 #pragma unroll
@@ -638,14 +806,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int cc = 0; cc < COLS; cc += 16) {
             uint32_t v[16];
-            tmem_ld16(lane_base + CORR_COL + static_cast<uint32_t>(cc), v);
+            tmem_ld16(lane_base + CORR_COL + static_cast<uint32_t>((tcount % NC) * BN + cc), v);
             tmem_wait_ld();
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc[cc + u] += __uint_as_float(v[u]);
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(corr_empty);
+          if (lane == 0) mbar_arrive(&corr_empty[tcount % NC]);
         }
         tc_fence_before();
         __syncwarp();
@@ -723,14 +891,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, int CK, bool BF>
+template <int BN, int STAGES, int CK, bool BF, bool WIN = false>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES, BF>;
+  using L = TcSmem<BN, STAGES, BF, WIN>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          L::BYTES);
     attr = true;
   }
@@ -741,7 +909,7 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   }
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
-  conv_tc_kernel<BN, STAGES, CK, BF><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  conv_tc_kernel<BN, STAGES, CK, BF, WIN><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 
 }  // namespace
@@ -758,6 +926,13 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
       case 64: launch_bn<64, 8, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
       default: launch_bn<128, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
     }
+    return;
+  }
+  if (p.win) {  // narrow tiles, every tap from one window (see TcSmem); ring = weight region
+    if (p.BN == 32)
+      launch_bn<32, 14, 1, false, true>(map_a, map_w, map_out, map_res, p, st);
+    else
+      launch_bn<64, 7, 1, false, true>(map_a, map_w, map_out, map_res, p, st);
     return;
   }
   switch (p.BN) {

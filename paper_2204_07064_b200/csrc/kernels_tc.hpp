@@ -20,6 +20,9 @@ struct TcParams {
   int a_c0;             // channel offset of the view
   int a_row0;           // first window row of output row 0
   int a_tap_rows;       // rows between taps
+  int win;              // 1: fp32 narrow tile, A box = 128 + halo rows per 32-channel block
+  int halo;             // (taps - 1) * a_tap_rows
+  int wres;             // 1 (win only): the whole weight (hi + lo) is resident in shared memory
   // epilogue (same meaning as ConvParams)
   int pre_act;
   float pre_alpha;

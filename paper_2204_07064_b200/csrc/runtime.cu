@@ -67,6 +67,11 @@ bool pqmf_disabled() {
   return e && std::atoi(e) != 0;
 }
 
+bool win_disabled() {
+  const char* e = std::getenv("SC_DISABLE_WIN");
+  return e && std::atoi(e) != 0;
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("SC_DISABLE_TC");
   return e && std::atoi(e) != 0;
@@ -483,6 +488,13 @@ CallPlan& State::call_plan(int64_t F) {
     p.a_c0 = S > 1 ? 0 : op.in_off;
     p.a_row0 = static_cast<int>((f0 - base_off) / S);
     p.a_tap_rows = d.tap_rows;
+    // window mode (fp32, BN <= 64, one stream per tile): the transform splits each input row
+    // once per 32-channel block and every tap's MMAs read it at a row offset
+    p.halo = (d.taps_view - 1) * d.tap_rows;
+    p.win = (!d.bf16 && d.BN <= 64 && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= 144 && !win_disabled()) ? 1 : 0;
+    // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
+    p.wres = (p.win && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
+              op.nout == d.BN) ? 1 : 0;
     p.pre_act = c.pre_act;
     p.pre_alpha = c.pre_alpha;
     p.post_act = c.post_act;
@@ -511,7 +523,7 @@ CallPlan& State::call_plan(int64_t F) {
     }
     cp->tc[i].map_a = make_map3(cp->base[op.in_buf] + base_off * bi.C, bufC_view, rows_view, streams,
                                 bufC_view * 4, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
-                                static_cast<uint32_t>(p.R), static_cast<uint32_t>(p.G));
+                                static_cast<uint32_t>(p.R + (p.win ? p.halo : 0)), static_cast<uint32_t>(p.G));
     // output rows start at out_base; rows >= t_out and streams >= n_streams are clipped by TMA
     cp->tc[i].map_out = make_map3(c.out + c.out_base, static_cast<uint64_t>(c.out_rstride),
                                   static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(c.out_rstride) * 4,
