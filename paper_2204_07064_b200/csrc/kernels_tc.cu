@@ -800,7 +800,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int u = 0; u < (COLS >= 32 ? 32 : 16); ++u)
-            acc[cc + u] = first ? __uint_as_float(v[u]) : acc[cc + u] + __uint_as_float(v[u]);
+            // the bias enters with the first chunk (keeps it off the tile-boundary epilogue)
+            acc[cc + u] = first ? __uint_as_float(v[u]) + sbias[tc.n0 + col0 + cc + u] : acc[cc + u] + __uint_as_float(v[u]);
         }
         if (!BF && kb == nk - 1) {  // the tile's corrections (complete with its last chunk)
 #pragma unroll
@@ -835,29 +836,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
           const int n = tc.n0 + col0 + u;
-          const float a = acc[u] + sbias[n];
-          const float gg = acc[u + 1] + sbias[n + 1];
-          stg[stg_off(r, (col0 + u) >> 1)] = gate_ool(a, gg);
+          stg[stg_off(r, (col0 + u) >> 1)] = gate_ool(acc[u], acc[u + 1]);
         }
       } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
+        // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
         const float ps = slope_of(p.post_act, p.post_alpha);
         const float rs = slope_of(p.res_act, p.res_alpha);
+        const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
+        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
 #pragma unroll
         for (int u = 0; u < COLS; u += 4) {
-          const int n = tc.n0 + col0 + u;
-          const float4 bv = *reinterpret_cast<const float4*>(sbias + n);
           float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
           float4 o;
-          o.x = act_lin(acc[u] + bv.x, ps);
-          o.y = act_lin(acc[u + 1] + bv.y, ps);
-          o.z = act_lin(acc[u + 2] + bv.z, ps);
-          o.w = act_lin(acc[u + 3] + bv.w, ps);
+          o.x = lin(acc[u], ps, pmax);
+          o.y = lin(acc[u + 1], ps, pmax);
+          o.z = lin(acc[u + 2], ps, pmax);
+          o.w = lin(acc[u + 3], ps, pmax);
           if (p.res) {
-            const float4 rv = *dst;
-            o.x += act_lin(rv.x, rs);
-            o.y += act_lin(rv.y, rs);
-            o.z += act_lin(rv.z, rs);
-            o.w += act_lin(rv.w, rs);
+            float4 rv = *dst;
+            if (!rid) rv = make_float4(lin(rv.x, rs, rmax), lin(rv.y, rs, rmax), lin(rv.z, rs, rmax), lin(rv.w, rs, rmax));
+            o.x += rv.x;
+            o.y += rv.y;
+            o.z += rv.z;
+            o.w += rv.w;
           }
           *dst = o;
         }
@@ -866,7 +867,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int u = 0; u < COLS; ++u) {
           const int n = tc.n0 + col0 + u;
           float* dst = stg + stg_off(r, col0 + u);
-          float o = act_apply(acc[u] + sbias[n], p.post_act, p.post_alpha);
+          float o = act_apply(acc[u], p.post_act, p.post_alpha);
           if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
           *dst = o;
         }

@@ -67,6 +67,15 @@ bool pqmf_disabled() {
   return e && std::atoi(e) != 0;
 }
 
+int graphs_per_plan() {
+  static int n = 0;
+  if (n == 0) {
+    const char* e = std::getenv("SC_GRAPHS_PER_PLAN");
+    n = std::max(1, e ? std::atoi(e) : 1);
+  }
+  return n;
+}
+
 bool win_disabled() {
   const char* e = std::getenv("SC_DISABLE_WIN");
   return e && std::atoi(e) != 0;
@@ -758,9 +767,11 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
     const auto key = std::make_pair(in, out);
     auto it = cp.graphs.find(key);
     if (it == cp.graphs.end()) {
-      // reuse the least recently used graph once 8 pointer pairs exist
+      // One graph per CallPlan, re-targeted (ingest / egress kernel-node params) when the I/O
+      // pointers change: a capture happens once per CallPlan (the strip cycle's few plans are
+      // all met within the first calls), never again in steady state.
       GraphEntry g;
-      if (cp.graphs.size() >= 8) {
+      if (cp.graphs.size() >= static_cast<size_t>(graphs_per_plan())) {
         auto lru = cp.graphs.begin();
         for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
           if (jt->second.last_use < lru->second.last_use) lru = jt;
