@@ -685,6 +685,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * 4u * p.R * p.G);
           for (int k = 0; k < BN / 32; ++k)
             tma_load_3d(&tmap_res, res_full, stg + k * (BM * 32), p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
+          // warm L2 with the next tile's residual: its load is issued only once this tile's
+          // output has left staging, so it must not also pay the DRAM latency
+          if (tile + static_cast<int>(gridDim.x) < n_tiles && !(p.debug & 4)) {
+            const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n2, BN);
+            for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
+          }
         }
         if (p.debug & 8) continue;
         mbar_wait(stg_written, tcount & 1);

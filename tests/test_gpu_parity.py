@@ -327,3 +327,15 @@ def test_strips_reset_subset(monkeypatch):
     y2, _, _ = run_gpu(m, x[:, :, :512], [512], plan=plan, state=st)
     assert np.array_equal(y2[2], y_fresh[2])
     assert not np.array_equal(y2[0], y_fresh[0])
+
+
+@pytest.mark.gpu
+def test_graph_retarget_with_strips(monkeypatch):
+    """One CUDA graph per call plan, re-targeted as the I/O pointers change every call, across
+    a strip cycle (5 call plans): identical to eager launches."""
+    monkeypatch.setenv("SC_STRIP_K", "3")
+    m = configs.build(4, seed=4)
+    x = configs.batch_input(4, range(3), m.in_channels, 10, seed=4)
+    ya, _, _ = run_gpu(m, x, [1] * 10, graphs=True)
+    yb, _, _ = run_gpu(m, x, [1] * 10, graphs=False)
+    assert np.array_equal(ya, yb)
