@@ -560,22 +560,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
         float4* hrow = reinterpret_cast<float4*>(win_hi(sa));
         float4* lrow = reinterpret_cast<float4*>(win_lo(sa));
-        for (int w = t; w < rows; w += 128) {
+        // (row, 16B chunk) items spread evenly over the 128 threads, all loads issued first;
+        // 8 consecutive items = the 8 chunks of one row: conflict-free 128-bit accesses
+        constexpr int IPT = (WIN_ROWS * 8 + 127) / 128;  // items per thread (9)
+        float4 v[IPT];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int pj = w * 8 + (j ^ (w & 7));
-            const float4 v = hrow[pj];
-            const float x[4] = {v.x, v.y, v.z, v.w};
-            float h[4], l[4];
+        for (int i = 0; i < IPT; ++i) {
+          const int e = t + 128 * i, w = e >> 3;
+          if (w < rows) v[i] = hrow[w * 8 + ((e & 7) ^ (w & 7))];
+        }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float y = pre_tanh ? tanh_ool(x[k]) : act_lin(x[k], pre_s);
-              h[k] = __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
-              l[k] = y - h[k];
-            }
-            hrow[pj] = make_float4(h[0], h[1], h[2], h[3]);
-            lrow[pj] = make_float4(l[0], l[1], l[2], l[3]);
+        for (int i = 0; i < IPT; ++i) {
+          const int e = t + 128 * i, w = e >> 3;
+          if (w >= rows) continue;
+          const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          float h[4], l[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float y = pre_tanh ? tanh_ool(x[k]) : act_lin(x[k], pre_s);
+            h[k] = __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
+            l[k] = y - h[k];
           }
+          const int pj = w * 8 + ((e & 7) ^ (w & 7));
+          hrow[pj] = make_float4(h[0], h[1], h[2], h[3]);
+          lrow[pj] = make_float4(l[0], l[1], l[2], l[3]);
         }
         fence_proxy_async();  // generic smem writes -> read by the tensor core (async proxy)
         __syncwarp();
