@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              if (!(p.debug & 1024)) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
             }
             // corrections accumulate over the whole tile in their own buffer (2^-10 of the
             // signal: their truncation is negligible, and the main chunk keeps 4 accumulation
@@ -700,7 +700,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
           }
         }
-        if (p.debug & 8) continue;
         mbar_wait(stg_written, tcount & 1);
         const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
         for (int k = 0; k < (out_cols + 31) / 32; ++k)
@@ -749,7 +748,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
-        if (!BF && !(p.debug & 512)) {
+        if (!BF) {
           // thread = tile row r (= TMEM lane): SW128 chunk j of row r lives at j ^ (r & 7); hi
           // and lo go to this stage's TMEM A columns (the MMAs read A from TMEM)
           const int quarter = warp & 3;
@@ -839,7 +838,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
       const bool trace = (p.debug & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
-      if (p.debug & 8) continue;
       if (p.res) {
         mbar_wait(res_full, tcount & 1);
       } else if (tcount > 0) {

@@ -45,7 +45,7 @@ struct TcParams {
   int res_act;
   float res_alpha;
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
-  int debug;  // experiments only (SC_TC_DEBUG): 1 skip transform math, 2 main MMA only, 4 skip drain loads
+  int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)
 };
 
 // map_out: output rows (dims out_rstride x t_out x streams, base at the first output row),
