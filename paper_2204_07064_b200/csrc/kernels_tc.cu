@@ -376,7 +376,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* wa_empty = bars + 4 * STAGES + 12;  // [2] window read by the last tap's MMAs (WIN)
   uint64_t* tfull = bars + 4 * STAGES + 14;   // [NB] main chunk accumulated
   uint64_t* tempty = bars + 4 * STAGES + 22;  // [NB] main chunk drained
-  uint64_t* corr_empty = bars + 4 * STAGES + 30;  // [NC] correction accumulator drained
   uint64_t* wres_full = bars + 4 * STAGES + 32;   // resident weights landed (WIN && p.wres)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 33);
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
@@ -393,25 +392,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int nk = p.n_kblocks;
   const int n_tiles_n = (p.nout + BN - 1) / BN;
   const int n_tiles = p.m_tiles * n_tiles_n;
-  // fp32: main x2 (chunk double buffer) | corr (whole tile) | A ring of TS slots, each A hi
-  //       (32 cols) + A lo (32 cols), decoupled from the shared-memory stages
-  // bf16: main x2
-  // bf16: main x2 | A ring of STAGES slots, 16 cols each (32 bf16 per row, two per column)
-  constexpr int TS = BF ? STAGES : ((512 - 3 * BN) / 64 < STAGES ? (512 - 3 * BN) / 64 : STAGES);
+  // TMEM columns: NB chunk accumulators (BN each) | A ring of TS slots — fp32: A hi (32 cols)
+  // + A lo (32 cols) per slot (none in window mode: A is in shared memory); bf16: 16 cols per
+  // slot (32 bf16 per row, two per column).  As many chunk accumulators as fit (<= 8), so the
+  // MMAs run ahead across a tile-boundary epilogue.
+  constexpr int TS = BF ? STAGES : WIN ? 2 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
   static_assert(4 * STAGES + 34 <= 128, "barrier area");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
-  // chunk accumulators: as many as TMEM holds (<= 8) so the MMAs run ahead of a tile-boundary
-  // epilogue; fp32 window tiles also double-buffer the correction accumulator per tile
-  constexpr int NC = (!BF && WIN) ? 2 : 1;
-  constexpr int OTHER = BF ? 16 * TS : WIN ? NC * BN : BN + 64 * TS;
+  constexpr int OTHER = BF ? 16 * TS : WIN ? 0 : 64 * TS;
   constexpr int NB = (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
   static_assert(NB >= 2, "two chunk accumulators");
   constexpr uint32_t COLS_USED = NB * BN + OTHER;
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
-  constexpr uint32_t CORR_COL = NB * BN;
-  constexpr uint32_t A_COL = BF ? NB * BN : NB * BN + BN;
+  constexpr uint32_t A_COL = NB * BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -423,7 +418,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8);
     }
-    for (int b = 0; b < NC; ++b) mbar_init(&corr_empty[b], 8);
     mbar_init(wres_full, 1);
     mbar_init(res_full, 1);
     mbar_init(stg_written, 8);
@@ -522,20 +516,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int ws = p.wres ? kb : s;
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
           const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+          // corrections first (2^-10 of the signal), then the main product, all into this
+          // chunk's accumulator: the truncating accumulation meets the large terms only in
+          // its last four steps (same error as a separate correction accumulator)
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+            mma_tf32_w(dmain, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
           }
-          const int cbuf = tcount % NC;
-          const uint32_t dcorr = tbase + CORR_COL + static_cast<uint32_t>(cbuf * BN);
-          if (kb == 0 && tcount >= NC) mbar_wait(&corr_empty[cbuf], ((tcount / NC) + 1) & 1);
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32_w(dcorr, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
-            mma_tf32_w(dcorr, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
-          }
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
           if (!p.wres) mma_commit_w(&empty[s]);
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
@@ -648,27 +640,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mma_commit_w(&aempty[g % TS]);
           } else {
             // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
-            // shared-memory operand traffic is the weight tile (A never re-read from smem)
+            // shared-memory operand traffic is the weight tile (A never re-read from smem).
+            // Corrections first (2^-10 of the signal), then the main product, all into this
+            // chunk's accumulator: the truncating accumulation meets the large terms only in
+            // its last four steps.
             const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
             const uint32_t ahi = tbase + A_COL + 64 * (g % TS);
             const uint32_t alo = ahi + 32;
-            const uint32_t dcorr = tbase + CORR_COL;
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
-            }
-            // corrections accumulate over the whole tile in their own buffer (2^-10 of the
-            // signal: their truncation is negligible, and the main chunk keeps 4 accumulation
-            // steps); wait until the drain has read the previous tile's
-            if (kb == 0 && tcount > 0) mbar_wait(&corr_empty[0], (tcount - 1) & 1);
             if (!(p.debug & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) {
-                const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-                mma_tf32_ts_w(dcorr, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
-                mma_tf32_ts_w(dcorr, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+                mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
               }
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
+              const uint32_t acc0 = (!chunk_first || kk > 0 || !(p.debug & 2)) ? 1u : 0u;
+              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
             }
             mma_commit_w(&aempty[g % TS]);
           }
@@ -815,19 +805,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int u = 0; u < (COLS >= 32 ? 32 : 16); ++u)
             // the bias enters with the first chunk (keeps it off the tile-boundary epilogue)
             acc[cc + u] = first ? __uint_as_float(v[u]) + sbias[tc.n0 + col0 + cc + u] : acc[cc + u] + __uint_as_float(v[u]);
-        }
-        if (!BF && kb == nk - 1) {  // the tile's corrections (complete with its last chunk)
-#pragma unroll
-          for (int cc = 0; cc < COLS; cc += 16) {
-            uint32_t v[16];
-            tmem_ld16(lane_base + CORR_COL + static_cast<uint32_t>((tcount % NC) * BN + cc), v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int u = 0; u < 16; ++u) acc[cc + u] += __uint_as_float(v[u]);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&corr_empty[tcount % NC]);
         }
         tc_fence_before();
         __syncwarp();
