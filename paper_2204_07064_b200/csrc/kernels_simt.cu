@@ -7,6 +7,7 @@
 //     for every buffer and stream in ONE launch.
 //   * reset_streams: SPEC reset for a subset of streams.
 #include <cuda_runtime.h>
+#include <cstdint>
 
 #include "kernels.hpp"
 
@@ -153,7 +154,40 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
     return;
   }
   __shared__ float tile[TC][TT + 1];
-  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0);
+  const bool in16 = (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;  // caller's pointer
+  if (a.C % 4 == 0 && a.C < TC && a.T % 4 == 0 && in16) {
+    // narrow buffers (4..28 channels): tiles of all C channels x 2048/C frames, float4 on both
+    // sides (a 32-channel tile would be mostly empty and fall back to scalar accesses)
+    float* t2 = &tile[0][0];
+    const int TTs = TC * TT / a.C, LD = TTs + 1, ntt = (a.T + TTs - 1) / TTs;
+    const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt;
+    const int tid = threadIdx.x, nv = a.C * TTs / 4, c4n = a.C / 4;
+    for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+      const int64_t s = tile_id / ntt;
+      const int t0 = static_cast<int>(tile_id - s * ntt) * TTs;
+      const int tn = min(TTs, a.T - t0);
+      for (int e = tid; e < nv; e += 256) {
+        const int c = e / (TTs / 4), t4 = e - c * (TTs / 4);
+        if (4 * t4 < tn) {
+          const float4 v = *reinterpret_cast<const float4*>(a.in + (s * a.C + c) * a.T + t0 + 4 * t4);
+          t2[c * LD + 4 * t4] = v.x;
+          t2[c * LD + 4 * t4 + 1] = v.y;
+          t2[c * LD + 4 * t4 + 2] = v.z;
+          t2[c * LD + 4 * t4 + 3] = v.w;
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < tn * c4n; e += 256) {
+        const int t = e / c4n, c4 = e - t * c4n;
+        const float4 v = make_float4(t2[(4 * c4) * LD + t], t2[(4 * c4 + 1) * LD + t], t2[(4 * c4 + 2) * LD + t],
+                                     t2[(4 * c4 + 3) * LD + t]);
+        *reinterpret_cast<float4*>(a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + 4 * c4) = v;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0) && in16;
   const int ntt = (a.T + TT - 1) / TT, ntc = (a.C + TC - 1) / TC;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
   const int tid = threadIdx.x;
@@ -211,7 +245,38 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
     return;
   }
   __shared__ float tile[TC][TT + 1];
-  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0) && (a.fstride % 4 == 0) && (a.off % 4 == 0);
+  const bool out16 = (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;  // caller's pointer
+  if (a.C % 4 == 0 && a.C < TC && a.T % 4 == 0 && a.fstride % 4 == 0 && a.off % 4 == 0 && out16) {
+    // narrow sinks: all C channels x 2048/C frames per tile (see ingest_kernel)
+    float* t2 = &tile[0][0];
+    const int TTs = TC * TT / a.C, LD = TTs + 1, ntt = (a.T + TTs - 1) / TTs;
+    const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt;
+    const int tid = threadIdx.x, nv = a.C * TTs / 4, c4n = a.C / 4;
+    for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+      const int64_t s = tile_id / ntt;
+      const int t0 = static_cast<int>(tile_id - s * ntt) * TTs;
+      const int tn = min(TTs, a.T - t0);
+      for (int e = tid; e < tn * c4n; e += 256) {
+        const int t = e / c4n, c4 = e - t * c4n;
+        const float4 v = *reinterpret_cast<const float4*>(
+            a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride + a.off + 4 * c4);
+        t2[(4 * c4) * LD + t] = act_apply(v.x, a.act, a.alpha);
+        t2[(4 * c4 + 1) * LD + t] = act_apply(v.y, a.act, a.alpha);
+        t2[(4 * c4 + 2) * LD + t] = act_apply(v.z, a.act, a.alpha);
+        t2[(4 * c4 + 3) * LD + t] = act_apply(v.w, a.act, a.alpha);
+      }
+      __syncthreads();
+      for (int e = tid; e < nv; e += 256) {
+        const int c = e / (TTs / 4), t4 = e - c * (TTs / 4);
+        if (4 * t4 < tn)
+          *reinterpret_cast<float4*>(a.out + (s * a.C + c) * a.T + t0 + 4 * t4) =
+              make_float4(t2[c * LD + 4 * t4], t2[c * LD + 4 * t4 + 1], t2[c * LD + 4 * t4 + 2], t2[c * LD + 4 * t4 + 3]);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const bool vec = (a.T % 4 == 0) && (a.C % 4 == 0) && (a.fstride % 4 == 0) && (a.off % 4 == 0) && out16;
   const int ntt = (a.T + TT - 1) / TT, ntc = (a.C + TC - 1) / TC;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
   const int tid = threadIdx.x;
@@ -359,6 +424,7 @@ void launch_ingest(const IngestArgs& a, cudaStream_t st) {
   if (a.C == 1) {
     ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
   } else {
+    // grid for the generic tiling (the kernel loops over its tiles persistently either way)
     const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + TT - 1) / TT) * ((a.C + TC - 1) / TC);
     ingest_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
   }

@@ -339,3 +339,26 @@ def test_graph_retarget_with_strips(monkeypatch):
     ya, _, _ = run_gpu(m, x, [1] * 10, graphs=True)
     yb, _, _ = run_gpu(m, x, [1] * 10, graphs=False)
     assert np.array_equal(ya, yb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_unaligned_io_pointers(cfg):
+    """Caller buffers that are not 16-byte aligned take the scalar ingest / egress paths and give
+    the same result as aligned ones."""
+    m = configs.build(cfg, seed=cfg)
+    plan = Plan(m)
+    num, den, cout = plan.sink
+    S, F = 2, 4096
+    x = configs.batch_input(cfg, range(S), m.in_channels, F, seed=9)
+    xa = torch.from_numpy(x).cuda()
+    ya = torch.empty((S, cout, F * num // den), device="cuda")
+    StreamState(plan, S, F).process_buffer(xa, ya, F)
+    raw_in = torch.empty(x.size + 1, device="cuda")
+    raw_out = torch.empty(ya.numel() + 1, device="cuda")
+    xu = raw_in[1:].view(x.shape)
+    xu.copy_(xa)
+    yu = raw_out[1:].view(ya.shape)
+    StreamState(plan, S, F).process_buffer(xu, yu, F)
+    torch.cuda.synchronize()
+    assert np.array_equal(yu.cpu().numpy(), ya.cpu().numpy())
