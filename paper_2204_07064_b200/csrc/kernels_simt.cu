@@ -144,12 +144,35 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvParams p) {
 constexpr int TT = 64, TC = 32;
 
 __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
-  if (a.C == 1) {  // mono: contiguous copy per stream
+  if (a.C == 1) {  // mono: contiguous copy per stream (float4 reads when aligned)
+    if (a.T % 4 == 0 && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0) {
+      const int64_t total4 = static_cast<int64_t>(a.streams) * a.T / 4;
+      for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total4;
+           g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = (4 * g) / a.T, t = 4 * g - s * a.T;
+        const float4 v = reinterpret_cast<const float4*>(a.in)[g];
+        float* d = a.buf + s * a.sstride + a.cache + t;
+        d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+      }
+      return;
+    }
     const int64_t total = static_cast<int64_t>(a.streams) * a.T;
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
       const int64_t s = g / a.T, t = g - s * a.T;
       a.buf[s * a.sstride + a.cache + t] = a.in[g];
+    }
+    return;
+  }
+  if (a.T < 16) {  // few frames per call (e.g. one latent frame): frame-major order, coalesced writes
+    const int64_t total = static_cast<int64_t>(a.streams) * a.T * a.C;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t row = g / a.C;
+      const int c = static_cast<int>(g - row * a.C);
+      const int64_t s = row / a.T;
+      const int t = static_cast<int>(row - s * a.T);
+      a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.C + c] = a.in[(s * a.C + c) * a.T + t];
     }
     return;
   }
@@ -235,6 +258,18 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
 
 __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
   if (a.C == 1) {
+    if (a.T % 4 == 0 && a.fstride == 1 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) {  // float4 writes
+      const int64_t total4 = static_cast<int64_t>(a.streams) * a.T / 4;
+      for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total4;
+           g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = (4 * g) / a.T, t = 4 * g - s * a.T;
+        const float* src = a.buf + s * a.sstride + a.cache + t + a.off;
+        reinterpret_cast<float4*>(a.out)[g] =
+            make_float4(act_apply(src[0], a.act, a.alpha), act_apply(src[1], a.act, a.alpha),
+                        act_apply(src[2], a.act, a.alpha), act_apply(src[3], a.act, a.alpha));
+      }
+      return;
+    }
     const int64_t total = static_cast<int64_t>(a.streams) * a.T;
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -423,6 +458,8 @@ const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_k
 void launch_ingest(const IngestArgs& a, cudaStream_t st) {
   if (a.C == 1) {
     ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
+  } else if (a.T < 16) {
+    ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T * a.C, 256), 256, 0, st>>>(a);
   } else {
     // grid for the generic tiling (the kernel loops over its tiles persistently either way)
     const int64_t tiles = static_cast<int64_t>(a.streams) * ((a.T + TT - 1) / TT) * ((a.C + TC - 1) / TC);
