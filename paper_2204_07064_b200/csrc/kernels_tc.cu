@@ -292,19 +292,22 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 // tools/desc_rowshift_test.cu).
 // The window kernels' weight region (112 KB) holds either a ring of K-slab tiles or, when
 // the layer's whole weight (hi + lo) fits, all of it — loaded once per CTA (p.wres).
-constexpr int WIN_ROWS = 144;  // 128 + halo (<= 16)
+constexpr int WIN_ROWS = 144;     // fp32 windows: 128 + halo (<= 16)
+constexpr int WIN_ROWS_BF = 192;  // bf16 windows of narrow tiles: 128 + halo (<= 64)
 constexpr uint32_t WREG = 112 * 1024;
 template <int BN, int STAGES, bool BF = false, bool WIN = false>
 struct TcSmem {
   static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
-  static constexpr uint32_t STAGE = WIN ? 2 * B_TILE : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
-  static constexpr int AST = WIN ? 2 : 0;
-  static constexpr uint32_t WIN_SLOT = 2 * WIN_ROWS * BK * 4;  // hi + lo
+  static constexpr uint32_t STAGE = WIN ? (BF ? B_TILE : 2 * B_TILE) : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
+  // window slots: fp32 = A hi + A lo (SW128); bf16 = the raw fp32 rows + their bf16 copy (SW64)
+  static constexpr int AST = WIN ? (BF ? 3 : 2) : 0;
+  static constexpr int WROWS = (BF && BN < 128) ? WIN_ROWS_BF : WIN_ROWS;
+  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * (4 + 2) : 2 * WROWS * BK * 4;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
-  static constexpr uint32_t WBYTES = WIN ? WREG : STAGES * STAGE;
+  static constexpr uint32_t WBYTES = (WIN && !BF) ? WREG : STAGES * STAGE;
   static constexpr uint32_t BYTES =
       WBYTES + AST * WIN_SLOT + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
-  static_assert(!WIN || STAGES * STAGE <= WREG, "window ring fits the weight region");
+  static_assert(!WIN || BF || STAGES * STAGE <= WREG, "window ring fits the weight region");
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
@@ -356,7 +359,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
   using L = TcSmem<BN, STAGES, BF, WIN>;
-  static_assert(!(WIN && BF), "window kernels are fp32");
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by an offset from the __shared__ array (not integer pointer math), so
   // the compiler keeps the shared address space: LDS/STS instead of generic LD/ST
@@ -371,13 +373,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* stg_written = bars + 3 * STAGES + 5;
   uint64_t* stg_free = bars + 3 * STAGES + 6;
   uint64_t* aempty = bars + 3 * STAGES + 8;  // [<= STAGES] TMEM A slots
-  uint64_t* wa_full = bars + 4 * STAGES + 8;    // [2] window rows landed (WIN)
-  uint64_t* wa_ready = bars + 4 * STAGES + 10;  // [2] window hi / lo written (WIN)
-  uint64_t* wa_empty = bars + 4 * STAGES + 12;  // [2] window read by the last tap's MMAs (WIN)
-  uint64_t* tfull = bars + 4 * STAGES + 14;   // [NB] main chunk accumulated
-  uint64_t* tempty = bars + 4 * STAGES + 22;  // [NB] main chunk drained
-  uint64_t* wres_full = bars + 4 * STAGES + 32;   // resident weights landed (WIN && p.wres)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 33);
+  uint64_t* wa_full = bars + 4 * STAGES + 8;    // [AST] window rows landed (WIN)
+  uint64_t* wa_ready = bars + 4 * STAGES + 12;  // [AST] window hi / lo (bf16 copy) written (WIN)
+  uint64_t* wa_empty = bars + 4 * STAGES + 16;  // [AST] window read by the last tap's MMAs (WIN)
+  uint64_t* tfull = bars + 4 * STAGES + 20;   // [NB] main chunk accumulated
+  uint64_t* tempty = bars + 4 * STAGES + 28;  // [NB] main chunk drained
+  uint64_t* wres_full = bars + 4 * STAGES + 36;   // resident weights landed (WIN && p.wres)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 37);
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
@@ -385,7 +387,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto b_lo = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE) + L::B_TILE; };
   auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
   auto win_hi = [&](int sa) { return wins + sa * L::WIN_SLOT; };
-  auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + WIN_ROWS * BK * 4; };
+  auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // fp32: A lo
+  auto win_bf = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // bf16 copy
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -397,9 +400,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // slot (32 bf16 per row, two per column).  As many chunk accumulators as fit (<= 8), so the
   // MMAs run ahead across a tile-boundary epilogue.
   constexpr int TS = BF ? STAGES : WIN ? 2 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
-  static_assert(4 * STAGES + 34 <= 128, "barrier area");
+  static_assert(4 * STAGES + 38 <= 128, "barrier area");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
-  constexpr int OTHER = BF ? 16 * TS : WIN ? 0 : 64 * TS;
+  constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : 64 * TS;
   constexpr int NB = (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
   static_assert(NB >= 2, "two chunk accumulators");
   constexpr uint32_t COLS_USED = NB * BN + OTHER;
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
     for (int a = 0; a < STAGES; ++a) mbar_init(&aempty[a], 1);
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < (L::AST > 0 ? L::AST : 1); ++a) {
       mbar_init(&wa_full[a], 1);
       mbar_init(&wa_ready[a], 4);
       mbar_init(&wa_empty[a], 1);
@@ -472,8 +475,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
       for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u & 1;
-        if (u >= 2) mbar_wait(&wa_empty[sa], ((u >> 1) + 1) & 1);
+        const int sa = u % L::AST;
+        if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
         if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
         mbar_expect_tx_w(&wa_full[sa], a_bytes);
         tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
@@ -482,9 +485,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
           const int kw = (q * p.cblocks + cb) * BK;
-          mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
+          mbar_expect_tx_w(&full[s], (BF ? 1 : 2) * L::B_TILE);
           tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
-          tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
+          if (!BF) tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
         }
       }
     }
@@ -498,8 +501,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (p.wres) mbar_wait(wres_full, 0);
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u & 1;
-        mbar_wait(&wa_ready[sa], (u >> 1) & 1);
+        const int sa = u % L::AST;
+        mbar_wait(&wa_ready[sa], (u / L::AST) & 1);
         tc_fence_after();
         const uint32_t wh = smem_u32(win_hi(sa)), wl = smem_u32(win_lo(sa));
         for (int q = 0; q < taps; ++q, ++g) {
@@ -512,22 +515,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (!p.wres) mbar_wait(&full[s], (g / STAGES) & 1);
           tc_fence_after();
           const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-          const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
-          const int ws = p.wres ? kb : s;
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
-          const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
-          // corrections first (2^-10 of the signal), then the main product, all into this
-          // chunk's accumulator: the truncating accumulation meets the large terms only in
-          // its last four steps (same error as a separate correction accumulator)
+          if (BF) {  // one bf16 window copy, SW64 rows of 64 B: tap q starts q * tap_rows rows in
+            const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                      (static_cast<uint32_t>(BM >> 4) << 24);
+            const uint32_t offb = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
+            const uint32_t wb = smem_u32(win_bf(sa)), bb = smem_u32(b_hi(s));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-            mma_tf32_w(dmain, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
-            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_bf16_w(dmain, sw64_desc(wb + offb + kk * 32), sw64_desc(bb + kk * 32), idesc_bf, acc0);
+            }
+          } else {
+            const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
+            const int ws = p.wres ? kb : s;
+            if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+            const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+            // corrections first (2^-10 of the signal), then the main product, all into this
+            // chunk's accumulator: the truncating accumulation meets the large terms only in
+            // its last four steps (same error as a separate correction accumulator)
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_tf32_w(dmain, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+              mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk)
+              mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
           }
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
           if (!p.wres) mma_commit_w(&empty[s]);
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
@@ -547,9 +562,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int u = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u & 1;
-        mbar_wait(&wa_full[sa], (u >> 1) & 1);
+        const int sa = u % L::AST;
+        mbar_wait(&wa_full[sa], (u / L::AST) & 1);
         if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
+        if (BF) {
+          // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
+          // (SW64 rows of 64 B, 16B chunk jo at jo ^ ((w >> 1) & 3)); item = (row, output chunk)
+          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
+          uint4* bfr = reinterpret_cast<uint4*>(win_bf(sa));
+          constexpr int IPB = (L::WROWS * 4 + 127) / 128;
+          float4 v[IPB][2];
+#pragma unroll
+          for (int i = 0; i < IPB; ++i) {
+            const int e = t + 128 * i, w = e >> 2, jo = e & 3;
+            if (w < rows) {
+              v[i][0] = raw[w * 8 + ((2 * jo) ^ (w & 7))];
+              v[i][1] = raw[w * 8 + ((2 * jo + 1) ^ (w & 7))];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < IPB; ++i) {
+            const int e = t + 128 * i, w = e >> 2, jo = e & 3;
+            if (w >= rows) continue;
+            float x[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
+            uint32_t pk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float y0 = pre_tanh ? tanh_ool(x[2 * k]) : act_lin(x[2 * k], pre_s);
+              const float y1 = pre_tanh ? tanh_ool(x[2 * k + 1]) : act_lin(x[2 * k + 1], pre_s);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(y0, y1);
+              pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            bfr[w * 4 + (jo ^ ((w >> 1) & 3))] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wa_ready[sa]);
+          continue;
+        }
         float4* hrow = reinterpret_cast<float4*>(win_hi(sa));
         float4* lrow = reinterpret_cast<float4*>(win_lo(sa));
         // (row, 16B chunk) items spread evenly over the 128 threads, all loads issued first;
@@ -910,6 +960,14 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
   // <BN, STAGES, CK (K-blocks per drained chunk), bf16>: as many stages as shared memory
   // holds next to the staging tile (narrow tiles are TMA-latency bound, not MMA bound)
+  if (p.bf16 && p.win) {  // every tap from one bf16 window copy (SS MMAs at a row offset)
+    switch (p.BN) {
+      case 32: launch_bn<32, 12, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 10, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 8, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
   if (p.bf16) {
     switch (p.BN) {
       case 32: launch_bn<32, 10, 4, true>(map_a, map_w, map_out, map_res, p, st); break;

@@ -500,9 +500,10 @@ CallPlan& State::call_plan(int64_t F) {
     // window mode (fp32, BN <= 64, one stream per tile): the transform splits each input row
     // once per 32-channel block and every tap's MMAs read it at a row offset
     p.halo = (d.taps_view - 1) * d.tap_rows;
-    p.win = (!d.bf16 && d.BN <= 64 && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= 144 && !win_disabled()) ? 1 : 0;
+    p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && d.BN < 128) ? 192 : 144) &&
+             !win_disabled()) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
-    p.wres = (p.win && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
+    p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
               op.nout == d.BN) ? 1 : 0;
     p.pre_act = c.pre_act;
     p.pre_alpha = c.pre_alpha;
