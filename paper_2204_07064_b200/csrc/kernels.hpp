@@ -11,8 +11,9 @@ namespace scb {
 struct IngestArgs {
   const float* in;   // [streams][C][T]
   float* buf;        // buffer base
-  int64_t sstride;   // floats per stream in the buffer
+  int64_t sstride;   // 4-byte words per stream in the buffer
   int C, T, cache, streams;
+  int bf;            // 1: the buffer holds bf16 (bf16 plans)
 };
 struct EgressArgs {
   const float* buf;
@@ -21,6 +22,7 @@ struct EgressArgs {
   int act;
   float alpha;
   float* out;        // [streams][C][T]
+  int bf;            // 1: the buffer holds bf16 (bf16 plans)
 };
 
 void launch_ingest(const IngestArgs& a, cudaStream_t st);

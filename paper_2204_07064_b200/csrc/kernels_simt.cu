@@ -7,6 +7,7 @@
 //     for every buffer and stream in ONE launch.
 //   * reset_streams: SPEC reset for a subset of streams.
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -143,6 +144,40 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvParams p) {
 // axis on both sides (frame rows of C floats in the buffer, time rows of T floats outside).
 constexpr int TT = 64, TC = 32;
 
+// Activation buffers are fp32 or (bf16 plans, tensor-core-only buffers) bf16.  `so` is the
+// stream offset in 4-byte words (the buffer strides are kept in words either way); element
+// (row, c) of a row of `fs` elements.
+__device__ __forceinline__ void bput(float* buf, int bf, int64_t so, int64_t row, int fs, int c, float v) {
+  if (bf)
+    reinterpret_cast<__nv_bfloat16*>(buf)[2 * so + row * fs + c] = __float2bfloat16_rn(v);
+  else
+    buf[so + row * fs + c] = v;
+}
+__device__ __forceinline__ void bput4(float* buf, int bf, int64_t so, int64_t row, int fs, int c, float4 v) {
+  if (bf) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(buf) + 2 * so + row * fs + c) = u;
+  } else {
+    *reinterpret_cast<float4*>(buf + so + row * fs + c) = v;
+  }
+}
+__device__ __forceinline__ float bget(const float* buf, int bf, int64_t so, int64_t row, int fs, int c) {
+  if (bf) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf)[2 * so + row * fs + c]);
+  return buf[so + row * fs + c];
+}
+__device__ __forceinline__ float4 bget4(const float* buf, int bf, int64_t so, int64_t row, int fs, int c) {
+  if (bf) {
+    const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(buf) + 2 * so + row * fs + c);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  return *reinterpret_cast<const float4*>(buf + so + row * fs + c);
+}
+
 __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
   if (a.C == 1) {  // mono: contiguous copy per stream (float4 reads when aligned)
     if (a.T % 4 == 0 && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0) {
@@ -151,8 +186,10 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
            g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t s = (4 * g) / a.T, t = 4 * g - s * a.T;
         const float4 v = reinterpret_cast<const float4*>(a.in)[g];
-        float* d = a.buf + s * a.sstride + a.cache + t;
-        d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+        bput(a.buf, a.bf, s * a.sstride, a.cache + t, 1, 0, v.x);
+        bput(a.buf, a.bf, s * a.sstride, a.cache + t + 1, 1, 0, v.y);
+        bput(a.buf, a.bf, s * a.sstride, a.cache + t + 2, 1, 0, v.z);
+        bput(a.buf, a.bf, s * a.sstride, a.cache + t + 3, 1, 0, v.w);
       }
       return;
     }
@@ -160,7 +197,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
       const int64_t s = g / a.T, t = g - s * a.T;
-      a.buf[s * a.sstride + a.cache + t] = a.in[g];
+      bput(a.buf, a.bf, s * a.sstride, a.cache + t, 1, 0, a.in[g]);
     }
     return;
   }
@@ -172,7 +209,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
       const int c = static_cast<int>(g - row * a.C);
       const int64_t s = row / a.T;
       const int t = static_cast<int>(row - s * a.T);
-      a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t) * a.C + c] = a.in[(s * a.C + c) * a.T + t];
+      bput(a.buf, a.bf, s * a.sstride, a.cache + t, a.C, c, a.in[(s * a.C + c) * a.T + t]);
     }
     return;
   }
@@ -204,7 +241,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
         const int t = e / c4n, c4 = e - t * c4n;
         const float4 v = make_float4(t2[(4 * c4) * LD + t], t2[(4 * c4 + 1) * LD + t], t2[(4 * c4 + 2) * LD + t],
                                      t2[(4 * c4 + 3) * LD + t]);
-        *reinterpret_cast<float4*>(a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + 4 * c4) = v;
+        bput4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.C, 4 * c4, v);
       }
       __syncthreads();
     }
@@ -243,13 +280,13 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
         const int e = tid + 256 * k;      // 512 float4 = 64 frames x 8
         const int t = e >> 3, c4 = e & 7;
         const float4 v = make_float4(tile[4 * c4][t], tile[4 * c4 + 1][t], tile[4 * c4 + 2][t], tile[4 * c4 + 3][t]);
-        *reinterpret_cast<float4*>(a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + c0 + 4 * c4) = v;
+        bput4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.C, c0 + 4 * c4, v);
       }
     } else {
       for (int e = tid; e < TC * TT; e += 256) {
         const int t = e / TC, c = e % TC;
         if (t0 + t < a.T && c0 + c < a.C)
-          a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.C + c0 + c] = tile[c][t];
+          bput(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.C, c0 + c, tile[c][t]);
       }
     }
     __syncthreads();
@@ -263,10 +300,12 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
       for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total4;
            g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t s = (4 * g) / a.T, t = 4 * g - s * a.T;
-        const float* src = a.buf + s * a.sstride + a.cache + t + a.off;
+        const int64_t so = s * a.sstride;
         reinterpret_cast<float4*>(a.out)[g] =
-            make_float4(act_apply(src[0], a.act, a.alpha), act_apply(src[1], a.act, a.alpha),
-                        act_apply(src[2], a.act, a.alpha), act_apply(src[3], a.act, a.alpha));
+            make_float4(act_apply(bget(a.buf, a.bf, so, a.cache + t, 1, a.off), a.act, a.alpha),
+                        act_apply(bget(a.buf, a.bf, so, a.cache + t + 1, 1, a.off), a.act, a.alpha),
+                        act_apply(bget(a.buf, a.bf, so, a.cache + t + 2, 1, a.off), a.act, a.alpha),
+                        act_apply(bget(a.buf, a.bf, so, a.cache + t + 3, 1, a.off), a.act, a.alpha));
       }
       return;
     }
@@ -274,8 +313,7 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
     for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
       const int64_t s = g / a.T, t = g - s * a.T;
-      a.out[g] = act_apply(a.buf[s * a.sstride + (a.cache + t) * static_cast<int64_t>(a.fstride) + a.off],
-                           a.act, a.alpha);
+      a.out[g] = act_apply(bget(a.buf, a.bf, s * a.sstride, a.cache + t, a.fstride, a.off), a.act, a.alpha);
     }
     return;
   }
@@ -293,8 +331,7 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
       const int tn = min(TTs, a.T - t0);
       for (int e = tid; e < tn * c4n; e += 256) {
         const int t = e / c4n, c4 = e - t * c4n;
-        const float4 v = *reinterpret_cast<const float4*>(
-            a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride + a.off + 4 * c4);
+        const float4 v = bget4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.fstride, a.off + 4 * c4);
         t2[(4 * c4) * LD + t] = act_apply(v.x, a.act, a.alpha);
         t2[(4 * c4 + 1) * LD + t] = act_apply(v.y, a.act, a.alpha);
         t2[(4 * c4 + 2) * LD + t] = act_apply(v.z, a.act, a.alpha);
@@ -325,8 +362,7 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
       for (int k = 0; k < 2; ++k) {
         const int e = tid + 256 * k;
         const int t = e >> 3, c4 = e & 7;
-        const float4 v = *reinterpret_cast<const float4*>(
-            a.buf + s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride + a.off + c0 + 4 * c4);
+        const float4 v = bget4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.fstride, a.off + c0 + 4 * c4);
         tile[4 * c4][t] = act_apply(v.x, a.act, a.alpha);
         tile[4 * c4 + 1][t] = act_apply(v.y, a.act, a.alpha);
         tile[4 * c4 + 2][t] = act_apply(v.z, a.act, a.alpha);
@@ -336,8 +372,7 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
       for (int e = tid; e < TC * TT; e += 256) {
         const int t = e / TC, c = e % TC;
         tile[c][t] = (t0 + t < a.T && c0 + c < a.C)
-                         ? act_apply(a.buf[s * a.sstride + static_cast<int64_t>(a.cache + t0 + t) * a.fstride +
-                                           a.off + c0 + c],
+                         ? act_apply(bget(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.fstride, a.off + c0 + c),
                                      a.act, a.alpha)
                          : 0.f;
       }

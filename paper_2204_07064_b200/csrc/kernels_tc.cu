@@ -295,14 +295,17 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 constexpr int WIN_ROWS = 144;     // fp32 windows: 128 + halo (<= 16)
 constexpr int WIN_ROWS_BF = 192;  // bf16 windows of narrow tiles: 128 + halo (<= 64)
 constexpr uint32_t WREG = 112 * 1024;
-template <int BN, int STAGES, bool BF = false, bool WIN = false>
+template <int BN, int STAGES, bool BF = false, bool WIN = false, int IOB = 0>
 struct TcSmem {
   static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
   static constexpr uint32_t STAGE = WIN ? (BF ? B_TILE : 2 * B_TILE) : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
   // window slots: fp32 = A hi + A lo (SW128); bf16 = the raw fp32 rows + their bf16 copy (SW64)
   static constexpr int AST = WIN ? (BF ? 3 : 2) : 0;
-  static constexpr int WROWS = (BF && BN < 128) ? WIN_ROWS_BF : WIN_ROWS;
-  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * (4 + 2) : 2 * WROWS * BK * 4;
+  // bf16 windows hold 128 + 64 rows when they fit three slots next to the staging tile (narrow
+  // tiles, or bf16 input rows: a raw bf16 row is half the size)
+  static constexpr bool ABF = BF && (IOB & 1);
+  static constexpr int WROWS = (BF && (BN < 128 || ABF)) ? WIN_ROWS_BF : WIN_ROWS;
+  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * ((ABF ? 2 : 4) + 2) : 2 * WROWS * BK * 4;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
   static constexpr uint32_t WBYTES = (WIN && !BF) ? WREG : STAGES * STAGE;
   static constexpr uint32_t BYTES =
@@ -329,6 +332,11 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 // float offset of (row, col) inside a staging tile of 32-column 128B-swizzled slabs
+// bf16 element offset of (row, col) inside a staging tile of 32-column 64B-swizzled slabs
+__device__ __forceinline__ int stg_off_b(int row, int col) {
+  const int slab = col >> 5, c = col & 31;
+  return slab * (BM * 32) + row * 32 + ((((c >> 3) ^ ((row >> 1) & 3))) << 3) + (c & 7);
+}
 __device__ __forceinline__ int stg_off(int row, int col) {
   const int slab = col >> 5, c = col & 31;
   return slab * (BM * 32) + row * 32 + ((((c >> 2) ^ (row & 7))) << 2) + (c & 3);
@@ -353,12 +361,16 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
   return tc;
 }
 
-template <int BN, int STAGES, int CK, bool BF, bool WIN>
+// IOB (bf16 plans): bit 0 = the input buffer holds bf16, bit 1 = the output (and residual)
+// buffer holds bf16 — compile-time, so each instance carries only its own load / store paths
+template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
-  using L = TcSmem<BN, STAGES, BF, WIN>;
+  using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
+  constexpr bool ABF = BF && (IOB & 1);  // input rows are bf16
+  constexpr bool OBF = BF && (IOB & 2);  // output / residual rows are bf16
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment by an offset from the __shared__ array (not integer pointer math), so
   // the compiler keeps the shared address space: LDS/STS instead of generic LD/ST
@@ -388,7 +400,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
   auto win_hi = [&](int sa) { return wins + sa * L::WIN_SLOT; };
   auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // fp32: A lo
-  auto win_bf = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // bf16 copy
+  auto win_bf = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * (ABF ? 2 : 4); };  // bf16 copy
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -461,7 +473,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // per 32-channel block: the 128 + halo input rows once (window slot), then per tap the
     // weight hi / lo tiles into the W ring
     const int taps = nk / p.cblocks;
-    const uint32_t a_bytes = static_cast<uint32_t>(BK * 4 * (p.R + p.halo));
+    const uint32_t a_bytes = static_cast<uint32_t>(BK * (ABF ? 2 : 4) * (p.R + p.halo));
     if (p.wres) {  // whole weight resident: slab kb = cb * taps + q at slot kb
       mbar_expect_tx_w(wres_full, static_cast<uint32_t>(nk) * 2 * L::B_TILE);
       for (int cb = 0; cb < p.cblocks; ++cb)
@@ -568,8 +580,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (BF) {
           // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
           // (SW64 rows of 64 B, 16B chunk jo at jo ^ ((w >> 1) & 3)); item = (row, output chunk)
-          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
           uint4* bfr = reinterpret_cast<uint4*>(win_bf(sa));
+          if (ABF) {  // the window rows are bf16 already (SW64): pre-activation into the copy
+            const uint4* rawb = reinterpret_cast<const uint4*>(win_hi(sa));
+            for (int e = t; e < rows * 4; e += 128) {
+              const int w = e >> 2, jp = (e & 3) ^ ((w >> 1) & 3);
+              uint4 u = rawb[w * 4 + jp];
+              if (pre_tanh || pre_s != 1.f) {
+                uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[k]));
+                  f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
+                  f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
+                  wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+              }
+              bfr[w * 4 + jp] = u;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wa_ready[sa]);
+            continue;
+          }
+          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
           constexpr int IPB = (L::WROWS * 4 + 127) / 128;
           float4 v[IPB][2];
 #pragma unroll
@@ -636,7 +672,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 0) {
     // ===================== TMA producer (whole warp, one elected lane issues) =====================
     {
-      const uint32_t bytes = static_cast<uint32_t>(BK * 4 * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
+      const uint32_t bytes = static_cast<uint32_t>(BK * (ABF ? 2 : 4) * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
       int g = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
@@ -730,9 +766,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
         const TileCoord tc = tile_coord(p, tile, n_tiles_n2, BN);
         if (p.res) {  // staging is free (previous store read it): bring this tile's residual in
-          mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * 4u * p.R * p.G);
+          const int res_es = OBF ? 2 : 4;  // bytes per residual element (slab = BM x 32 elements)
+          mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * res_es * p.R * p.G);
           for (int k = 0; k < BN / 32; ++k)
-            tma_load_3d(&tmap_res, res_full, stg + k * (BM * 32), p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
+            tma_load_3d(&tmap_res, res_full, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * res_es),
+                        p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
           // warm L2 with the next tile's residual: its load is issued only once this tile's
           // output has left staging, so it must not also pay the DRAM latency
           if (tile + static_cast<int>(gridDim.x) < n_tiles && !(p.debug & 4)) {
@@ -743,7 +781,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(stg_written, tcount & 1);
         const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
         for (int k = 0; k < (out_cols + 31) / 32; ++k)
-          tma_store_3d(&tmap_out, stg + k * (BM * 32), oc0 + 32 * k, tc.i0, tc.s0);
+          tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
+                       tc.i0, tc.s0);
         bulk_commit();
         bulk_wait_read0();
         mbar_arrive(stg_free);
@@ -768,6 +807,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool pre_tanh = p.pre_act == ACT_TANH;
           const float pre_s = slope_of(p.pre_act, p.pre_alpha);
           uint32_t pk[16];
+          if (ABF) {
+            // bf16 buffer: SW64 row of 64 B (16B chunk jb at jb ^ ((r >> 1) & 3)), bf16 pairs
+            const uint4* rowb = reinterpret_cast<const uint4*>(a_hi(s)) + r * 4;
+            const bool ident = !pre_tanh && pre_s == 1.f;
+#pragma unroll
+            for (int jb = 0; jb < 4; ++jb) {
+              const uint4 u = rowb[jb ^ ((r >> 1) & 3)];
+              const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (ident) {
+                  pk[4 * jb + k] = w[k];
+                } else {
+                  float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+                  f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
+                  f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
+                  pk[4 * jb + k] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+              }
+            }
+          }
+          if (!ABF) {
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
             float4 v = row[j4 ^ (r & 7)];
@@ -780,6 +842,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __nv_bfloat162 hi2 = __floats2bfloat162_rn(v.z, v.w);
             pk[2 * j4] = *reinterpret_cast<uint32_t*>(&lo2);
             pk[2 * j4 + 1] = *reinterpret_cast<uint32_t*>(&hi2);
+          }
           }
           const int a = g % TS;
           if (g >= TS) mbar_wait(&aempty[a], ((g / TS) + 1) & 1);  // MMAs of g - TS done
@@ -871,11 +934,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(stg_free, (tcount - 1) & 1);
       }
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
+      __nv_bfloat16* stgb = reinterpret_cast<__nv_bfloat16*>(stg);  // bf16 buffers (bf16 plans)
       if (p.gate) {
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
-          const int n = tc.n0 + col0 + u;
-          stg[stg_off(r, (col0 + u) >> 1)] = gate_ool(acc[u], acc[u + 1]);
+          const float o = gate_ool(acc[u], acc[u + 1]);
+          if (OBF)
+            stgb[stg_off_b(r, (col0 + u) >> 1)] = __float2bfloat16_rn(o);
+          else
+            stg[stg_off(r, (col0 + u) >> 1)] = o;
+        }
+      } else if (OBF && p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
+        // bf16 output (and bf16 residual: a plan never mixes the two on one op), 4 columns per access
+        const float ps = slope_of(p.post_act, p.post_alpha);
+        const float rs = slope_of(p.res_act, p.res_alpha);
+        const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
+        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
+#pragma unroll
+        for (int u = 0; u < COLS; u += 4) {
+          uint2* dst = reinterpret_cast<uint2*>(stgb + stg_off_b(r, col0 + u));
+          float o[4] = {lin(acc[u], ps, pmax), lin(acc[u + 1], ps, pmax), lin(acc[u + 2], ps, pmax),
+                        lin(acc[u + 3], ps, pmax)};
+          if (p.res) {
+            const uint2 rv = *dst;
+            const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.x));
+            const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.y));
+            const float rr[4] = {r0.x, r0.y, r1.x, r1.y};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] += rid ? rr[k] : lin(rr[k], rs, rmax);
+          }
+          __nv_bfloat162 a2 = __floats2bfloat162_rn(o[0], o[1]), b2 = __floats2bfloat162_rn(o[2], o[3]);
+          uint2 w;
+          w.x = *reinterpret_cast<uint32_t*>(&a2);
+          w.y = *reinterpret_cast<uint32_t*>(&b2);
+          *dst = w;
         }
       } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
         // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
@@ -905,10 +997,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < COLS; ++u) {
           const int n = tc.n0 + col0 + u;
-          float* dst = stg + stg_off(r, col0 + u);
           float o = act_apply(acc[u], p.post_act, p.post_alpha);
-          if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
-          *dst = o;
+          if (OBF) {
+            __nv_bfloat16* dst = stgb + stg_off_b(r, col0 + u);
+            if (p.res) o += act_apply(__bfloat162float(*dst), p.res_act, p.res_alpha);
+            *dst = __float2bfloat16_rn(o);
+          } else {
+            float* dst = stg + stg_off(r, col0 + u);
+            if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
+            *dst = o;
+          }
         }
       }
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 2] = clk();
@@ -931,14 +1029,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, int CK, bool BF, bool WIN = false>
+template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES, BF, WIN>;
+  using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          L::BYTES);
     attr = true;
   }
@@ -949,7 +1047,25 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   }
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
-  conv_tc_kernel<BN, STAGES, CK, BF, WIN><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+}
+
+template <int IOB>
+void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
+                 const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
+  if (p.win) {  // every tap from one bf16 window copy (SS MMAs at a row offset)
+    switch (p.BN) {
+      case 32: launch_bn<32, 12, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 10, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 8, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
+  switch (p.BN) {
+    case 32: launch_bn<32, 10, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+    case 64: launch_bn<64, 8, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+    default: launch_bn<128, 6, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+  }
 }
 
 }  // namespace
@@ -958,21 +1074,15 @@ void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, siz
 
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
-  // <BN, STAGES, CK (K-blocks per drained chunk), bf16>: as many stages as shared memory
-  // holds next to the staging tile (narrow tiles are TMA-latency bound, not MMA bound)
-  if (p.bf16 && p.win) {  // every tap from one bf16 window copy (SS MMAs at a row offset)
-    switch (p.BN) {
-      case 32: launch_bn<32, 12, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 10, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 8, 4, true, true>(map_a, map_w, map_out, map_res, p, st); break;
-    }
-    return;
-  }
+  // <BN, STAGES, CK (K-blocks per drained chunk), bf16, window, bf16 I/O>: as many stages as
+  // shared memory holds next to the staging tile (narrow tiles are TMA-latency bound)
   if (p.bf16) {
-    switch (p.BN) {
-      case 32: launch_bn<32, 10, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 8, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 6, 4, true>(map_a, map_w, map_out, map_res, p, st); break;
+    const int iob = (p.a_bf ? 1 : 0) | (p.o_bf ? 2 : 0);
+    switch (iob) {
+      case 0: launch_bf16<0>(map_a, map_w, map_out, map_res, p, st); break;
+      case 1: launch_bf16<1>(map_a, map_w, map_out, map_res, p, st); break;
+      case 2: launch_bf16<2>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bf16<3>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;
   }

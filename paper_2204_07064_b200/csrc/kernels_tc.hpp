@@ -45,6 +45,7 @@ struct TcParams {
   int res_act;
   float res_alpha;
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
+  int a_bf, r_bf, o_bf;  // bf16 plans: input / residual / output buffer holds bf16 (else fp32)
   int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)
 };
 

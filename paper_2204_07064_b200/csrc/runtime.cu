@@ -76,6 +76,11 @@ int graphs_per_plan() {
   return n;
 }
 
+bool bf16_store_disabled() {
+  const char* e = std::getenv("SC_BF16_STORE");
+  return e && std::atoi(e) == 0;  // SC_BF16_STORE=0: keep every buffer fp32 in bf16 plans
+}
+
 bool win_disabled() {
   const char* e = std::getenv("SC_DISABLE_WIN");
   return e && std::atoi(e) != 0;
@@ -250,6 +255,39 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
                             d.BN, 1);
     }
   }
+  // bf16 plans store a buffer as bf16 when every op touching it is a tensor-core op (the bf16
+  // operands are rounded once, by the producer) — halves the activation traffic
+  plan->buf_bf16.assign(plan->prog.bufs.size(), 0);
+  if (precision == SC_PREC_BF16 && !bf16_store_disabled()) {
+    const Program& pg = plan->prog;
+    for (size_t b = 0; b < pg.bufs.size(); ++b) {
+      bool ok = pg.bufs[b].C % 8 == 0;
+      bool touched = b == 0;
+      for (size_t i = 0; i < nops && ok; ++i) {
+        const ConvOp& op = pg.ops[i];
+        const DevOp& d = plan->dops[i];
+        const bool rd = op.in_buf == static_cast<int>(b), rs = op.res_buf == static_cast<int>(b);
+        const bool wr = op.out_buf == static_cast<int>(b);
+        if (!rd && !rs && !wr) continue;
+        touched = true;
+        if (d.kernel != KERNEL_TC) ok = false;
+        if (rd && op.in_off % 8 != 0) ok = false;
+        if (rs && op.res_off % 8 != 0) ok = false;
+        if (wr && op.out_rstride % 8 != 0) ok = false;
+      }
+      plan->buf_bf16[b] = (ok && touched) ? 1 : 0;
+    }
+    // a residual epilogue reads and writes the staging tile in place: its residual and output
+    // buffers must share the element type
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (const ConvOp& op : pg.ops)
+        if (op.res_buf >= 0 && plan->buf_bf16[op.res_buf] != plan->buf_bf16[op.out_buf]) {
+          plan->buf_bf16[op.res_buf] = plan->buf_bf16[op.out_buf] = 0;
+          changed = true;
+        }
+    }
+  }
   plan->desc = plan->prog.describe();
   ck(cudaSetDevice(prev), "cudaSetDevice");
   return plan;
@@ -319,7 +357,7 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   // states keep k = 1 (one CallPlan / graph per buffer length).
   {
     int64_t cache_floats = 0;
-    for (size_t i = 0; i < pg.bufs.size(); ++i) cache_floats += st->cache[i] * pg.bufs[i].C;
+    for (size_t i = 0; i < pg.bufs.size(); ++i) cache_floats += st->cache[i] * plan->fw(i);
     const bool big = cache_floats * 4 * static_cast<int64_t>(streams) >= (int64_t{256} << 20);
     const char* e = std::getenv("SC_STRIP_K");
     st->strip_k = st->phase_mode ? 1 : std::max(1, e ? std::atoi(e) : (big ? 4 : 1));
@@ -334,11 +372,11 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
       const BufferSpec& b = pg.bufs[i];
       // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
       const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
-      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T) * b.C, 32);
+      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T) * plan->fw(i), 32);
       st->buf_sstride.push_back(sstride);
       off.push_back(total);
       total += round_up(sstride * streams, 64);
-      st->cache_bytes_per_stream += st->cache[i] * b.C * 4;
+      st->cache_bytes_per_stream += st->cache[i] * plan->fw(i) * 4;
     }
     st->mem_bytes = total * 4;
     const cudaError_t e = cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256));
@@ -359,9 +397,9 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
     d.base = st->buf_base[i];
     d.sstride = st->buf_sstride[i];
     d.ritem0 = ritems;
-    d.C = b.C;
+    d.C = plan->fw(i);
     d.cache = static_cast<int>(st->cache[i]);
-    ritems += b.C;
+    ritems += plan->fw(i);
     desc.push_back(d);
   }
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
@@ -410,7 +448,7 @@ CallPlan& State::call_plan(int64_t F) {
   // (its cache moves to the strip start: the carry, once per strip_k calls)
   std::vector<int64_t> pw(pos);
   for (size_t b = 0; b < n.size(); ++b) {
-    const int64_t cap = buf_sstride[b] / pg.bufs[b].C;
+    const int64_t cap = buf_sstride[b] / plan->fw(b);
     if (pos[b] + cache[b] + (n[b] - N[b]) > cap) pw[b] = 0;
   }
   std::vector<int64_t> key;
@@ -424,7 +462,7 @@ CallPlan& State::call_plan(int64_t F) {
 
   auto cp = std::make_unique<CallPlan>();
   cp->pos = pw;
-  for (size_t b = 0; b < n.size(); ++b) cp->base.push_back(buf_base[b] + pw[b] * pg.bufs[b].C);
+  for (size_t b = 0; b < n.size(); ++b) cp->base.push_back(buf_base[b] + pw[b] * plan->fw(b));
   cp->F = F;
   cp->egress_row = row;
   cp->egress_T = Fs;
@@ -434,7 +472,7 @@ CallPlan& State::call_plan(int64_t F) {
     cp->t_out.push_back(op.convt ? cp->T[op.in_buf] : cp->T[op.out_buf]);
   }
   for (size_t b = 0; b < pg.bufs.size(); ++b)
-    if (cache[b] > static_cast<int64_t>(buf_sstride[b] / pg.bufs[b].C) - cp->T[b])
+    if (cache[b] > static_cast<int64_t>(buf_sstride[b] / plan->fw(b)) - cp->T[b])
       fail(SC_ERR_INVALID_ARGUMENT, "buffer length exceeds max_frames");
   // carry table (runs first): wrapped buffers move their cache from row pos to the strip start
   std::vector<BufDesc> desc;
@@ -446,10 +484,10 @@ CallPlan& State::call_plan(int64_t F) {
     d.base = buf_base[i];
     d.sstride = buf_sstride[i];
     d.item0 = items;
-    d.C = b.C;
+    d.C = plan->fw(i);
     d.cache = static_cast<int>(cache[i]);
     d.t = static_cast<int>(pos[i]);
-    items += static_cast<int64_t>(streams) * ((b.C % 4 == 0) ? b.C / 4 : b.C);  // float4 groups
+    items += static_cast<int64_t>(streams) * ((d.C % 4 == 0) ? d.C / 4 : d.C);  // float4 groups
     desc.push_back(d);
   }
   if (desc.size() > 64) fail(SC_ERR_UNSUPPORTED_FORMAT, "more than 64 cached buffers");
@@ -475,7 +513,11 @@ CallPlan& State::call_plan(int64_t F) {
     const int64_t f0 = c.in_f0;
     const int64_t base_off = f0 % S;
     const uint64_t bufC_view = static_cast<uint64_t>(bi.C) * S;
-    const int64_t frames_avail = buf_sstride[op.in_buf] / bi.C - cp->pos[op.in_buf] - base_off;
+    const int64_t frames_avail = buf_sstride[op.in_buf] / plan->fw(op.in_buf) - cp->pos[op.in_buf] - base_off;
+    const bool a_bf = plan->buf_bf16[op.in_buf] != 0;
+    const bool o_bf = plan->buf_bf16[op.out_buf] != 0;
+    const bool r_bf = op.res_buf >= 0 && plan->buf_bf16[op.res_buf] != 0;
+    const uint64_t aes = a_bf ? 2 : 4, oes = o_bf ? 2 : 4, res_es = r_bf ? 2 : 4;
     const uint64_t rows_view = static_cast<uint64_t>(frames_avail / S);
     TcParams& p = cp->tc[i].p;
     p.BN = d.BN;
@@ -500,7 +542,7 @@ CallPlan& State::call_plan(int64_t F) {
     // window mode (fp32, BN <= 64, one stream per tile): the transform splits each input row
     // once per 32-channel block and every tap's MMAs read it at a row offset
     p.halo = (d.taps_view - 1) * d.tap_rows;
-    p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && d.BN < 128) ? 192 : 144) &&
+    p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
              !win_disabled()) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
     p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
@@ -531,20 +573,24 @@ CallPlan& State::call_plan(int64_t F) {
       const char* tr = std::getenv("SC_TC_TRACE_OP");
       if (tr && std::atoi(tr) == static_cast<int>(i)) p.debug |= 32;
     }
-    cp->tc[i].map_a = make_map3(cp->base[op.in_buf] + base_off * bi.C, bufC_view, rows_view, streams,
-                                bufC_view * 4, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
-                                static_cast<uint32_t>(p.R + (p.win ? p.halo : 0)), static_cast<uint32_t>(p.G));
-    // output rows start at out_base; rows >= t_out and streams >= n_streams are clipped by TMA
-    cp->tc[i].map_out = make_map3(c.out + c.out_base, static_cast<uint64_t>(c.out_rstride),
-                                  static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(c.out_rstride) * 4,
+    p.a_bf = a_bf ? 1 : 0;
+    p.o_bf = o_bf ? 1 : 0;
+    p.r_bf = r_bf ? 1 : 0;
+    // word (4-byte) offsets into the buffers: a bf16 buffer packs two elements per word
+    cp->tc[i].map_a = make_map3(cp->base[op.in_buf] + base_off * plan->fw(op.in_buf), bufC_view, rows_view, streams,
+                                bufC_view * aes, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
+                                static_cast<uint32_t>(p.R + (p.win ? p.halo : 0)), static_cast<uint32_t>(p.G), a_bf);
+    // output rows start at the cache end; rows >= t_out and streams >= n_streams are clipped by TMA
+    cp->tc[i].map_out = make_map3(c.out + cache[op.out_buf] * plan->fw(op.out_buf), static_cast<uint64_t>(c.out_rstride),
+                                  static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(c.out_rstride) * oes,
                                   static_cast<uint64_t>(c.out_sstride) * 4, 32, static_cast<uint32_t>(p.R),
-                                  static_cast<uint32_t>(p.G));
+                                  static_cast<uint32_t>(p.G), o_bf);
     if (c.res) {
-      cp->tc[i].map_res = make_map3(c.res + static_cast<int64_t>(c.res_f0) * c.res_fstride,
+      cp->tc[i].map_res = make_map3(c.res + static_cast<int64_t>(c.res_f0) * plan->fw(op.res_buf),
                                     static_cast<uint64_t>(c.res_fstride), static_cast<uint64_t>(t_out), streams,
-                                    static_cast<uint64_t>(c.res_fstride) * 4,
+                                    static_cast<uint64_t>(c.res_fstride) * res_es,
                                     static_cast<uint64_t>(c.res_sstride) * 4, 32, static_cast<uint32_t>(p.R),
-                                    static_cast<uint32_t>(p.G));
+                                    static_cast<uint32_t>(p.G), r_bf);
     } else {
       cp->tc[i].map_res = cp->tc[i].map_out;  // unused
     }
@@ -627,6 +673,7 @@ IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
   IngestArgs a{};
   a.in = in;
   a.buf = cp.base[0];
+  a.bf = plan->buf_bf16[0];
   a.sstride = buf_sstride[0];
   a.C = pg.in_C;
   a.T = static_cast<int>(cp.F);
@@ -640,6 +687,7 @@ EgressArgs State::egress_args(float* out, const CallPlan& cp) const {
   const BufferSpec& b = pg.bufs[pg.sink_buf];
   EgressArgs a{};
   a.buf = cp.base[pg.sink_buf];
+  a.bf = plan->buf_bf16[pg.sink_buf];
   a.sstride = buf_sstride[pg.sink_buf];
   a.fstride = b.C;
   a.off = pg.sink_off;

@@ -42,7 +42,9 @@ struct Plan {
   int device = 0;
   float* wmem = nullptr;
   std::vector<DevOp> dops;
+  std::vector<uint8_t> buf_bf16;  // bf16 plans: buffers touched only by tensor-core ops hold bf16
   std::string desc;
+  int fw(size_t b) const { return buf_bf16[b] ? prog.bufs[b].C / 2 : prog.bufs[b].C; }  // words/frame
   ~Plan();
 };
 
