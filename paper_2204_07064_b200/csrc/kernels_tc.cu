@@ -590,11 +590,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                  float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[k]));
-                  f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
-                  f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
-                  __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
-                  wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                  if (!pre_tanh && pre_s < 1.f) {  // exact LeakyReLU on the packed pair
+                    const float lo = __uint_as_float(wv[k] << 16), hi = __uint_as_float(wv[k] & 0xFFFF0000u);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(fmaxf(lo, lo * pre_s), fmaxf(hi, hi * pre_s));
+                    wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                  } else {
+                    float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[k]));
+                    f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
+                    f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
+                    wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                  }
                 }
                 u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
               }
@@ -810,7 +816,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (ABF) {
             // bf16 buffer: SW64 row of 64 B (16B chunk jb at jb ^ ((r >> 1) & 3)), bf16 pairs
             const uint4* rowb = reinterpret_cast<const uint4*>(a_hi(s)) + r * 4;
+            // LeakyReLU on a packed pair, exact: unpack by shifts, max(x, a x) in fp32 (a <= 1),
+            // one round-to-nearest pack (the fp32 route's rounding) — 7 instructions per pair
             const bool ident = !pre_tanh && pre_s == 1.f;
+            const bool pk_lrelu = !pre_tanh && pre_s < 1.f;
 #pragma unroll
             for (int jb = 0; jb < 4; ++jb) {
               const uint4 u = rowb[jb ^ ((r >> 1) & 3)];
@@ -819,6 +828,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int k = 0; k < 4; ++k) {
                 if (ident) {
                   pk[4 * jb + k] = w[k];
+                } else if (pk_lrelu) {
+                  const float lo = __uint_as_float(w[k] << 16), hi = __uint_as_float(w[k] & 0xFFFF0000u);
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(fmaxf(lo, lo * pre_s), fmaxf(hi, hi * pre_s));
+                  pk[4 * jb + k] = *reinterpret_cast<uint32_t*>(&b2);
                 } else {
                   float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
                   f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
