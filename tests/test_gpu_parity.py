@@ -74,8 +74,9 @@ BF16_CORR = 0.9998
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg,streams,parts", [(2, 2, [2048, 2048]), (4, 4, [1] * 8), (5, 2, [2048] * 8)],
-                         ids=["cfg2", "cfg4", "cfg5"])
+@pytest.mark.parametrize("cfg,streams,parts", [(2, 2, [2048, 2048]), (3, 2, [4096, 4096]), (4, 4, [1] * 8),
+                                               (5, 2, [2048] * 8)],
+                         ids=["cfg2", "cfg3", "cfg4", "cfg5"])
 def test_config_parity_bf16(cfg, streams, parts):
     m = configs.build(cfg, seed=cfg)
     x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=cfg)
@@ -362,3 +363,31 @@ def test_unaligned_io_pointers(cfg):
     StreamState(plan, S, F).process_buffer(xu, yu, F)
     torch.cuda.synchronize()
     assert np.array_equal(yu.cpu().numpy(), ya.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_bf16_phase_state_and_reset():
+    """bf16 plans (bf16 activation storage) in phase state (cfg5 B=512) stay within the bf16
+    bounds of the oracle, and a subset reset returns those streams to a fresh start."""
+    m = configs.build(5, seed=5)
+    plan = Plan(m, precision="bf16")
+    r, B = plan.ratio, 512
+    total = 8 * r
+    x = configs.batch_input(5, range(2), m.in_channels, total, seed=5)
+    y_ref = po.run(m, x, [r] * 8, "stream")
+    st = StreamState(plan, 2, B)
+    y_gpu, _, _ = run_gpu(m, x, [B] * (total // B), plan=plan, state=st)
+    D = r - B
+    yg, yo = y_gpu[..., D:], y_ref[..., :total - D]
+    rms = float(np.sqrt(np.mean(yo.astype(np.float64) ** 2)))
+    nrmse = float(np.sqrt(np.mean((yg.astype(np.float64) - yo) ** 2))) / rms
+    assert nrmse <= BF16_NRMSE, nrmse
+    m2 = configs.build(2, seed=5)
+    plan2 = Plan(m2, precision="bf16")
+    x2 = configs.batch_input(2, range(3), 128, 1024, seed=5)
+    st2 = StreamState(plan2, 3, 512)
+    y_fresh, _, _ = run_gpu(m2, x2[:, :, :512], [512], plan=plan2)
+    run_gpu(m2, x2, [512, 512], plan=plan2, state=st2)
+    st2.reset([1])
+    y2, _, _ = run_gpu(m2, x2[:, :, :512], [512], plan=plan2, state=st2)
+    assert np.array_equal(y2[1], y_fresh[1])
