@@ -191,6 +191,117 @@ SC_API const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t
 /* Enable/disable CUDA-graph replay (default on). */
 SC_API int sc_state_set_graphs(sc_state* state, int32_t enabled);
 
+/* ---- SPEC graph_ir: general DAGs ------------------------------------
+ * The reference's model description is a DAG of typed nodes (SPEC NodeKind)
+ * joined by ordered (from, to, input port) edges.  Node ids are the array
+ * indices (dense integers); edge order into a Sum is its operand order.  Every
+ * node has exactly one output edge except FANOUT (`arity`) and SINK (none); every input port
+ * (SUM: 0..arity-1, SINK and the others: 0, SOURCE: none) has exactly one incoming edge.
+ * GATE and SLICE are builder extensions of SPEC's kinds (the RAVE head, the mean/var split). */
+enum sc_gnode_kind {
+  SC_G_SOURCE = 0,         /* Source; out_channels = channels (0: the in_channels argument)   */
+  SC_G_SINK = 1,           /* Sink                                                            */
+  SC_G_CONV = 2,           /* Conv{kernel, stride, dilation, padding}        kernels.cpp:73  */
+  SC_G_ZERO_UPSAMPLE = 3,  /* ZeroUpsample{factor}                           kernels.cpp:106 */
+  SC_G_ACTIVATION = 4,     /* Activation{kind}                               kernels.cpp:119 */
+  SC_G_DELAY = 5,          /* Delay{samples >= 0}     */
+  SC_G_SUM = 6,            /* Sum{arity >= 2}: in_0 + in_1 + ... in port order                */
+  SC_G_FANOUT = 7,         /* Fanout{arity >= 2}                                              */
+  SC_G_GATE = 8,           /* extension: y[c] = tanh(x[c]) * sigmoid(x[c + C/2])              */
+  SC_G_SLICE = 9           /* extension: keep channels [slice_begin, slice_begin+slice_count) */
+};
+
+typedef struct sc_gnode {
+  int32_t kind;          /* enum sc_gnode_kind */
+  int32_t in_channels;   /* CONV: M */
+  int32_t out_channels;  /* CONV: N;  SOURCE: channels (0 = the in_channels argument) */
+  int32_t taps;          /* CONV: K */
+  int32_t stride;        /* CONV: S */
+  int32_t dilation;      /* CONV: d */
+  int64_t pad_left;      /* CONV: PaddingSpec{left,right} (tensor.hpp:90-95) */
+  int64_t pad_right;
+  int64_t shift;         /* CONV: right pad already folded into the left pad by causalize —
+                            the output delay the rewrite introduced (ledger R) */
+  int32_t factor;        /* ZERO_UPSAMPLE: s */
+  int32_t act;           /* ACTIVATION: enum sc_act */
+  float alpha;           /* ACTIVATION: leaky_relu slope */
+  int32_t arity;         /* SUM / FANOUT */
+  int64_t samples;       /* DELAY: d, at the node's native rate */
+  int64_t weight_offset; /* CONV: float offset of weights[N][M][K] then bias[N] */
+  int32_t slice_begin;   /* SLICE */
+  int32_t slice_count;   /* SLICE */
+  int32_t hint;          /* CONV: enum sc_hint */
+  int32_t inserted;      /* DELAY: 1 if inserted by causalize (D_a or A_i), else 0 */
+} sc_gnode;
+
+typedef struct sc_edge {
+  int32_t from;          /* producing node id */
+  int32_t to;            /* consuming node id */
+  int32_t port;          /* input port of `to` */
+} sc_edge;
+
+/* SPEC validate: returns SC_OK iff every GraphIR invariant holds, else
+ * CycleDetected / ChannelMismatch / RateMismatchAtSum / DanglingNode / MalformedGraph /
+ * InvalidArgument / SchemaError naming the offending node id.  edge_rates (optional,
+ * [n_edges][2]) receives the RateMap: edge rate num/den relative to the Source. */
+SC_API int sc_graph_validate(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                             int32_t n_edges, int32_t in_channels, int64_t* edge_rates,
+                             int32_t* out_channels);
+/* SPEC compression_ratio: the streaming buffer granularity — the lcm of
+ * every edge rate's denominator (= the denominator of the minimum rate ratio on any
+ * Source->Sink path for the stride / upsample products SPEC lists). */
+SC_API int sc_graph_compression_ratio(const sc_gnode* nodes, int32_t n_nodes,
+                                      const sc_edge* edges, int32_t n_edges,
+                                      int32_t in_channels, int64_t* ratio);
+/* SPEC receptive_field: past / future extents in input samples by interval
+ * propagation (Conv with padding (L,R) adds its span, Delay shifts, Sum / Fanout take the
+ * union); extents are rounded up to whole input samples, future is clamped at 0.  An output
+ * frame of a stride-S conv stands at the last input frame it consumes (streaming emits it
+ * then), so a streamable strided conv (pad >= span - S, all on the left) has future 0. */
+SC_API int sc_graph_receptive_field(const sc_gnode* nodes, int32_t n_nodes,
+                                    const sc_edge* edges, int32_t n_edges, int32_t in_channels,
+                                    int64_t* past, int64_t* future);
+/* SPEC causalize as a graph-to-graph rewrite: every Conv pad (L,R) becomes
+ * (L+R, 0) with shift += R; Delay(D_a) nodes (Eq. 2) are inserted before strided convs and
+ * Delay(A_i) nodes (branch_alignment) on Sum inputs; ids of original nodes are kept, new
+ * Delay nodes are appended.  Caps are the capacities of the output arrays (n_nodes + n_edges
+ * nodes and 2 x n_edges edges always suffice).  latency = total latency in input samples. */
+SC_API int sc_graph_causalize(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                              int32_t n_edges, int32_t in_channels, sc_gnode* out_nodes,
+                              int32_t node_cap, int32_t* n_out_nodes, sc_edge* out_edges,
+                              int32_t edge_cap, int32_t* n_out_edges, int64_t* latency);
+/* SPEC latency_of: NotCausal if the graph's future receptive field is > 0,
+ * else its Sink cumulated delay in input samples.  The ledger counts the delay
+ * causalize introduces — conv R + shift, and Delay nodes marked `inserted` — but not a Delay
+ * of the model itself, which shifts the original and the causalized graph alike (counting it
+ * would break offline_run(causalize(g)) == shift(offline_run(g), latency)). */
+SC_API int sc_graph_latency(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                            int32_t n_edges, int32_t in_channels, int64_t* samples);
+/* sc_plan_create for a DAG: validate + causalize + lower to the fused cached-conv program.
+ * ZeroUpsample must feed a stride-1, dilation-1 Conv (lowered to a polyphase ConvTranspose);
+ * a Sum becomes the residual epilogue of a conv branch when one operand is a conv output
+ * with nothing else reading it, else one SIMT sum launch; Delays become read offsets. */
+SC_API int sc_plan_create_graph(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                                int32_t n_edges, const float* weights_host, int64_t n_weights,
+                                int32_t in_channels, int32_t precision, int32_t device,
+                                sc_plan** out);
+
+/* ---- SPEC model_io: JSON manifest + raw little-endian f32 blob --------
+ * Manifest schema: docs in INTEGRATION.md §model_io.  `blob_path` NULL = the manifest path
+ * with its extension replaced by ".bin" (paired files share a basename).
+ * Errors: VersionMismatch, CorruptBlob (blob size / weight ranges), SchemaError with the JSON
+ * path of the offending value, plus every sc_graph_validate error. */
+typedef struct sc_model sc_model;
+SC_API int sc_model_load(const char* manifest_path, const char* blob_path, sc_model** out);
+/* Arrays owned by the model (valid until sc_model_destroy). */
+SC_API int sc_model_graph(const sc_model* model, const sc_gnode** nodes, int32_t* n_nodes,
+                          const sc_edge** edges, int32_t* n_edges, const float** weights,
+                          int64_t* n_weights, int32_t* in_channels);
+SC_API int sc_model_destroy(sc_model* model);
+SC_API int sc_model_save(const char* manifest_path, const char* blob_path, const sc_gnode* nodes,
+                         int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                         const float* weights, int64_t n_weights, int32_t in_channels);
+
 /* ---- tensor_core ops on device batches (kernels.hpp:16-32) ----------------------------- */
 /* conv1d (kernels.cpp:73-104) over a batch: x [batch][M][L] -> y [batch][N][Lout],
  * Lout = (L - ((K-1)d+1))/S + 1 (kernels.cpp:46-49).  w/b device, reference layout.      */

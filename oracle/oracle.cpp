@@ -485,7 +485,369 @@ int guard(F&& f) {
   }
 }
 
+// ---------------------------------------------------------------- SPEC graph_ir DAGs
+// A second, independent restatement for general DAGs: the graph is
+// validated minimally (the product's sc_graph_validate is tested separately), causalized as a
+// literal graph-to-graph rewrite — pads (L,R) -> (L+R,0), Delay(D_a) nodes before strided
+// convs (Eq. 2), Delay(A_i) nodes on Sum inputs (branch_alignment) — and executed node by
+// node in topological order: Conv caches / Delay rings per node in streaming mode
+// (SPEC.md:255-280), zero-prepend + truncate offline.
+struct DagG {
+  std::vector<sc_gnode> nd;       // causalized nodes (original ids kept, inserted appended)
+  std::vector<int64_t> L0, R0;    // original pads per node (OFFLINE_ORIGINAL)
+  std::vector<sc_edge> ed;
+  std::vector<std::vector<int>> in_e, out_e;
+  std::vector<int> order;
+  std::vector<int> slot;          // state slot per node (-1: none)
+  std::vector<int> slot_C;
+  std::vector<int64_t> slot_len;
+  int in_C = 1, out_C = 1;
+  Rate sink;
+  int64_t ratio = 1, latency_in = 0, state_bytes = 0;
+};
+
+int d_inputs(const sc_gnode& g) { return g.kind == SC_G_SOURCE ? 0 : g.kind == SC_G_SUM ? g.arity : 1; }
+
+void dag_topo(DagG& g) {
+  const int n = static_cast<int>(g.nd.size());
+  g.in_e.assign(n, {});
+  g.out_e.assign(n, {});
+  for (int i = 0; i < n; ++i) g.in_e[i].assign(d_inputs(g.nd[i]), -1);
+  for (size_t e = 0; e < g.ed.size(); ++e) {
+    const sc_edge& x = g.ed[e];
+    if (x.from < 0 || x.from >= n || x.to < 0 || x.to >= n || x.port < 0 ||
+        x.port >= static_cast<int>(g.in_e[x.to].size()) || g.in_e[x.to][x.port] >= 0)
+      throw OracleError(SC_ERR_MALFORMED_GRAPH, "bad edge");
+    g.in_e[x.to][x.port] = static_cast<int>(e);
+    g.out_e[x.from].push_back(static_cast<int>(e));
+  }
+  std::vector<int> done(n, 0);
+  g.order.clear();
+  for (bool progress = true; progress;) {
+    progress = false;
+    for (int i = 0; i < n; ++i) {
+      if (done[i]) continue;
+      bool ready = true;
+      for (int e : g.in_e[i]) ready = ready && e >= 0 && done[g.ed[e].from];
+      if (ready) {
+        done[i] = 1;
+        g.order.push_back(i);
+        progress = true;
+      }
+    }
+  }
+  if (static_cast<int>(g.order.size()) != n) throw OracleError(SC_ERR_CYCLE_DETECTED, "cycle");
+}
+
+void dag_build(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
+               int64_t nW, int in_C, DagG& g) {
+  (void)W;  // weights are read by dag_pass; here only their ranges are checked
+  g.nd.assign(nodes, nodes + n);
+  g.ed.assign(edges, edges + ne);
+  g.in_C = in_C;
+  dag_topo(g);
+  // rates, channels and the ledger on the ORIGINAL graph
+  std::vector<int> C(ne, 0);
+  std::vector<Rate> rate(ne);
+  std::vector<int64_t> D(ne, 0), ins(ne, 0);
+  for (int u : g.order) {
+    const sc_gnode& x = g.nd[u];
+    int c = in_C;
+    Rate r;
+    int64_t d = 0;
+    if (x.kind != SC_G_SOURCE) {
+      const int e0 = g.in_e[u][0];
+      c = C[e0];
+      r = rate[e0];
+      d = D[e0];
+    }
+    switch (x.kind) {
+      case SC_G_CONV: {
+        if (x.in_channels != c) throw OracleError(SC_ERR_CHANNEL_MISMATCH, "conv channels");
+        const int64_t need = static_cast<int64_t>(x.out_channels) * x.in_channels * x.taps + x.out_channels;
+        if (x.weight_offset < 0 || x.weight_offset + need > nW) throw OracleError(SC_ERR_INVALID_ARGUMENT, "weights");
+        const int64_t R = x.pad_right + x.shift;
+        const int64_t span = static_cast<int64_t>(x.taps - 1) * x.dilation + 1;
+        const int64_t P = x.pad_left + x.pad_right;
+        if (x.stride == 1 ? P != span - 1 : P < span - x.stride)
+          throw OracleError(SC_ERR_PADDING_NOT_STREAMABLE, "conv padding");
+        if (x.stride > 1) {
+          const int64_t Da = oc_delay_for_stride(x.stride, R, d);  // Eq. (2)
+          ins[g.in_e[u][0]] = Da;
+          d = (d + R + Da) / x.stride;
+          r.den *= x.stride;
+        } else {
+          d += R;
+        }
+        c = x.out_channels;
+        break;
+      }
+      case SC_G_ZERO_UPSAMPLE:
+        d *= x.factor;
+        r.num *= x.factor;
+        break;
+      case SC_G_DELAY:
+        if (x.inserted) d += x.samples;  // a model Delay shifts original and causal alike
+        break;
+      case SC_G_SUM: {
+        for (int q = 0; q < x.arity; ++q) {
+          const int e = g.in_e[u][q];
+          if (C[e] != c) throw OracleError(SC_ERR_CHANNEL_MISMATCH, "sum channels");
+          if (rate[e].num * r.den != r.num * rate[e].den) throw OracleError(SC_ERR_RATE_MISMATCH_AT_SUM, "sum rates");
+          d = std::max(d, D[e]);
+        }
+        for (int q = 0; q < x.arity; ++q) ins[g.in_e[u][q]] = d - D[g.in_e[u][q]];  // A_i
+        break;
+      }
+      case SC_G_GATE:
+        c /= 2;
+        break;
+      case SC_G_SLICE:
+        if (x.slice_begin < 0 || x.slice_count < 1 || x.slice_begin + x.slice_count > c)
+          throw OracleError(SC_ERR_CHANNEL_MISMATCH, "slice");
+        c = x.slice_count;
+        break;
+      case SC_G_SINK:
+        g.out_C = c;
+        g.sink = r;
+        g.latency_in = d * r.den / r.num;
+        break;
+      default:
+        break;
+    }
+    r.norm();
+    for (int e : g.out_e[u]) {
+      C[e] = c;
+      rate[e] = r;
+      D[e] = d;
+      g.ratio = std::lcm(g.ratio, r.den);
+    }
+  }
+  // the causalize rewrite: inserted Delay nodes on their edges, causal pads
+  g.L0.assign(n, 0);
+  g.R0.assign(n, 0);
+  for (int i = 0; i < n; ++i) {
+    sc_gnode& x = g.nd[i];
+    g.L0[i] = x.pad_left;
+    g.R0[i] = x.pad_right;
+    if (x.kind == SC_G_CONV) {
+      x.pad_left += x.pad_right;
+      x.pad_right = 0;
+    }
+  }
+  std::vector<sc_edge> ed2;
+  for (int e = 0; e < ne; ++e) {
+    if (ins[e] == 0) {
+      ed2.push_back(g.ed[e]);
+      continue;
+    }
+    sc_gnode dl{};
+    dl.kind = SC_G_DELAY;
+    dl.samples = ins[e];
+    dl.inserted = 1;
+    dl.in_channels = C[e];
+    const int id = static_cast<int>(g.nd.size());
+    g.nd.push_back(dl);
+    g.L0.push_back(0);
+    g.R0.push_back(0);
+    ed2.push_back(sc_edge{g.ed[e].from, id, 0});
+    ed2.push_back(sc_edge{id, g.ed[e].to, g.ed[e].port});
+  }
+  g.ed.swap(ed2);
+  dag_topo(g);
+  // state slots: conv caches (causal pad at the conv's input rate), Delay rings
+  std::vector<int> C2(g.ed.size(), 0);
+  g.slot.assign(g.nd.size(), -1);
+  for (int u : g.order) {
+    const sc_gnode& x = g.nd[u];
+    int c = x.kind == SC_G_SOURCE ? in_C : C2[g.in_e[u][0]];
+    int64_t len = 0;
+    if (x.kind == SC_G_CONV) {
+      len = x.pad_left;
+      g.slot[u] = static_cast<int>(g.slot_C.size());
+      g.slot_C.push_back(c);
+      g.slot_len.push_back(len);
+      c = x.out_channels;
+    } else if (x.kind == SC_G_DELAY) {
+      len = x.samples;
+      g.slot[u] = static_cast<int>(g.slot_C.size());
+      g.slot_C.push_back(c);
+      g.slot_len.push_back(len);
+    } else if (x.kind == SC_G_GATE) {
+      c /= 2;
+    } else if (x.kind == SC_G_SLICE) {
+      c = x.slice_count;
+    }
+    if (g.slot[u] >= 0) g.state_bytes += static_cast<int64_t>(g.slot_C[g.slot[u]]) * len * 4;
+    for (int e : g.out_e[u]) C2[e] = c;
+  }
+}
+
+// One pass of the DAG over a buffer (STREAM) or a whole signal (offline modes).
+Sig dag_pass(const DagG& g, const float* W, Sig x, StreamState* st, Mode mode, conv_fn_t fn) {
+  std::vector<Sig> val(g.ed.size());
+  Sig out;
+  for (int u : g.order) {
+    const sc_gnode& nd = g.nd[u];
+    Sig v;
+    if (nd.kind == SC_G_SOURCE) {
+      v = std::move(x);
+    } else if (nd.kind != SC_G_SUM) {
+      v = val[g.in_e[u][0]];
+    }
+    switch (nd.kind) {
+      case SC_G_CONV: {
+        const float* w = W + nd.weight_offset;
+        const float* b = w + static_cast<int64_t>(nd.out_channels) * nd.in_channels * nd.taps;
+        const int S = nd.stride;
+        int64_t Tout = v.T / S;
+        Sig xin;
+        if (mode == STREAM) {
+          Sig& cache = st->slot[g.slot[u]];
+          const int64_t n_prev = st->n_in[g.slot[u]];
+          const int64_t n_now = n_prev + v.T;
+          Tout = n_now / S - n_prev / S;
+          st->n_in[g.slot[u]] = n_now;
+          xin = concat_time(cache, v);
+          const int64_t keep = nd.pad_left + (n_now % S);
+          cache = slice_time(xin, xin.T - keep, keep);
+          if (Tout == 0) {
+            v = Sig(nd.out_channels, 0);
+            break;
+          }
+        } else if (mode == OFFLINE_CAUSAL) {
+          xin = pad_zeros(v, nd.pad_left, 0);
+        } else {
+          xin = pad_zeros(v, g.L0[u], g.R0[u]);
+        }
+        Sig y = conv(fn, xin, nd.out_channels, nd.taps, S, nd.dilation, w, b);
+        if (y.T < Tout) throw OracleError(SC_ERR_INPUT_TOO_SHORT, "conv produced too few");
+        v = (y.T == Tout) ? std::move(y) : slice_time(y, 0, Tout);
+        break;
+      }
+      case SC_G_ZERO_UPSAMPLE:
+        v = zero_upsample(v, nd.factor);
+        break;
+      case SC_G_ACTIVATION:
+        activation_inplace(v, nd.act, nd.alpha);
+        break;
+      case SC_G_DELAY:
+        if (mode == OFFLINE_ORIGINAL && nd.inserted) break;  // absent from the original graph
+        v = run_delay(v, nd.samples, (mode == STREAM && nd.samples > 0) ? &st->slot[g.slot[u]] : nullptr);
+        break;
+      case SC_G_SUM: {
+        v = val[g.in_e[u][0]];
+        for (int q = 1; q < nd.arity; ++q) {
+          const Sig& o = val[g.in_e[u][q]];
+          if (o.T != v.T || o.C != v.C) throw OracleError(SC_ERR_LENGTH_MISMATCH, "sum operands differ in length");
+          for (size_t i = 0; i < v.d.size(); ++i) v.d[i] = v.d[i] + o.d[i];  // port order
+        }
+        break;
+      }
+      case SC_G_GATE: {
+        const int H = v.C / 2;
+        Sig y(H, v.T);
+        for (int c = 0; c < H; ++c)
+          for (int64_t t = 0; t < v.T; ++t)
+            y.ch(c)[t] = std::tanh(v.ch(c)[t]) * (1.0f / (1.0f + std::exp(-v.ch(c + H)[t])));
+        v = std::move(y);
+        break;
+      }
+      case SC_G_SLICE: {
+        Sig y(nd.slice_count, v.T);
+        for (int c = 0; c < nd.slice_count; ++c) std::memcpy(y.ch(c), v.ch(nd.slice_begin + c), sizeof(float) * v.T);
+        v = std::move(y);
+        break;
+      }
+      case SC_G_SINK:
+        out = v;
+        break;
+      default:
+        break;
+    }
+    for (int e : g.out_e[u]) val[e] = v;
+  }
+  return out;
+}
+
 }  // namespace
+
+extern "C" {
+
+// DAG versions of oc_graph_info / oc_run (same conventions, sc_gnode / sc_edge graphs).
+int oc_dag_info(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
+                int64_t nW, int in_C, int64_t* info) {
+  return guard([&] {
+    DagG g;
+    dag_build(nodes, n, edges, ne, W, nW, in_C, g);
+    info[0] = g.ratio;
+    info[1] = g.sink.num;
+    info[2] = g.sink.den;
+    info[3] = g.out_C;
+    info[4] = g.latency_in;
+    info[5] = g.state_bytes;
+  });
+}
+
+int oc_dag_run(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
+               int64_t nW, int in_C, int n_streams, const float* x, int64_t T_total,
+               const int64_t* parts, int n_parts, float* y, int mode, void* conv_fn, int threads) {
+  return guard([&] {
+    DagG g;
+    dag_build(nodes, n, edges, ne, W, nW, in_C, g);
+    conv_fn_t fn = conv_fn ? reinterpret_cast<conv_fn_t>(conv_fn) : g_default_conv;
+    const bool phase = mode == 3;
+    if (phase) mode = 0;
+    int64_t sum = 0;
+    for (int p = 0; p < n_parts; ++p) {
+      if (parts[p] <= 0 || (!phase && parts[p] % g.ratio != 0))
+        throw OracleError(SC_ERR_BUFFER_NOT_MULTIPLE_OF_RATIO, "buffer not multiple of ratio");
+      sum += parts[p];
+    }
+    if (mode != 0 && T_total % g.ratio != 0)
+      throw OracleError(SC_ERR_LENGTH_NOT_MULTIPLE_OF_RATIO, "length not multiple of ratio");
+    if (mode == 0 && sum != T_total) throw OracleError(SC_ERR_LENGTH_MISMATCH, "parts do not sum to length");
+    const int64_t Tout_total = T_total * g.sink.num / g.sink.den;
+    std::vector<std::string> errs(n_streams);
+    std::vector<int> codes(n_streams, 0);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads > 0 ? threads : omp_get_max_threads())
+    for (int s = 0; s < n_streams; ++s) {
+      try {
+        const float* xs = x + static_cast<size_t>(s) * in_C * T_total;
+        float* ys = y + static_cast<size_t>(s) * g.out_C * Tout_total;
+        if (mode == 0) {
+          StreamState st;
+          for (size_t k = 0; k < g.slot_C.size(); ++k) st.slot.emplace_back(g.slot_C[k], g.slot_len[k]);
+          st.n_in.assign(g.slot_C.size(), 0);
+          int64_t t0 = 0, o0 = 0;
+          for (int p = 0; p < n_parts; ++p) {
+            Sig buf(in_C, parts[p]);
+            for (int c = 0; c < in_C; ++c)
+              std::memcpy(buf.ch(c), xs + static_cast<size_t>(c) * T_total + t0, sizeof(float) * parts[p]);
+            Sig out = dag_pass(g, W, std::move(buf), &st, STREAM, fn);
+            for (int c = 0; c < g.out_C; ++c)
+              std::memcpy(ys + static_cast<size_t>(c) * Tout_total + o0, out.ch(c), sizeof(float) * out.T);
+            t0 += parts[p];
+            o0 += out.T;
+          }
+        } else {
+          Sig buf(in_C, T_total);
+          std::memcpy(buf.d.data(), xs, sizeof(float) * in_C * T_total);
+          Sig out = dag_pass(g, W, std::move(buf), nullptr, mode == 1 ? OFFLINE_CAUSAL : OFFLINE_ORIGINAL, fn);
+          if (out.T != Tout_total) throw OracleError(SC_ERR_LENGTH_MISMATCH, "sink length");
+          std::memcpy(ys, out.d.data(), sizeof(float) * out.d.size());
+        }
+      } catch (const OracleError& e) {
+        errs[s] = e.what();
+        codes[s] = e.code;
+      }
+    }
+    for (int s = 0; s < n_streams; ++s)
+      if (codes[s]) throw OracleError(codes[s], errs[s]);
+  });
+}
+
+}  // extern "C"
 
 extern "C" {
 

@@ -49,6 +49,11 @@ def oracle() -> C.CDLL:
         L.oc_activation.argtypes = [F32P, C.c_int64, C.c_int, C.c_float, F32P]
         L.oc_activation.restype = None
         L.oc_graph_info.argtypes = [C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int, I64P]
+        L.oc_dag_info.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int,
+                                  I64P]
+        L.oc_dag_run.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int,
+                                 C.c_int, F32P, C.c_int64, I64P, C.c_int, F32P, C.c_int, C.c_void_p,
+                                 C.c_int]
         L.oc_run.argtypes = [C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int, C.c_int, F32P,
                              C.c_int64, I64P, C.c_int, F32P, C.c_int, C.c_void_p, C.c_int]
         _o = L
@@ -150,7 +155,20 @@ def branch_alignment(D):
 
 
 # ----------------------------------------------------------------------- stream runtime
+def _is_dag(model) -> bool:
+    return hasattr(model, "edges")
+
+
 def graph_info(model) -> dict:
+    if _is_dag(model):
+        nodes, n, edges, ne, w = model.pack()
+        info = np.zeros(6, np.int64)
+        st = oracle().oc_dag_info(C.cast(nodes, C.c_void_p), n, C.cast(edges, C.c_void_p), ne, _fp(w),
+                                  w.size, model.in_channels, info.ctypes.data_as(I64P))
+        if st:
+            raise OracleError(st, oracle().oc_last_error().decode())
+        return dict(ratio=int(info[0]), sink_num=int(info[1]), sink_den=int(info[2]),
+                    out_channels=int(info[3]), latency_in=int(info[4]), state_bytes=int(info[5]))
     nodes, n, w = model.pack()
     info = np.zeros(6, np.int64)
     st = oracle().oc_graph_info(C.cast(nodes, C.c_void_p), n, _fp(w), w.size, model.in_channels,
@@ -166,7 +184,22 @@ MODES = {"stream": 0, "offline": 1, "offline_original": 2, "phase": 3}
 
 def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = False,
         threads: int = 0) -> np.ndarray:
-    """x: [streams][in_C][T].  Returns [streams][out_C][T*sink]."""
+    """x: [streams][in_C][T].  Returns [streams][out_C][T*sink].  `model`: a flat Model or a
+    SPEC DAG (graph.Graph, run by the oracle's independent DAG restatement)."""
+    if _is_dag(model):
+        nodes, n, edges, ne, w = model.pack()
+        x = np.ascontiguousarray(x, np.float32)
+        S, Cin, T = x.shape
+        info = graph_info(model)
+        y = np.zeros((S, info["out_channels"], T * info["sink_num"] // info["sink_den"]), np.float32)
+        p = np.ascontiguousarray([T] if parts is None else parts, np.int64)
+        fn = C.cast(ref().ref_conv1d, C.c_void_p) if use_ref else None
+        st = oracle().oc_dag_run(C.cast(nodes, C.c_void_p), n, C.cast(edges, C.c_void_p), ne, _fp(w),
+                                 w.size, model.in_channels, S, _fp(x), T, p.ctypes.data_as(I64P),
+                                 p.size, _fp(y), MODES[mode], fn, threads)
+        if st:
+            raise OracleError(st, oracle().oc_last_error().decode())
+        return y
     nodes, n, w = model.pack()
     x = np.ascontiguousarray(x, np.float32)
     S, Cin, T = x.shape

@@ -51,6 +51,29 @@ class SCNode(C.Structure):
     ]
 
 
+(G_SOURCE, G_SINK, G_CONV, G_ZERO_UPSAMPLE, G_ACTIVATION, G_DELAY, G_SUM, G_FANOUT, G_GATE,
+ G_SLICE) = range(10)
+GKIND_NAMES = ["Source", "Sink", "Conv", "ZeroUpsample", "Activation", "Delay", "Sum", "Fanout",
+               "Gate", "Slice"]
+
+
+class SCGNode(C.Structure):
+    """sc_gnode: one SPEC graph_ir node."""
+    _fields_ = [
+        ("kind", C.c_int32), ("in_channels", C.c_int32), ("out_channels", C.c_int32),
+        ("taps", C.c_int32), ("stride", C.c_int32), ("dilation", C.c_int32),
+        ("pad_left", C.c_int64), ("pad_right", C.c_int64), ("shift", C.c_int64),
+        ("factor", C.c_int32), ("act", C.c_int32), ("alpha", C.c_float), ("arity", C.c_int32),
+        ("samples", C.c_int64), ("weight_offset", C.c_int64), ("slice_begin", C.c_int32),
+        ("slice_count", C.c_int32), ("hint", C.c_int32), ("inserted", C.c_int32),
+    ]
+
+
+class SCEdge(C.Structure):
+    """sc_edge: (from, to, input port)."""
+    _fields_ = [("from_", C.c_int32), ("to", C.c_int32), ("port", C.c_int32)]
+
+
 _LIB = None
 
 _SIGS = {
@@ -61,6 +84,31 @@ _SIGS = {
     "sc_branch_alignment": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int64)]),
     "sc_plan_create": (C.c_int, [C.POINTER(SCNode), C.c_int32, C.POINTER(C.c_float), C.c_int64,
                                  C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "sc_plan_create_graph": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                       C.POINTER(C.c_float), C.c_int64, C.c_int32, C.c_int32,
+                                       C.c_int32, C.POINTER(C.c_void_p)]),
+    "sc_graph_validate": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                    C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "sc_graph_compression_ratio": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge),
+                                             C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "sc_graph_receptive_field": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge),
+                                           C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64)]),
+    "sc_graph_causalize": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                     C.c_int32, C.POINTER(SCGNode), C.c_int32,
+                                     C.POINTER(C.c_int32), C.POINTER(SCEdge), C.c_int32,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "sc_graph_latency": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                   C.c_int32, C.POINTER(C.c_int64)]),
+    "sc_model_load": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "sc_model_graph": (C.c_int, [C.c_void_p, C.POINTER(C.POINTER(SCGNode)), C.POINTER(C.c_int32),
+                                 C.POINTER(C.POINTER(SCEdge)), C.POINTER(C.c_int32),
+                                 C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int32)]),
+    "sc_model_destroy": (C.c_int, [C.c_void_p]),
+    "sc_model_save": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(SCGNode), C.c_int32,
+                                C.POINTER(SCEdge), C.c_int32, C.POINTER(C.c_float), C.c_int64,
+                                C.c_int32]),
     "sc_plan_destroy": (C.c_int, [C.c_void_p]),
     "sc_plan_ratio": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_plan_sink_rate": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),

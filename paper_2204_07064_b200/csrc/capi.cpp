@@ -92,6 +92,114 @@ int sc_plan_create(const sc_node* nodes, int32_t n_nodes, const float* weights_h
   });
 }
 
+int sc_plan_create_graph(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                         int32_t n_edges, const float* weights_host, int64_t n_weights,
+                         int32_t in_channels, int32_t precision, int32_t device, sc_plan** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    *out = nullptr;
+    auto p = scb::make_plan_dag(nodes, n_nodes, edges, n_edges, weights_host, n_weights, in_channels,
+                                precision, device);
+    *out = new sc_plan{std::move(p)};
+  });
+}
+
+int sc_graph_validate(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                      int32_t in_channels, int64_t* edge_rates, int32_t* out_channels) {
+  return guard([&] {
+    const scb::DagInfo g = scb::dag_validate(nodes, n_nodes, edges, n_edges, in_channels);
+    if (edge_rates)
+      for (int e = 0; e < n_edges; ++e) {
+        edge_rates[2 * e] = g.edge_rate[e].num;
+        edge_rates[2 * e + 1] = g.edge_rate[e].den;
+      }
+    if (out_channels) *out_channels = g.out_C;
+  });
+}
+
+int sc_graph_compression_ratio(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                               int32_t n_edges, int32_t in_channels, int64_t* ratio) {
+  return guard([&] {
+    need(ratio != nullptr, "ratio is null");
+    *ratio = scb::dag_validate(nodes, n_nodes, edges, n_edges, in_channels).ratio;
+  });
+}
+
+int sc_graph_receptive_field(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                             int32_t n_edges, int32_t in_channels, int64_t* past, int64_t* future) {
+  return guard([&] {
+    need(past && future, "null argument");
+    scb::dag_receptive_field(nodes, n_nodes, edges, n_edges, in_channels, past, future);
+  });
+}
+
+int sc_graph_causalize(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                       int32_t in_channels, sc_gnode* out_nodes, int32_t node_cap, int32_t* n_out_nodes,
+                       sc_edge* out_edges, int32_t edge_cap, int32_t* n_out_edges, int64_t* latency) {
+  return guard([&] {
+    std::vector<sc_gnode> on;
+    std::vector<sc_edge> oe;
+    const int64_t lat = scb::dag_causalize(nodes, n_nodes, edges, n_edges, in_channels, &on, &oe);
+    if (latency) *latency = lat;
+    if (n_out_nodes) *n_out_nodes = static_cast<int32_t>(on.size());
+    if (n_out_edges) *n_out_edges = static_cast<int32_t>(oe.size());
+    if (out_nodes || out_edges) {
+      need(out_nodes && out_edges && static_cast<size_t>(node_cap) >= on.size() &&
+               static_cast<size_t>(edge_cap) >= oe.size(),
+           "causalize: output arrays too small");
+      std::copy(on.begin(), on.end(), out_nodes);
+      std::copy(oe.begin(), oe.end(), out_edges);
+    }
+  });
+}
+
+int sc_graph_latency(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                     int32_t in_channels, int64_t* samples) {
+  return guard([&] {
+    need(samples != nullptr, "samples is null");
+    int64_t past = 0, future = 0;
+    scb::dag_receptive_field(nodes, n_nodes, edges, n_edges, in_channels, &past, &future);
+    if (future > 0)
+      scb::fail(SC_ERR_NOT_CAUSAL, "the graph sees " + std::to_string(future) +
+                                       " future input samples: causalize it first (SPEC.md:218-226)");
+    *samples = scb::dag_causalize(nodes, n_nodes, edges, n_edges, in_channels, nullptr, nullptr);
+  });
+}
+
+int sc_model_load(const char* manifest_path, const char* blob_path, sc_model** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    *out = nullptr;
+    *out = scb::model_load(manifest_path, blob_path).release();
+  });
+}
+
+int sc_model_graph(const sc_model* m, const sc_gnode** nodes, int32_t* n_nodes, const sc_edge** edges,
+                   int32_t* n_edges, const float** weights, int64_t* n_weights, int32_t* in_channels) {
+  return guard([&] {
+    need(m != nullptr, "model is null");
+    if (nodes) *nodes = m->nodes.data();
+    if (n_nodes) *n_nodes = static_cast<int32_t>(m->nodes.size());
+    if (edges) *edges = m->edges.data();
+    if (n_edges) *n_edges = static_cast<int32_t>(m->edges.size());
+    if (weights) *weights = m->weights.data();
+    if (n_weights) *n_weights = static_cast<int64_t>(m->weights.size());
+    if (in_channels) *in_channels = m->in_channels;
+  });
+}
+
+int sc_model_destroy(sc_model* m) {
+  return guard([&] { delete m; });
+}
+
+int sc_model_save(const char* manifest_path, const char* blob_path, const sc_gnode* nodes, int32_t n_nodes,
+                  const sc_edge* edges, int32_t n_edges, const float* weights, int64_t n_weights,
+                  int32_t in_channels) {
+  return guard([&] {
+    scb::model_save(manifest_path, blob_path, nodes, n_nodes, edges, n_edges, weights, n_weights, in_channels);
+  });
+}
+
 int sc_plan_destroy(sc_plan* plan) {
   return guard([&] { delete plan; });
 }

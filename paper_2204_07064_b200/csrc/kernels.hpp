@@ -33,6 +33,28 @@ const void* egress_kernel_ptr();
 // Generic SIMT cached conv (FFMA, fp32 accumulate): narrow layers and the v0 dense path.
 void launch_conv_simt(const ConvParams& p, cudaStream_t st);
 
+// SPEC Sum that no conv epilogue absorbed: for every stream s, row t < t_out and
+// channel c < C:  out(s, t)[c] = post( sum_q act_q(in_q(s, in_f0[q] + t)[in_off[q] + c]) ),
+// operands added left to right in port order (fp32), frame-major buffers as in ConvParams.
+constexpr int kMaxSumIn = 8;
+struct SumParams {
+  int n_in;
+  const float* in[kMaxSumIn];
+  int64_t in_sstride[kMaxSumIn];
+  int in_fstride[kMaxSumIn];
+  int in_off[kMaxSumIn];
+  int in_f0[kMaxSumIn];     // row of output row 0 (cache - delay)
+  int act[kMaxSumIn];
+  float alpha[kMaxSumIn];
+  float* out;
+  int64_t out_sstride;
+  int64_t out_base;         // cache * C
+  int C, t_out, streams;
+  int post_act;
+  float post_alpha;
+};
+void launch_sum(const SumParams& p, cudaStream_t st);
+
 // Batched cache carry: for every buffer with cache > 0, frames [T, T+cache) -> [0, cache)
 // for every stream.  `items` = sum over buffers of streams*C (precomputed).
 void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, cudaStream_t st);

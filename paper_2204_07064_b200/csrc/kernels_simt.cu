@@ -477,6 +477,30 @@ __global__ void relayout_w_kernel(const float* __restrict__ w, int N, int M, int
   }
 }
 
+// SPEC Sum over frame-major buffers (kernels.hpp SumParams): one thread per output element,
+// consecutive threads on consecutive channels of a frame (coalesced rows in and out).
+__global__ void __launch_bounds__(256) sum_kernel(const SumParams p) {
+  const int64_t total = static_cast<int64_t>(p.streams) * p.t_out * p.C;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(e % p.C);
+    const int64_t st = e / p.C;
+    const int t = static_cast<int>(st % p.t_out);
+    const int64_t s = st / p.t_out;
+    float acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < kMaxSumIn; ++q) {
+      if (q >= p.n_in) break;
+      const float v = act_apply(
+          p.in[q][s * p.in_sstride[q] + static_cast<int64_t>(p.in_f0[q] + t) * p.in_fstride[q] + p.in_off[q] + c],
+          p.act[q], p.alpha[q]);
+      acc = (q == 0) ? v : acc + v;  // left to right in port order, like the oracle's Sum
+    }
+    p.out[s * p.out_sstride + p.out_base + static_cast<int64_t>(t) * p.C + c] =
+        act_apply(acc, p.post_act, p.post_alpha);
+  }
+}
+
 int grid_for(int64_t items, int threads) {
   int64_t g = (items + threads - 1) / threads;
   const int64_t cap = 148 * 32;
@@ -523,6 +547,11 @@ void launch_conv_simt(const ConvParams& p, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>((M + 255) / 256), (p.nout + 15) / 16);
     conv_simt_kernel<256, 16, 4, 4><<<grid, 256, 0, st>>>(p);
   }
+}
+
+void launch_sum(const SumParams& p, cudaStream_t st) {
+  if (p.t_out <= 0 || p.streams <= 0) return;
+  sum_kernel<<<grid_for(static_cast<int64_t>(p.streams) * p.t_out * p.C, 256), 256, 0, st>>>(p);
 }
 
 void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, cudaStream_t st) {

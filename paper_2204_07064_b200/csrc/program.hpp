@@ -1,6 +1,7 @@
 // program.hpp — a causalized model lowered to frame buffers and fused cached-conv ops.
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -18,8 +19,21 @@ struct BufferSpec {
   std::string name;
 };
 
-// One fused cached-convolution launch (see ConvParams in common.hpp for the exact formula).
+// One input of a Sum launch (OPK_SUM): rows `cache - delay + t` of buffer `buf`, channels
+// [off, off + C), with a pending activation applied on load.
+struct SumIn {
+  int buf = 0, off = 0, act = ACT_ID;
+  float alpha = 0.f;
+  int64_t delay = 0;
+};
+
+enum OpKind { OPK_CONV = 0, OPK_SUM = 1 };
+
+// One fused cached-convolution launch (see ConvParams in common.hpp for the exact formula), or
+// one SPEC Sum that no conv epilogue could absorb (kind OPK_SUM: out = post(sum_i in_i)).
 struct ConvOp {
+  int kind = OPK_CONV;
+  std::vector<SumIn> sum_in;  // OPK_SUM operands in port order
   bool convt = false;        // polyphase ConvTranspose1d
   int in_buf = 0, in_off = 0, cin = 0;
   int out_buf = 0;
@@ -55,6 +69,7 @@ struct Program {
   std::vector<BufferSpec> bufs;  // bufs[0] = source (ingest target)
   std::vector<ConvOp> ops;
   int sink_buf = 0, sink_off = 0, sink_C = 1, sink_act = ACT_ID;
+  int64_t sink_delay = 0;     // a Delay in front of the Sink: egress reads rows cache - delay + t
   float sink_alpha = 0.f;
   Rate sink_rate;
   int64_t ratio = 1;          // SPEC compression_ratio
@@ -68,4 +83,38 @@ struct Program {
 Program lower_graph(const sc_node* nodes, int n_nodes, const float* W, int64_t n_weights,
                     int in_C);
 
+// SPEC graph_ir DAG (include/streamconv_b200.h sc_gnode / sc_edge): analyses and lowering.
+struct DagInfo {
+  std::vector<int> order;           // topological node order
+  std::vector<int> edge_C;          // channels per edge
+  std::vector<Rate> edge_rate;      // RateMap per edge
+  std::vector<std::vector<int>> in_edge;    // [node][port] -> edge
+  std::vector<std::vector<int>> out_edges;  // [node] -> edges, in edge order
+  int source = -1, sink = -1;
+  int out_C = 0;
+  int64_t ratio = 1;
+};
+DagInfo dag_validate(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
+                     int in_C);
+void dag_receptive_field(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
+                         int in_C, int64_t* past, int64_t* future);
+// causalize rewrite; returns the total latency in input samples
+int64_t dag_causalize(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
+                      int in_C, std::vector<sc_gnode>* out_nodes, std::vector<sc_edge>* out_edges);
+Program lower_dag(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
+                  const float* W, int64_t n_weights, int in_C);
+
+// SPEC model_io (model_io.cpp): JSON manifest + f32 blob.
+std::unique_ptr<struct ::sc_model> model_load(const char* manifest_path, const char* blob_path);
+void model_save(const char* manifest_path, const char* blob_path, const sc_gnode* nodes, int n,
+                const sc_edge* edges, int ne, const float* W, int64_t nW, int in_C);
+
 }  // namespace scb
+
+// The C-ABI model handle: a loaded graph and its weights (owned arrays).
+struct sc_model {
+  std::vector<sc_gnode> nodes;
+  std::vector<sc_edge> edges;
+  std::vector<float> weights;
+  int32_t in_channels = 0;
+};

@@ -94,6 +94,10 @@ bool tc_disabled() {
 // Decide whether an op runs on the tensor-core kernel and build its hi/lo weight planes.
 void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<float>& wtc) {
   const ConvOp& op = pg.ops[i];
+  if (op.kind == OPK_SUM) {
+    d.kernel = KERNEL_SUM;
+    return;
+  }
   const BufferSpec& bi = pg.bufs[op.in_buf];
   const bool strided = !op.convt && op.S > 1;
   const int S = strided ? op.S : 1;
@@ -165,8 +169,21 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
   if (precision != SC_PREC_FP32 && precision != SC_PREC_BF16)
     fail(SC_ERR_INVALID_ARGUMENT, "precision must be SC_PREC_FP32 or SC_PREC_BF16");
   if (n_nodes > 0 && !W && nW > 0) fail(SC_ERR_INVALID_ARGUMENT, "weights pointer is null");
+  return make_plan(lower_graph(nodes, n_nodes, W, nW, in_C), precision, device);
+}
+
+std::unique_ptr<Plan> make_plan_dag(const sc_gnode* nodes, int n_nodes, const sc_edge* edges,
+                                    int n_edges, const float* W, int64_t nW, int in_C,
+                                    int precision, int device) {
+  if (precision != SC_PREC_FP32 && precision != SC_PREC_BF16)
+    fail(SC_ERR_INVALID_ARGUMENT, "precision must be SC_PREC_FP32 or SC_PREC_BF16");
+  if (!W && nW > 0) fail(SC_ERR_INVALID_ARGUMENT, "weights pointer is null");
+  return make_plan(lower_dag(nodes, n_nodes, edges, n_edges, W, nW, in_C), precision, device);
+}
+
+std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
   auto plan = std::make_unique<Plan>();
-  plan->prog = lower_graph(nodes, n_nodes, W, nW, in_C);
+  plan->prog = std::move(prog);
   plan->precision = precision;
   plan->device = device;
   plan->desc = plan->prog.describe();
@@ -266,7 +283,9 @@ std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* 
       for (size_t i = 0; i < nops && ok; ++i) {
         const ConvOp& op = pg.ops[i];
         const DevOp& d = plan->dops[i];
-        const bool rd = op.in_buf == static_cast<int>(b), rs = op.res_buf == static_cast<int>(b);
+        bool rd = op.in_buf == static_cast<int>(b);
+        for (const SumIn& si : op.sum_in) rd = rd || si.buf == static_cast<int>(b);
+        const bool rs = op.res_buf == static_cast<int>(b);
         const bool wr = op.out_buf == static_cast<int>(b);
         if (!rd && !rs && !wr) continue;
         touched = true;
@@ -345,6 +364,21 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   st->cache.clear();
   for (const BufferSpec& b : pg.bufs) st->cache.push_back(b.cache);
   if (st->phase_mode) {
+    // every operand of a Sum (and a residual epilogue) must receive its frames in lockstep with
+    // the other operands; a branch that changes rate internally does not under phase state
+    std::vector<int64_t> n(pg.bufs.size(), 0);
+    for (int64_t k = 0; k < 2 * pg.ratio; ++k) {
+      n[0] += 1;
+      for (const ConvOp& op : pg.ops) {
+        const int64_t nin = n[op.in_buf];
+        n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? nin / op.S : nin);
+        bool ok = op.res_buf < 0 || n[op.res_buf] == n[op.out_buf];
+        for (const SumIn& si : op.sum_in) ok = ok && n[si.buf] == nin;
+        if (!ok)
+          fail(SC_ERR_UNSUPPORTED_FORMAT, "buffers shorter than the compression ratio with a Sum whose operands change rate "
+                                          "inside the branch (" + op.name + ")");
+      }
+    }
     for (const ConvOp& op : pg.ops)
       if (!op.convt && op.S > 1) st->cache[op.in_buf] = std::max(st->cache[op.in_buf], pg.bufs[op.in_buf].cache + op.S);
     st->cache[pg.sink_buf] += (pg.ratio - 1) * pg.sink_rate.num / pg.sink_rate.den;
@@ -464,7 +498,7 @@ CallPlan& State::call_plan(int64_t F) {
   cp->pos = pw;
   for (size_t b = 0; b < n.size(); ++b) cp->base.push_back(buf_base[b] + pw[b] * plan->fw(b));
   cp->F = F;
-  cp->egress_row = row;
+  cp->egress_row = row - pg.sink_delay;  // a Delay in front of the Sink (cache >= delay)
   cp->egress_T = Fs;
   for (size_t b = 0; b < n.size(); ++b) cp->T.push_back(n[b] - N[b]);
   for (const ConvOp& op : pg.ops) {
@@ -668,6 +702,32 @@ PqmfParams State::pqmf_params(size_t i, const CallPlan& cp) const {
   return p;
 }
 
+SumParams State::sum_params(size_t i, const CallPlan& cp) const {
+  const Program& pg = plan->prog;
+  const ConvOp& op = pg.ops[i];
+  SumParams p{};
+  p.n_in = static_cast<int>(op.sum_in.size());
+  for (int q = 0; q < p.n_in; ++q) {
+    const SumIn& si = op.sum_in[q];
+    p.in[q] = cp.base[si.buf];
+    p.in_sstride[q] = buf_sstride[si.buf];
+    p.in_fstride[q] = pg.bufs[si.buf].C;
+    p.in_off[q] = si.off;
+    p.in_f0[q] = static_cast<int>(cache[si.buf] - si.delay);
+    p.act[q] = si.act;
+    p.alpha[q] = si.alpha;
+  }
+  p.out = cp.base[op.out_buf];
+  p.out_sstride = buf_sstride[op.out_buf];
+  p.out_base = cache[op.out_buf] * pg.bufs[op.out_buf].C;
+  p.C = op.nout;
+  p.t_out = static_cast<int>(cp.t_out[i]);
+  p.streams = streams;
+  p.post_act = op.post_act;
+  p.post_alpha = op.post_alpha;
+  return p;
+}
+
 IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
   const Program& pg = plan->prog;
   IngestArgs a{};
@@ -720,7 +780,7 @@ std::string State::launch_name(int64_t F, int i) {
       const DevOp& d = plan->dops[j];
       return "op" + std::to_string(j) + " " + op.name + " [" +
              (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
-              : d.kernel == KERNEL_SIMT ? "simt" : "pqmf") + "]";
+              : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";
     }
   }
   if (i == k++) return "egress";
@@ -741,6 +801,8 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     if (plan->dops[i].kernel == KERNEL_TC) {
       const TcLaunch& t = cp.tc[i];
       launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
+    } else if (plan->dops[i].kernel == KERNEL_SUM) {
+      launch_sum(sum_params(i, cp), s);
     } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {
       launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_params(i, cp), s);
     } else {

@@ -16,7 +16,7 @@
 
 namespace scb {
 
-enum KernelKind { KERNEL_SIMT = 0, KERNEL_TC = 1, KERNEL_PQMF_ANA = 2, KERNEL_PQMF_SYN = 3 };
+enum KernelKind { KERNEL_SIMT = 0, KERNEL_TC = 1, KERNEL_PQMF_ANA = 2, KERNEL_PQMF_SYN = 3, KERNEL_SUM = 4 };
 
 struct DevOp {
   float* w = nullptr;
@@ -123,6 +123,7 @@ struct State {
   CallPlan& call_plan(int64_t F);
   ConvParams conv_params(size_t op, const CallPlan& cp) const;
   PqmfParams pqmf_params(size_t op, const CallPlan& cp) const;
+  SumParams sum_params(size_t op, const CallPlan& cp) const;
   IngestArgs ingest_args(const float* in, const CallPlan& cp) const;
   EgressArgs egress_args(float* out, const CallPlan& cp) const;
   void check_frames(int64_t frames) const;
@@ -146,6 +147,10 @@ struct State {
 
 std::unique_ptr<Plan> make_plan(const sc_node* nodes, int n_nodes, const float* W, int64_t nW,
                                 int in_C, int precision, int device);
+std::unique_ptr<Plan> make_plan_dag(const sc_gnode* nodes, int n_nodes, const sc_edge* edges,
+                                    int n_edges, const float* W, int64_t nW, int in_C,
+                                    int precision, int device);
+std::unique_ptr<Plan> make_plan(Program prog, int precision, int device);
 std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_frames);
 
 // tensor_core conv1d (kernels.cpp:73-104) on a device batch, reference layout in and out.

@@ -43,13 +43,22 @@ def _ptr(t) -> int:
 
 class Plan:
     def __init__(self, model, precision: str = "fp32", device: int = 0):
-        nodes, n, w = model.pack()
-        self._w = w
-        self.in_channels = model.in_channels
+        """`model`: a flat cached-module stack (graph.Model) or a SPEC DAG (graph.Graph)."""
+        from .graph import Graph
         prec = {"fp32": PREC_FP32, "bf16": PREC_BF16}[precision]
         h = C.c_void_p()
-        check(lib().sc_plan_create(nodes, n, w.ctypes.data_as(C.POINTER(C.c_float)), w.size,
-                                   model.in_channels, prec, device, C.byref(h)))
+        self.in_channels = model.in_channels
+        if isinstance(model, Graph):
+            nodes, n, edges, ne, w = model.pack()
+            self._w = w
+            check(lib().sc_plan_create_graph(nodes, n, edges, ne,
+                                             w.ctypes.data_as(C.POINTER(C.c_float)), w.size,
+                                             model.in_channels, prec, device, C.byref(h)))
+        else:
+            nodes, n, w = model.pack()
+            self._w = w
+            check(lib().sc_plan_create(nodes, n, w.ctypes.data_as(C.POINTER(C.c_float)), w.size,
+                                       model.in_channels, prec, device, C.byref(h)))
         self._h = h
         self.device = device
         self.precision = precision
