@@ -419,6 +419,8 @@ struct Lowerer {
             fail(SC_ERR_UNSUPPORTED_FORMAT, "residual branch must end with a conv");
           ConvOp& op = p->ops[br.producer];
           if (op.res_buf >= 0 || op.gate) fail(SC_ERR_UNSUPPORTED_FORMAT, "residual epilogue busy");
+          if (op.convt)  // r frames per polyphase row: use sc_plan_create_graph (SIMT sum)
+            fail(SC_ERR_UNSUPPORTED_FORMAT, "a residual branch ending in a ConvTranspose1d (use the DAG API)");
           op.res_buf = skip.buf;
           op.res_off = skip.off;
           op.res_act = skip.act;
@@ -830,7 +832,8 @@ struct DagLowerer {
         const Value& v = in[q];
         if (v.producer < 0 || eff[q] != 0 || v.off != 0 || v.act != ACT_ID) continue;
         const ConvOp& op = p.ops[v.producer];
-        if (op.kind != OPK_CONV || op.out_buf != v.buf || op.res_buf >= 0 || op.gate) continue;
+        // (a polyphase ConvT writes r frames per row: its epilogue has no per-frame residual)
+        if (op.kind != OPK_CONV || op.convt || op.out_buf != v.buf || op.res_buf >= 0 || op.gate) continue;
         if (v.producer > best) best = v.producer, j = q;
       }
       if (j >= 0) {

@@ -686,16 +686,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
-          const int q = kb / p.cblocks;
-          const int cb = kb - q * p.cblocks;
+          // K-slab order (32-channel block major, tap minor) is the window mode's: every
+          // variant accumulates a layer's slabs in one order, so outputs do not depend on the
+          // per-call tile geometry (bit-identical across buffer partitions)
+          const int taps = nk / p.cblocks;
+          const int cb = kb / taps;
+          const int q = kb - cb * taps;
+          const int kw = (q * p.cblocks + cb) * BK;
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
           mbar_expect_tx_w(&full[s], bytes);
           tma_load_3d_w(&tmap_a, &full[s], a_hi(s), p.a_c0 + cb * BK, p.a_row0 + tc.i0 + q * p.a_tap_rows, tc.s0);
           if (BF) {
-            tma_load_3d_w(&tmap_w, &full[s], b_bf(s), kb * BK, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_bf(s), kw, tc.n0, 0);
           } else {
-            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
-            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
           }
         }
       }
