@@ -302,6 +302,43 @@ SC_API int sc_model_save(const char* manifest_path, const char* blob_path, const
                          int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
                          const float* weights, int64_t n_weights, int32_t in_channels);
 
+/* ---- SPEC baseline_ola: overlap-add over the non-causal graph ---------
+ * Chunks x[i*hop : i*hop + chunk] (hop = chunk x (1 - overlap/100)) are each run OFFLINE through
+ * the unmodified graph (original pads, zero state: offline_run), multiplied by the
+ * ratio-scaled window and summed at offsets i*hop; the output is trimmed to the input length.
+ * All chunks of all streams run batched on the GPU.  overlap_pct in {0, 25, 50}; chunk and hop
+ * must be multiples of the compression ratio (ChunkTooSmall below it).                     */
+typedef struct sc_ola sc_ola;
+SC_API int sc_ola_create(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                         int32_t n_edges, const float* weights_host, int64_t n_weights,
+                         int32_t in_channels, int32_t precision, int32_t device, int64_t chunk,
+                         int32_t overlap_pct, int32_t n_streams, int64_t max_frames, sc_ola** out);
+/* d_in [n_streams][in_channels][frames] -> d_out [n_streams][out_channels][frames x sink];
+ * frames >= chunk, a multiple of the hop, <= max_frames.  Asynchronous on `stream`. */
+SC_API int sc_ola_process(sc_ola* ola, const float* d_in, float* d_out, int64_t frames, void* stream);
+SC_API int sc_ola_destroy(sc_ola* ola);
+/* Lowering summary of the OLA's offline program (valid until sc_ola_destroy). */
+SC_API const char* sc_ola_describe(const sc_ola* ola);
+/* hann_window: 50 -> sin^2(pi n / N); 25 -> flat top with sin^2 quarter lobes
+ * (SPEC.md:350 decision, COLA at hop 3N/4); 0 -> rectangular.  w: N floats (computed in double). */
+SC_API int sc_ola_window(int64_t n, int32_t overlap_pct, float* w);
+/* redundancy_factor: samples pushed through the network per output sample. */
+SC_API double sc_ola_redundancy(int32_t overlap_pct);
+
+/* ---- SPEC metrics_bench fidelity scores, batches of device signals ------
+ * ref / test: [n_signals][length] fp32 device.  Any of the outputs may be NULL.
+ *   l_s: spectral distance, Eq. 3 (n_fft 256/512/1024, hop n_fft/4, Hann, log(|S|+1), L2 over
+ *        frames x bins divided by the frame count, summed over scales; cuFFT)
+ *   l_w: Euclidean distance ||x - y||_2, Eq. 4
+ *   l_c: normalized correlation; ZeroEnergy (and NaN) when a signal has no energy.
+ * Synchronous: returns after the host outputs are written. */
+SC_API int sc_fidelity(const float* d_ref, const float* d_test, int32_t n_signals, int64_t length,
+                       double* l_s, double* l_w, double* l_c, void* stream);
+/* best_lag: argmax over lag in [0, max_lag] of correlation(ref[0:T-lag],
+ * test[lag:T]) per signal.  Synchronous. */
+SC_API int sc_best_lag(const float* d_ref, const float* d_test, int32_t n_signals, int64_t length,
+                       int32_t max_lag, int64_t* lags, void* stream);
+
 /* ---- tensor_core ops on device batches (kernels.hpp:16-32) ----------------------------- */
 /* conv1d (kernels.cpp:73-104) over a batch: x [batch][M][L] -> y [batch][N][Lout],
  * Lout = (L - ((K-1)d+1))/S + 1 (kernels.cpp:46-49).  w/b device, reference layout.      */

@@ -220,3 +220,92 @@ def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = 
 
 def host_threads() -> int:
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+# ----------------------------------------------------------------------- baseline_ola + metrics
+def ola_window(n: int, overlap: int) -> np.ndarray:
+    """SPEC hann_window: 50 -> sin^2(pi k / N); 25 -> the flat-top decision
+    (sin^2 quarter lobes); 0 -> rectangular.  Double precision."""
+    k = np.arange(n, dtype=np.float64)
+    if overlap == 50:
+        return np.sin(np.pi * k / n) ** 2
+    w = np.ones(n)
+    if overlap == 25:
+        q = n // 4
+        j = np.arange(q, dtype=np.float64)
+        w[:q] = np.sin(np.pi * j / (2 * q)) ** 2
+        w[n - q:] = np.sin(np.pi * (q - j) / (2 * q)) ** 2
+    return w
+
+
+def ola(model, x: np.ndarray, chunk: int, overlap: int) -> np.ndarray:
+    """SPEC ola_process: chunks x[i*hop : i*hop+N] through offline_run of the
+    ORIGINAL graph, times the ratio-scaled window, summed at offsets i*hop, trimmed to x."""
+    S, Cin, T = x.shape
+    hop = chunk * (100 - overlap) // 100
+    nc = (T - chunk) // hop + 1
+    chunks = np.stack([x[:, :, i * hop:i * hop + chunk] for i in range(nc)], axis=1)
+    out = run(model, chunks.reshape(S * nc, Cin, chunk), mode="offline_original")
+    No = out.shape[-1]
+    out = out.reshape(S, nc, out.shape[1], No)
+    hop_o = hop * No // chunk
+    w = ola_window(No, overlap).astype(np.float32)
+    y = np.zeros((S, out.shape[2], T * No // chunk), np.float32)
+    for i in range(nc):
+        y[:, :, i * hop_o:i * hop_o + No] += w * out[:, i]
+    return y
+
+
+def spectral_distance(x: np.ndarray, y: np.ndarray) -> float:
+    """SPEC spectral_distance (Eq. 3 with epsilon 1): scales 256/512/1024, hop
+    n/4, Hann sin^2 window, || log(|X|+1) - log(|Y|+1) ||_2 / frames, summed over scales."""
+    x = np.asarray(x, np.float64).ravel()
+    y = np.asarray(y, np.float64).ravel()
+    if x.size != y.size:
+        raise OracleError(14, "LengthMismatch")
+    T = x.size
+    total = 0.0
+    for n in (256, 512, 1024):
+        if T < n:
+            continue
+        hop = n // 4
+        F = 1 + (T - n) // hop
+        idx = np.arange(F)[:, None] * hop + np.arange(n)[None, :]
+        w = np.sin(np.pi * np.arange(n) / n) ** 2
+        X = np.abs(np.fft.rfft(x[idx] * w, axis=1))
+        Y = np.abs(np.fft.rfft(y[idx] * w, axis=1))
+        total += np.sqrt(np.sum((np.log1p(X) - np.log1p(Y)) ** 2)) / F
+    return float(total)
+
+
+def euclidean_distance(x, y) -> float:
+    x = np.asarray(x, np.float64).ravel()
+    y = np.asarray(y, np.float64).ravel()
+    return float(np.sqrt(np.sum((x - y) ** 2)))
+
+
+def correlation(x, y) -> float:
+    x = np.asarray(x, np.float64).ravel()
+    y = np.asarray(y, np.float64).ravel()
+    ex, ey = np.sum(x * x), np.sum(y * y)
+    if ex <= 0 or ey <= 0:
+        raise OracleError(15, "ZeroEnergy")
+    return float(np.sum(x * y) / np.sqrt(ex * ey))
+
+
+def best_lag(ref, test, max_lag: int) -> int:
+    ref = np.asarray(ref, np.float64).ravel()
+    test = np.asarray(test, np.float64).ravel()
+    T = ref.size
+    best, bv = -1, -2.0
+    for lag in range(max_lag + 1):
+        a, b = ref[:T - lag], test[lag:]
+        ea, eb = np.sum(a * a), np.sum(b * b)
+        if ea <= 0 or eb <= 0:
+            continue
+        c = np.sum(a * b) / np.sqrt(ea * eb)
+        if c > bv:
+            best, bv = lag, c
+    if best < 0:
+        raise OracleError(15, "ZeroEnergy")
+    return best

@@ -109,6 +109,18 @@ _SIGS = {
     "sc_model_save": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(SCGNode), C.c_int32,
                                 C.POINTER(SCEdge), C.c_int32, C.POINTER(C.c_float), C.c_int64,
                                 C.c_int32]),
+    "sc_ola_create": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                C.POINTER(C.c_float), C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.POINTER(C.c_void_p)]),
+    "sc_ola_process": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "sc_ola_destroy": (C.c_int, [C.c_void_p]),
+    "sc_ola_describe": (C.c_char_p, [C.c_void_p]),
+    "sc_ola_window": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_float)]),
+    "sc_ola_redundancy": (C.c_double, [C.c_int32]),
+    "sc_fidelity": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double),
+                              C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p]),
+    "sc_best_lag": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
+                              C.POINTER(C.c_int64), C.c_void_p]),
     "sc_plan_destroy": (C.c_int, [C.c_void_p]),
     "sc_plan_ratio": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_plan_sink_rate": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -15,6 +16,9 @@ struct sc_plan {
 };
 struct sc_state {
   std::unique_ptr<scb::State> s;
+};
+struct sc_ola {
+  std::unique_ptr<scb::Ola> o;
 };
 
 namespace {
@@ -197,6 +201,74 @@ int sc_model_save(const char* manifest_path, const char* blob_path, const sc_gno
                   int32_t in_channels) {
   return guard([&] {
     scb::model_save(manifest_path, blob_path, nodes, n_nodes, edges, n_edges, weights, n_weights, in_channels);
+  });
+}
+
+int sc_ola_create(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                  const float* weights_host, int64_t n_weights, int32_t in_channels, int32_t precision,
+                  int32_t device, int64_t chunk, int32_t overlap_pct, int32_t n_streams, int64_t max_frames,
+                  sc_ola** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    *out = nullptr;
+    auto o = scb::make_ola(nodes, n_nodes, edges, n_edges, weights_host, n_weights, in_channels, precision, device,
+                           chunk, overlap_pct, n_streams, max_frames);
+    *out = new sc_ola{std::move(o)};
+  });
+}
+
+int sc_ola_process(sc_ola* ola, const float* d_in, float* d_out, int64_t frames, void* stream) {
+  return guard([&] {
+    need(ola && d_in && d_out, "null argument");
+    scb::ola_process(*ola->o, d_in, d_out, frames, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sc_ola_destroy(sc_ola* ola) {
+  return guard([&] { delete ola; });
+}
+
+const char* sc_ola_describe(const sc_ola* ola) { return ola ? scb::ola_plan(*ola->o).desc.c_str() : ""; }
+
+int sc_ola_window(int64_t n, int32_t overlap_pct, float* w) {
+  return guard([&] {
+    need(n >= 1 && w, "window length must be >= 1");
+    need(overlap_pct == 0 || overlap_pct == 25 || overlap_pct == 50, "overlap must be 0, 25 or 50");
+    const std::vector<double> v = scb::ola_window(n, overlap_pct);
+    for (int64_t i = 0; i < n; ++i) w[i] = static_cast<float>(v[i]);
+  });
+}
+
+double sc_ola_redundancy(int32_t overlap_pct) { return 100.0 / (100.0 - overlap_pct); }
+
+int sc_fidelity(const float* d_ref, const float* d_test, int32_t n, int64_t T, double* l_s, double* l_w,
+                double* l_c, void* stream) {
+  return guard([&] {
+    need(d_ref && d_test && n >= 1 && T >= 1, "fidelity: empty input");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (l_s) scb::spectral_distance(d_ref, d_test, n, T, l_s, st);
+    if (l_w || l_c) {
+      std::vector<double> m(static_cast<size_t>(n) * 4);
+      scb::signal_moments(d_ref, d_test, n, T, m.data(), st);
+      bool zero = false;
+      for (int i = 0; i < n; ++i) {
+        if (l_w) l_w[i] = std::sqrt(m[4 * i]);
+        if (l_c) {
+          const bool z = m[4 * i + 2] <= 0 || m[4 * i + 3] <= 0;
+          zero = zero || z;
+          l_c[i] = z ? std::nan("") : m[4 * i + 1] / std::sqrt(m[4 * i + 2] * m[4 * i + 3]);
+        }
+      }
+      if (zero) scb::fail(SC_ERR_ZERO_ENERGY, "correlation of a signal with zero energy");
+    }
+  });
+}
+
+int sc_best_lag(const float* d_ref, const float* d_test, int32_t n, int64_t T, int32_t max_lag, int64_t* lags,
+                void* stream) {
+  return guard([&] {
+    need(d_ref && d_test && lags && n >= 1, "best_lag: null argument");
+    scb::best_lag(d_ref, d_test, n, T, max_lag, lags, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -173,12 +173,18 @@ struct Lowerer {
   Program* p;
   int pos = 0;
   int64_t ratio = 1;
+  bool offline = false;  // original pads, no causalize delays (OLA per-chunk offline_run)
 
   static int64_t lcm(int64_t a, int64_t b) { return a / Rate::gcd(a, b) * b; }
 
   void need_cache(int buf, int64_t frames) {
     BufferSpec& b = p->bufs[buf];
     b.cache = std::max(b.cache, frames);
+  }
+
+  void need_tail(int buf, int64_t frames) {
+    BufferSpec& b = p->bufs[buf];
+    b.tail = std::max(b.tail, frames);
   }
 
   void need_align(int buf, int64_t a) {
@@ -244,7 +250,35 @@ struct Lowerer {
       op.nout = static_cast<int>(r * N);
       op.w.assign(static_cast<size_t>(op.taps) * M * op.nout, 0.0f);
       op.bias.resize(op.nout);
-      for (int phi = 0; phi < r; ++phi) {
+      if (offline) {
+        // original pad L on the zero-stuffed signal: y[r i + phi] = b + sum_k w[k] up[r i + phi
+        // - L + k] with up[r m] = x[m]: phase phi takes the taps k = r e - phi + L at input row
+        // i + e, e in [e_lo, e_hi] over all phases (e_hi > 0 reads rows past the chunk: zeros)
+        int64_t elo = INT64_MAX, ehi = INT64_MIN;
+        for (int phi = 0; phi < r; ++phi)
+          for (int64_t k = 0; k < K; ++k) {
+            const int64_t m = phi - L + k;
+            if (((m % r) + r) % r) continue;
+            const int64_t e = (m >= 0) ? m / r : -((-m) / r);
+            elo = std::min(elo, e);
+            ehi = std::max(ehi, e);
+          }
+        op.look = -elo + v.dly;
+        op.taps = static_cast<int>(ehi - elo + 1);
+        op.w.assign(static_cast<size_t>(op.taps) * M * op.nout, 0.0f);
+        for (int phi = 0; phi < r; ++phi) {
+          for (int q = 0; q < op.taps; ++q) {
+            const int64_t k = r * (elo + q) - phi + L;
+            if (k < 0 || k >= K) continue;
+            for (int64_t c = 0; c < M; ++c)
+              for (int64_t nn = 0; nn < N; ++nn)
+                op.w[(static_cast<size_t>(q) * M + c) * op.nout + phi * N + nn] = w[(nn * M + c) * K + k];
+          }
+          for (int64_t nn = 0; nn < N; ++nn) op.bias[phi * N + nn] = b[nn];
+        }
+        need_tail(v.buf, std::max<int64_t>(0, ehi - v.dly));
+      }
+      for (int phi = 0; phi < r && !offline; ++phi) {
         const int64_t k0 = ((K - 1 - phi) % r + r) % r;
         const int64_t e = (K - 1 - phi - k0) / r;
         for (int q = 0; q < op.taps; ++q) {
@@ -276,9 +310,9 @@ struct Lowerer {
       } else {
         if (Ptot < span - S)
           fail(SC_ERR_PADDING_NOT_STREAMABLE, "strided conv: pad must be >= span - stride");
-        Da = delay_for_stride(S, R, v.D);
-        if ((v.D + R + Da) % S != 0) fail(SC_ERR_INTERNAL_NON_INTEGER_DELAY, "ledger division");
-        v.D = (v.D + R + Da) / S;
+        Da = offline ? 0 : delay_for_stride(S, R, v.D);
+        if (!offline && (v.D + R + Da) % S != 0) fail(SC_ERR_INTERNAL_NON_INTEGER_DELAY, "ledger division");
+        v.D = offline ? 0 : (v.D + R + Da) / S;  // (offline programs keep no ledger)
         out_rate.den *= S;
         out_rate.norm();
         p->state_bytes_spec += M * Da * 4;  // inserted Delay(D_a) ring
@@ -288,7 +322,9 @@ struct Lowerer {
       // window start must sit on a super-row boundary, so the look-back is rounded up to a
       // multiple of S and the kernel is front-padded with zero taps by the same shift.
       // a pending Delay (DAG path) widens the window look-back like an Eq. (2) delay does
-      const int64_t P = Ptot + Da + v.dly;
+      // offline: the original left pad only; rows past the chunk read as zeros (tail)
+      const int64_t P = (offline ? L : Ptot + Da) + v.dly;
+      if (offline) need_tail(v.buf, std::max<int64_t>(0, span - S - P));
       // (a dilated strided conv never runs on super-rows — the SIMT path reads it frame by
       // frame — and a zero-tap front pad would land on the wrong rows for d > 1)
       const int64_t Pa = (S > 1 && nd.dilation == 1) ? (P + S - 1) / S * S : P;
@@ -822,8 +858,9 @@ struct DagLowerer {
     }
     std::vector<int64_t> eff(in.size());
     for (size_t q = 0; q < in.size(); ++q) {  // pending Delay + branch_alignment A_i
-      eff[q] = in[q].dly + (Dmax - in[q].D);
-      p.state_bytes_spec += static_cast<int64_t>(in[q].C) * (Dmax - in[q].D) * 4;
+      const int64_t A = lw.offline ? 0 : Dmax - in[q].D;  // the original graph has no A_i
+      eff[q] = in[q].dly + A;
+      p.state_bytes_spec += static_cast<int64_t>(in[q].C) * A * 4;
     }
     if (nd.arity == 2) {
       // residual epilogue: the operand computed last is a conv output nobody else reads
@@ -883,6 +920,29 @@ struct DagLowerer {
     out.producer = static_cast<int>(p.ops.size()) - 1;
   }
 
+  // Write the value (pending activation and Delay applied) to a buffer of its own with a
+  // one-operand SIMT sum launch; `post` is applied on the store.
+  void materialize(Value& v, int post, float post_alpha, const char* what) {
+    ConvOp op;
+    op.kind = OPK_SUM;
+    op.in_buf = v.buf;
+    op.cin = op.nout = op.cout = op.out_rstride = v.C;
+    op.in_rate = v.rate;
+    op.sum_in.push_back(SumIn{v.buf, v.off, v.act, v.alpha, v.dly});
+    lw.need_cache(v.buf, v.dly);
+    op.post_act = post;
+    op.post_alpha = post_alpha;
+    op.name = std::string(what) + " C" + std::to_string(v.C);
+    op.out_buf = lw.new_buffer(v.C, v.rate, op.name);
+    p.ops.push_back(std::move(op));
+    v.buf = p.ops.back().out_buf;
+    v.off = 0;
+    v.act = ACT_ID;
+    v.alpha = 0.f;
+    v.dly = 0;
+    v.producer = static_cast<int>(p.ops.size()) - 1;
+  }
+
   void run() {
     for (int u : g.order) {
       const sc_gnode& nd = nodes[u];
@@ -898,6 +958,9 @@ struct DagLowerer {
         case SC_G_FANOUT:
           break;
         case SC_G_CONV: {
+          // offline: a model Delay truncates its output at the chunk end, and a conv with right
+          // padding must read zeros there, not the undelayed frames: materialise the delay
+          if (lw.offline && v.dly > 0) materialize(v, ACT_ID, 0.f, "delay");
           sc_node c{};
           c.kind = SC_NODE_CONV;
           c.in_channels = nd.in_channels;
@@ -944,28 +1007,12 @@ struct DagLowerer {
           } else {
             // a second activation on a value that already carries one: materialise
             // act2(act1(x)) with a one-operand SIMT sum launch (load act, store act)
-            ConvOp op;
-            op.kind = OPK_SUM;
-            op.in_buf = v.buf;
-            op.cin = op.nout = op.cout = op.out_rstride = v.C;
-            op.in_rate = v.rate;
-            op.sum_in.push_back(SumIn{v.buf, v.off, v.act, v.alpha, v.dly});
-            lw.need_cache(v.buf, v.dly);
-            op.post_act = nd.act;
-            op.post_alpha = nd.alpha;
-            op.name = "act C" + std::to_string(v.C);
-            op.out_buf = lw.new_buffer(v.C, v.rate, op.name);
-            p.ops.push_back(std::move(op));
-            v.buf = p.ops.back().out_buf;
-            v.off = 0;
-            v.act = ACT_ID;
-            v.alpha = 0.f;
-            v.dly = 0;
-            v.producer = static_cast<int>(p.ops.size()) - 1;
+            materialize(v, nd.act, nd.alpha, "act");
           }
           break;
         }
         case SC_G_DELAY:
+          if (lw.offline && nd.inserted) break;  // absent from the original graph
           if (v.zup > 1) {
             v.dly_up += nd.samples;
           } else {
@@ -1033,7 +1080,7 @@ struct DagLowerer {
 }  // namespace
 
 Program lower_dag(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
-                  int64_t nW, int in_C) {
+                  int64_t nW, int in_C, bool offline) {
   if (in_C < 1) fail(SC_ERR_INVALID_ARGUMENT, "in_channels must be >= 1");
   const DagInfo g = dag_validate(nodes, n, edges, ne, in_C);
   Program p;
@@ -1044,6 +1091,8 @@ Program lower_dag(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, co
   p.bufs.push_back(src);
   sc_node dummy{};
   Lowerer lw{&dummy, 0, W, nW, &p};
+  lw.offline = offline;
+  p.offline = offline;
   DagLowerer dl{nodes, edges, g, lw, p, std::vector<Value>(ne)};
   dl.run();
   for (BufferSpec& b : p.bufs) b.cache = (b.cache + b.align - 1) / b.align * b.align;
@@ -1081,9 +1130,10 @@ Program lower_graph(const sc_node* nodes, int n_nodes, const float* W, int64_t n
 
 std::string Program::describe() const {
   std::ostringstream os;
-  os << "buffers:\n";
+  os << (offline ? "offline (original pads, per-call zero state)\n" : "") << "buffers:\n";
   for (size_t i = 0; i < bufs.size(); ++i)
-    os << "  b" << i << " C=" << bufs[i].C << " cache=" << bufs[i].cache << " rate=" << bufs[i].rate.num
+    os << "  b" << i << " C=" << bufs[i].C << " cache=" << bufs[i].cache
+       << (bufs[i].tail ? " tail=" + std::to_string(bufs[i].tail) : std::string()) << " rate=" << bufs[i].rate.num
        << "/" << bufs[i].rate.den << " (" << bufs[i].name << ")\n";
   os << "ops:\n";
   for (size_t i = 0; i < ops.size(); ++i) {

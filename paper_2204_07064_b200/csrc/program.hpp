@@ -15,6 +15,7 @@ struct BufferSpec {
   int C = 1;
   int64_t cache = 0;  // frames kept across calls (max look-back of all readers)
   int64_t align = 1;  // cache is rounded to a multiple of this (strided readers' super-rows)
+  int64_t tail = 0;   // offline (OLA) programs: zero frames readers see after the new frames
   Rate rate;
   std::string name;
 };
@@ -72,6 +73,8 @@ struct Program {
   int64_t sink_delay = 0;     // a Delay in front of the Sink: egress reads rows cache - delay + t
   float sink_alpha = 0.f;
   Rate sink_rate;
+  bool offline = false;       // original (non-causal) pads, no causalize delays: the per-chunk
+                              // offline_run of the OLA baseline (every call starts from zeros)
   int64_t ratio = 1;          // SPEC compression_ratio
   int64_t latency_sink = 0;   // D_c at the sink, native rate
   int64_t latency_in = 0;     // latency in input samples
@@ -102,7 +105,7 @@ void dag_receptive_field(const sc_gnode* nodes, int n_nodes, const sc_edge* edge
 int64_t dag_causalize(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
                       int in_C, std::vector<sc_gnode>* out_nodes, std::vector<sc_edge>* out_edges);
 Program lower_dag(const sc_gnode* nodes, int n_nodes, const sc_edge* edges, int n_edges,
-                  const float* W, int64_t n_weights, int in_C);
+                  const float* W, int64_t n_weights, int in_C, bool offline = false);
 
 // SPEC model_io (model_io.cpp): JSON manifest + f32 blob.
 std::unique_ptr<struct ::sc_model> model_load(const char* manifest_path, const char* blob_path);

@@ -406,7 +406,7 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
       const BufferSpec& b = pg.bufs[i];
       // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
       const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
-      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T) * plan->fw(i), 32);
+      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T + b.tail) * plan->fw(i), 32);
       st->buf_sstride.push_back(sstride);
       off.push_back(total);
       total += round_up(sstride * streams, 64);

@@ -153,6 +153,29 @@ std::unique_ptr<Plan> make_plan_dag(const sc_gnode* nodes, int n_nodes, const sc
 std::unique_ptr<Plan> make_plan(Program prog, int precision, int device);
 std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_frames);
 
+// SPEC baseline_ola (ola.cu) and metrics_bench (metrics.cu).
+struct Ola {
+  std::unique_ptr<Plan> plan;                        // offline program (original pads)
+  std::map<int64_t, std::unique_ptr<State>> states;  // by chunks per stream
+  int streams = 0;
+  int64_t N = 0, hop = 0, max_frames = 0;
+  int overlap = 0;
+  float* d_in = nullptr;   // gathered chunks [streams * nc][C][N]
+  float* d_out = nullptr;  // chunk outputs [streams * nc][C'][N * sink]
+  float* d_w = nullptr;    // window, N * sink
+  int64_t in_floats = 0, out_floats = 0;
+  ~Ola();
+};
+std::unique_ptr<Ola> make_ola(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
+                              int64_t nW, int in_C, int precision, int device, int64_t chunk, int overlap_pct,
+                              int streams, int64_t max_frames);
+void ola_process(Ola& o, const float* in, float* out, int64_t T, cudaStream_t s);
+const Plan& ola_plan(const Ola& o);
+std::vector<double> ola_window(int64_t Nw, int overlap_pct);
+void signal_moments(const float* x, const float* y, int n, int64_t T, double* moments, cudaStream_t st);
+void spectral_distance(const float* x, const float* y, int n, int64_t T, double* out, cudaStream_t st);
+void best_lag(const float* ref, const float* test, int n, int64_t T, int max_lag, int64_t* lags, cudaStream_t st);
+
 // tensor_core conv1d (kernels.cpp:73-104) on a device batch, reference layout in and out.
 void conv1d_batched(const float* x, int batch, int M, int64_t L, const float* w, const float* b,
                     int N, int K, int S, int d, float* y, cudaStream_t s);

@@ -201,6 +201,72 @@ class StreamState:
         return r.value
 
 
+class Ola:
+    """SPEC baseline_ola on the GPU: overlap-add of the unmodified
+    (non-causal) graph over windowed chunks, every chunk of every stream batched (sc_ola_*)."""
+
+    def __init__(self, graph, chunk: int, overlap: int, n_streams: int, max_frames: int,
+                 precision: str = "fp32", device: int = 0):
+        from .graph import Graph, Model, model_to_graph
+        if isinstance(graph, Model):
+            graph = model_to_graph(graph)
+        nodes, n, edges, ne, w = graph.pack()
+        self._w = w
+        self.chunk, self.overlap, self.n_streams = chunk, overlap, n_streams
+        h = C.c_void_p()
+        check(lib().sc_ola_create(nodes, n, edges, ne, w.ctypes.data_as(C.POINTER(C.c_float)), w.size,
+                                  graph.in_channels, {"fp32": PREC_FP32, "bf16": PREC_BF16}[precision],
+                                  device, chunk, overlap, n_streams, max_frames, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().sc_ola_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
+
+    def process(self, x, y, frames: int, stream=None) -> None:
+        """x: device [n_streams][in_C][frames], y: device [n_streams][out_C][frames x sink]."""
+        check(lib().sc_ola_process(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
+                                   C.c_void_p(_stream_handle(stream))))
+
+    def describe(self) -> str:
+        return lib().sc_ola_describe(self._h).decode()
+
+    @staticmethod
+    def window(n: int, overlap: int) -> np.ndarray:
+        w = np.zeros(n, np.float32)
+        check(lib().sc_ola_window(n, overlap, w.ctypes.data_as(C.POINTER(C.c_float))))
+        return w
+
+    @staticmethod
+    def redundancy(overlap: int) -> float:
+        return lib().sc_ola_redundancy(overlap)
+
+
+def fidelity(ref, test, stream=None):
+    """SPEC metrics_bench scores of device signals [n][T] (or [n][1][T]): dict of numpy arrays
+    L_s (spectral, Eq. 3), L_w (Euclidean, Eq. 4), L_c (correlation)."""
+    n = int(ref.shape[0])
+    T = int(ref.shape[-1])
+    ls, lw, lc = (np.zeros(n, np.float64) for _ in range(3))
+    dp = C.POINTER(C.c_double)
+    check(lib().sc_fidelity(C.c_void_p(_ptr(ref)), C.c_void_p(_ptr(test)), n, T, ls.ctypes.data_as(dp),
+                            lw.ctypes.data_as(dp), lc.ctypes.data_as(dp), C.c_void_p(_stream_handle(stream))))
+    return dict(L_s=ls, L_w=lw, L_c=lc)
+
+
+def best_lag(ref, test, max_lag: int, stream=None) -> np.ndarray:
+    """SPEC best_lag per signal of device batches [n][T]."""
+    n = int(ref.shape[0])
+    out = np.zeros(n, np.int64)
+    check(lib().sc_best_lag(C.c_void_p(_ptr(ref)), C.c_void_p(_ptr(test)), n, int(ref.shape[-1]), max_lag,
+                            out.ctypes.data_as(C.POINTER(C.c_int64)), C.c_void_p(_stream_handle(stream))))
+    return out
+
+
 def conv1d(x, w, b, y, batch: int, in_channels: int, length: int, out_channels: int, taps: int,
            stride: int = 1, dilation: int = 1, stream=None) -> None:
     """Device conv1d (kernels.cpp:73-104) over a batch; reference layouts, device pointers."""
