@@ -791,9 +791,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         mbar_wait(stg_written, tcount & 1);
         const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
-        for (int k = 0; k < (out_cols + 31) / 32; ++k)
-          tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
-                       tc.i0, tc.s0);
+        for (int k = 0; k < (out_cols + 31) / 32; ++k) {
+          const uint8_t* src = reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4));
+          if (p.out_t)  // fused egress: (frame, channel, stream) box of the caller's output
+            tma_store_3d(&tmap_out, src, tc.i0, oc0 + 32 * k, tc.s0);
+          else
+            tma_store_3d(&tmap_out, src, oc0 + 32 * k, tc.i0, tc.s0);
+        }
         bulk_commit();
         bulk_wait_read0();
         mbar_arrive(stg_free);
@@ -953,7 +957,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
       __nv_bfloat16* stgb = reinterpret_cast<__nv_bfloat16*>(stg);  // bf16 buffers (bf16 plans)
-      if (p.gate) {
+      if (!OBF && !p.gate && p.out_t) {
+        // fused egress: finish the tile in registers (the residual comes from the frame-major
+        // staging), then — once every epilogue thread has read its residual — write it back
+        // channel-major: slab k holds [G][32 channels][R frames] (frame contiguous), the layout
+        // of the caller's [stream][C][T] box
+        const bool fast = p.post_act != ACT_TANH && p.res_act != ACT_TANH;
+        const float ps = slope_of(p.post_act, p.post_alpha);
+        const float rs = slope_of(p.res_act, p.res_alpha);
+        const bool pmax = ps <= 1.f, rmax = rs <= 1.f;
+        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
+#pragma unroll
+        for (int u = 0; u < COLS; u += 4) {
+          float rv[4] = {0.f, 0.f, 0.f, 0.f};
+          if (p.res) {  // float4 reads of the swizzled frame-major residual slab
+            const float4 v = *reinterpret_cast<const float4*>(stg + stg_off(r, col0 + u));
+            rv[0] = v.x, rv[1] = v.y, rv[2] = v.z, rv[3] = v.w;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float o = fast ? lin(acc[u + k], ps, pmax) : act_apply(acc[u + k], p.post_act, p.post_alpha);
+            if (p.res) o += fast ? lin(rv[k], rs, rmax) : act_apply(rv[k], p.res_act, p.res_alpha);
+            acc[u + k] = o;
+          }
+        }
+        if (p.res) named_bar(1, 256);  // the 8 epilogue warps
+        const int gi = r / p.R, ri = r - gi * p.R;
+#pragma unroll
+        for (int u = 0; u < COLS; ++u) {
+          const int col = col0 + u;
+          stg[(col >> 5) * (BM * 32) + (gi * 32 + (col & 31)) * p.R + ri] = acc[u];
+        }
+      } else if (p.gate) {
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
           const float o = gate_ool(acc[u], acc[u + 1]);
@@ -1087,6 +1122,8 @@ void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUten
 }
 
 }  // namespace
+
+int tc_num_threads() { return NUM_THREADS; }
 
 void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 12 * 256); }
 
