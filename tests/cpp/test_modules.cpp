@@ -61,6 +61,33 @@ int main(int argc, char** argv) {
     }
     REQUIRE(threw);
   }
+  {
+    // SPEC graph_ir DAG: a centered residual unit with a 3-way Sum and a model Delay
+    Graph g(4);
+    const int x = g.source();
+    const int a = g.conv(x, CachedConv1d{4, 4, 3, 1, 1, {1, 1}, lcg(48, 5, 0.3f), {}});
+    const int b = g.conv(g.leaky_relu(x, 0.2f), CachedConv1d{4, 4, 5, 1, 1, {2, 2}, lcg(80, 6, 0.3f), {}});
+    g.sink(g.sum({a, b, g.delay(x, 1)}));
+    int64_t past = 0, future = 0;
+    g.receptive_field(&past, &future);
+    REQUIRE(past == 2 && future == 2);
+    REQUIRE(g.compression_ratio() == 1);
+    REQUIRE(g.causalize_latency() == 2);
+    bool nc = false;
+    try {
+      g.latency();
+    } catch (const Error& e) {
+      nc = e.code() == "NotCausal";
+    }
+    REQUIRE(nc);
+    Plan hp(g, -1);
+    REQUIRE(hp.latency() == 2);
+    g.save("/tmp/sc_cpp_model.json");
+    Model m2("/tmp/sc_cpp_model.json");
+    REQUIRE(m2.n_nodes() == 8 && m2.in_channels() == 4);  // 7 + the Fanout of x
+    Plan hp2(m2, -1);
+    REQUIRE(hp2.latency() == 2 && hp2.state_bytes() == hp.state_bytes());
+  }
   if (!gpu) {
     std::printf("OK host\n");
     return 0;
@@ -113,6 +140,34 @@ int main(int argc, char** argv) {
     threw = e.code() == "InvalidArgument";
   }
   REQUIRE(threw);
+  {
+    // the DAG through the GPU: one buffer vs two halves must be bit-identical, and the OLA
+    // baseline over the same graph runs
+    Graph g(C);
+    const int x0 = g.source();
+    const int a0 = g.conv(x0, CachedConv1d{C, C, 3, 1, 1, {1, 1}, lcg(C * C * 3, 5, 0.2f), {}});
+    const int b0 = g.conv(g.leaky_relu(x0, 0.2f), CachedConv1d{C, C, 5, 1, 1, {2, 2}, lcg(C * C * 5, 6, 0.2f), {}});
+    g.sink(g.sum({a0, b0, g.delay(x0, 1)}));
+    Plan gp(g, 0);
+    StreamBatch gs(gp, S, T);
+    gs.process_buffer(dx, dy1, T);
+    gs.reset();
+    gs.process_buffer(da, ya, T / 2);
+    gs.process_buffer(db, yb, T / 2);
+    cudaDeviceSynchronize();
+    cudaMemcpy(y1.data(), dy1, y1.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h1.data(), ya, h1.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h2.data(), yb, h2.size() * 4, cudaMemcpyDeviceToHost);
+    for (int s = 0; s < S; ++s)
+      for (int c = 0; c < C; ++c) {
+        const float* full = &y1[(static_cast<size_t>(s) * C + c) * T];
+        REQUIRE(std::memcmp(full, &h1[(static_cast<size_t>(s) * C + c) * T / 2], 4 * T / 2) == 0);
+        REQUIRE(std::memcmp(full + T / 2, &h2[(static_cast<size_t>(s) * C + c) * T / 2], 4 * T / 2) == 0);
+      }
+    OverlapAdd ola(g, 128, 50, S, T);
+    ola.process(dx, dy2, T);
+    REQUIRE(cudaDeviceSynchronize() == cudaSuccess);
+  }
   std::printf("OK gpu\n");
   return 0;
 }
