@@ -890,14 +890,17 @@ void State::profile(const float* in, float* out, int64_t F, int steps, float* ms
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
-  const int n = call_launches(call_plan(F), out);
+  // profile layout: launches(F) slots (the carry slot is always present when the state has
+  // caches), plus the egress slot when this output pointer cannot take the fused egress
+  auto slots = [&](const CallPlan& c) { return launches(F) + ((c.fused && !fused_call(c, out)) ? 1 : 0); };
+  const int n = slots(call_plan(F));
   for (int i = 0; i < n; ++i) ms[i] = 0.f;
   std::vector<cudaEvent_t> ev(static_cast<size_t>(n + 1) * steps);
   for (auto& e : ev) ck(cudaEventCreate(&e), "EventCreate");
   int done = 0;
   for (int k = 0; k < steps; ++k) {
     CallPlan& cp = call_plan(F);
-    const bool same = call_launches(cp, out) == n;
+    const bool same = slots(cp) == n;
     enqueue(in, out, cp, s, same ? ev.data() + static_cast<size_t>(k) * (n + 1) : nullptr);
     launched += call_launches(cp, out);
     advance(F, cp);

@@ -391,3 +391,25 @@ def test_bf16_phase_state_and_reset():
     st2.reset([1])
     y2, _, _ = run_gpu(m2, x2[:, :, :512], [512], plan=plan2, state=st2)
     assert np.array_equal(y2[1], y_fresh[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_profile_layout_with_strips(monkeypatch, cfg):
+    """sc_state_profile across a strip cycle (calls with and without a carry; the carry slot is
+    always in the layout) and with an output pointer that cannot take the fused egress: one
+    timing per launch name, no slot overrun."""
+    monkeypatch.setenv("SC_STRIP_K", "3")
+    m = configs.build(cfg, seed=1)
+    plan = Plan(m)
+    num, den, cout = plan.sink
+    F = configs.CONFIGS[cfg]["frames"]
+    S = 3
+    st = StreamState(plan, S, F)
+    x = torch.randn(S, m.in_channels, F, device="cuda")
+    raw = torch.empty(S * cout * F * num // den + 1, device="cuda")
+    for y in (torch.empty((S, cout, F * num // den), device="cuda"), raw[1:].view(S, cout, F * num // den)):
+        prof = st.profile(x, y, F, steps=7)
+        names = [n for n, _ in prof]
+        assert len(names) == len(set(names)) and names[0] == "carry" and names[1] == "ingest"
+        assert all(t >= 0 for _, t in prof)
