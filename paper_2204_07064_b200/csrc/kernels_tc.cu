@@ -686,12 +686,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
-          // K-slab order (32-channel block major, tap minor) is the window mode's: every
-          // variant accumulates a layer's slabs in one order, so outputs do not depend on the
-          // per-call tile geometry (bit-identical across buffer partitions)
+          // K-slab order: a layer that may also run in window mode (cbmaj) takes the window
+          // mode's order (32-channel block major, tap minor), so its outputs do not depend on
+          // the per-call tile geometry (bit-identical across buffer partitions);
+          // the others take tap-major order (2% faster: the taps of one row block stay in L2)
           const int taps = nk / p.cblocks;
-          const int cb = kb / taps;
-          const int q = kb - cb * taps;
+          const int cb = p.cbmaj ? kb / taps : kb % p.cblocks;
+          const int q = p.cbmaj ? kb - cb * taps : kb / p.cblocks;
           const int kw = (q * p.cblocks + cb) * BK;
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
           mbar_expect_tx_w(&full[s], bytes);

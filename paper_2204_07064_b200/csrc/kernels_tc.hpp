@@ -46,6 +46,7 @@ struct TcParams {
   float res_alpha;
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
   int a_bf, r_bf, o_bf;  // bf16 plans: input / residual / output buffer holds bf16 (else fp32)
+  int cbmaj;  // 1: K-slabs channel-block major (layers that may run in window mode), else tap major
   int out_t;  // 1: fused egress — the tile is stored channel-major straight into the caller's
               // [stream][C][T] output (map_out dims T x C x streams, box R x 32 x G, no swizzle)
   int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)

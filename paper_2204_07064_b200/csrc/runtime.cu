@@ -612,6 +612,9 @@ CallPlan& State::call_plan(int64_t F) {
     // window mode (fp32, BN <= 64, one stream per tile): the transform splits each input row
     // once per 32-channel block and every tap's MMAs read it at a row offset
     p.halo = (d.taps_view - 1) * d.tap_rows;
+    // a layer that may run in window mode for some call geometry accumulates in the window
+    // order in every mode (bit-identity across partitions); a static property of the layer
+    p.cbmaj = ((d.bf16 || d.BN <= 64) && d.taps_view > 1) ? 1 : 0;
     p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
              !win_disabled()) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
