@@ -277,6 +277,14 @@ SC_API int sc_graph_causalize(const sc_gnode* nodes, int32_t n_nodes, const sc_e
  * would break offline_run(causalize(g)) == shift(offline_run(g), latency)). */
 SC_API int sc_graph_latency(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
                             int32_t n_edges, int32_t in_channels, int64_t* samples);
+/* SPEC mac_count: exact multiply-accumulates of an offline run over
+ * `input_samples` — sum over Conv nodes of out_len x N x M x K, the reference's literal
+ * arithmetic (a Conv after a ZeroUpsample counts its zero-stuffed MACs; the GPU's polyphase
+ * form skips them, sc_plan_macs_per_sample).  input_samples should be a multiple of the
+ * compression ratio (out_len = input_samples x the conv's output rate, rounded down). */
+SC_API int sc_graph_mac_count(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges,
+                              int32_t n_edges, int32_t in_channels, int64_t input_samples,
+                              int64_t* macs);
 /* sc_plan_create for a DAG: validate + causalize + lower to the fused cached-conv program.
  * ZeroUpsample must feed a stride-1, dilation-1 Conv (lowered to a polyphase ConvTranspose);
  * a Sum becomes the residual epilogue of a conv branch when one operand is a conv output

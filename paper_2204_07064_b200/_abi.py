@@ -98,6 +98,8 @@ _SIGS = {
                                      C.c_int32, C.POINTER(SCGNode), C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(SCEdge), C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "sc_graph_mac_count": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
+                                     C.c_int32, C.c_int64, C.POINTER(C.c_int64)]),
     "sc_graph_latency": (C.c_int, [C.POINTER(SCGNode), C.c_int32, C.POINTER(SCEdge), C.c_int32,
                                    C.c_int32, C.POINTER(C.c_int64)]),
     "sc_model_load": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),

@@ -157,6 +157,24 @@ int sc_graph_causalize(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* ed
   });
 }
 
+int sc_graph_mac_count(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
+                       int32_t in_channels, int64_t input_samples, int64_t* macs) {
+  return guard([&] {
+    need(macs != nullptr && input_samples >= 0, "mac_count: bad argument");
+    const scb::DagInfo g = scb::dag_validate(nodes, n_nodes, edges, n_edges, in_channels);
+    int64_t total = 0;
+    for (int e = 0; e < n_edges; ++e) {
+      const sc_gnode& nd = nodes[edges[e].to];
+      if (nd.kind != SC_G_CONV) continue;
+      // the conv's output edge rate = its input edge rate / S
+      const scb::Rate r = g.edge_rate[e];
+      const int64_t out_len = input_samples * r.num / (r.den * nd.stride);
+      total += out_len * nd.out_channels * nd.in_channels * nd.taps;
+    }
+    *macs = total;
+  });
+}
+
 int sc_graph_latency(const sc_gnode* nodes, int32_t n_nodes, const sc_edge* edges, int32_t n_edges,
                      int32_t in_channels, int64_t* samples) {
   return guard([&] {

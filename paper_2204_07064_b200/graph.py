@@ -332,6 +332,13 @@ class Graph:
         _abi.check(_abi.lib().sc_graph_receptive_field(*self._args(), C.byref(p), C.byref(f)))
         return p.value, f.value
 
+    def mac_count(self, input_samples: int) -> int:
+        """SPEC mac_count: the literal offline MACs over input_samples."""
+        import ctypes as C
+        r = C.c_int64()
+        _abi.check(_abi.lib().sc_graph_mac_count(*self._args(), input_samples, C.byref(r)))
+        return r.value
+
     def latency(self) -> int:
         """SPEC latency_of; NotCausal for a graph with future context."""
         import ctypes as C

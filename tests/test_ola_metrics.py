@@ -74,6 +74,20 @@ def test_metric_known_answers():
     assert po.best_lag(x, x, 20) == 0
 
 
+def test_mac_count_known_answers():
+    g = identity_graph()  # identity 1x1x1 conv, 100 samples -> 100
+    assert g.mac_count(100) == 100
+    g = Graph(2)  # K=3, N=M=2, stride 1, out_len 10 -> 120
+    g.sink(g.conv(g.source, 2, 2, 3, padding=(1, 1)))
+    assert g.mac_count(10) == 120
+    # ola-50 vs streaming on the same graph / duration: ratio 2 up to chunk-edge effects
+    g = make_synthetic_rave(SynthConfig())
+    T, N = 32 * 1024, 32 * 16
+    nc = (T - N) // (N // 2) + 1
+    assert abs(nc * g.mac_count(N) / g.mac_count(T) - 2.0) < 0.05
+    assert g.mac_count(0) == 0
+
+
 def test_ola_host_only_argument_errors():
     g = make_synthetic_rave(SynthConfig())  # ratio 32
     with pytest.raises(StreamconvError) as e:

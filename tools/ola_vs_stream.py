@@ -25,16 +25,22 @@ from paper_2204_07064_b200.graph import model_to_graph  # noqa: E402
 from paper_2204_07064_b200.runtime import Ola, Plan, StreamState, best_lag, fidelity  # noqa: E402
 
 
-def timed(fn, reps=3):
+TRIALS = 10  # SPEC metrics_bench: >= 10 trials
+
+
+def timed(fn, reps=TRIALS):
+    """Device ms per run: (mean, std) over `reps` trials after one warm-up run."""
     fn()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    ts = []
     for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         fn()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.mean(ts)), float(np.std(ts))
 
 
 def main():
@@ -71,14 +77,14 @@ def main():
             for xi, yo in zip(xin, yout):
                 st.process_buffer(xi, yo, B)
 
-        ms = timed(stream_all)
+        ms, sd = timed(stream_all)
         y = torch.cat(yout, dim=2)
         # buffers below the compression ratio add the phase-state lag: measure the total lag
         # (SPEC best_lag) and check it against the plan's latency
         lag = int(best_lag(ref[:1, 0].contiguous(), y[:1, 0].contiguous(), lat + plan.ratio)[0])
         f = fidelity(ref[:, 0, W - lag:T - W - lag].contiguous(), y[:, 0, sl].contiguous())
-        rows.append(dict(method="stream", buffer=B, calls=T // B, ms=ms, samples_per_s=S * T / ms * 1e3, latency=lag,
-                         plan_latency=lat,
+        rows.append(dict(method="stream", buffer=B, calls=T // B, ms=ms, ms_std=sd, samples_per_s=S * T / ms * 1e3,
+                         latency=lag, plan_latency=lat, macs=g.mac_count(T), state_bytes=plan.state_bytes,
                          L_s=float(np.median(f["L_s"])), L_w=float(np.median(f["L_w"])),
                          L_c=float(np.median(f["L_c"])), redundancy=1.0))
         del st
@@ -89,9 +95,11 @@ def main():
                 rows.append(dict(method=f"ola{ov}", buffer=B, error=str(e)))
                 continue
             z = torch.empty((S, 1, T), device="cuda")
-            ms = timed(lambda: o.process(xd, z, T))
+            ms, sd = timed(lambda: o.process(xd, z, T))
+            nc = (T - B) // (B * (100 - ov) // 100) + 1
             f = fidelity(ref[:, 0, sl].contiguous(), z[:, 0, sl].contiguous())
-            rows.append(dict(method=f"ola{ov}", buffer=B, calls=1, ms=ms, samples_per_s=S * T / ms * 1e3, latency=B,
+            rows.append(dict(method=f"ola{ov}", buffer=B, calls=1, ms=ms, ms_std=sd, samples_per_s=S * T / ms * 1e3,
+                             latency=B, macs=nc * g.mac_count(B), state_bytes=0,
                              L_s=float(np.median(f["L_s"])), L_w=float(np.median(f["L_w"])),
                              L_c=float(np.median(f["L_c"])), redundancy=Ola.redundancy(ov)))
             del o
@@ -112,6 +120,18 @@ def main():
             continue
         print(f"| {r['method']} | {r['buffer']} | {r['calls']} | {r['latency']} | {r['L_s']:.3e} | {r['L_w']:.3e} | {r['L_c']:.6f} | "
               f"{r['redundancy']:.2f} | {r['ms']:.2f} | {r['samples_per_s']:.3e} |")
+    # SPEC metrics_bench BenchReport: per stream; rtf = device time share per
+    # stream / audio duration (all streams processed concurrently), over TRIALS trials
+    dur = T / configs.SR
+    print("\nSPEC BenchReport (per stream, MACs per second of audio; rtf over %d trials):\n" % TRIALS)
+    print("```csv")
+    print("method,buffer,macs_per_sec,rtf_mean,rtf_std,state_bytes,latency_samples")
+    for r in rows:
+        if "error" in r:
+            continue
+        print(f"{r['method']},{r['buffer']},{r['macs'] / dur:.6e},{r['ms'] / 1e3 / S / dur:.6e},"
+              f"{r['ms_std'] / 1e3 / S / dur:.3e},{r['state_bytes']},{r['latency']}")
+    print("```")
     print("\n```json")
     for r in rows:
         print(json.dumps(r))
