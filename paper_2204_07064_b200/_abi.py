@@ -167,6 +167,8 @@ def lib() -> C.CDLL:
                 "(there is no CPU fallback)")
         L = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("SC_LIB_PATH") and not hasattr(L, name):
+                continue  # A/B experiments against an older build: newer entry points absent
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -680,8 +680,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     {
       const uint32_t bytes = static_cast<uint32_t>(BK * (ABF ? 2 : 4) * p.R * p.G) + (BF ? 1 : 2) * L::B_TILE;
       int g = 0;
+      const int taps = nk / p.cblocks;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+        int cb = 0, q = 0;  // this slab's 32-channel block and tap (advanced below, no divisions)
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
@@ -690,9 +692,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // mode's order (32-channel block major, tap minor), so its outputs do not depend on
           // the per-call tile geometry (bit-identical across buffer partitions);
           // the others take tap-major order (2% faster: the taps of one row block stay in L2)
-          const int taps = nk / p.cblocks;
-          const int cb = p.cbmaj ? kb / taps : kb % p.cblocks;
-          const int q = p.cbmaj ? kb - cb * taps : kb / p.cblocks;
           const int kw = (q * p.cblocks + cb) * BK;
           if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
           mbar_expect_tx_w(&full[s], bytes);
@@ -702,6 +701,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
             tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
             tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
+          }
+          if (p.cbmaj) {
+            if (++q == taps) q = 0, ++cb;
+          } else if (++cb == p.cblocks) {
+            cb = 0, ++q;
           }
         }
       }
@@ -792,13 +796,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         mbar_wait(stg_written, tcount & 1);
         const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
-        for (int k = 0; k < (out_cols + 31) / 32; ++k) {
-          const uint8_t* src = reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4));
-          if (p.out_t)  // fused egress: (frame, channel, stream) box of the caller's output
-            tma_store_3d(&tmap_out, src, tc.i0, oc0 + 32 * k, tc.s0);
-          else
-            tma_store_3d(&tmap_out, src, oc0 + 32 * k, tc.i0, tc.s0);
-        }
+        for (int k = 0; k < (out_cols + 31) / 32; ++k)
+          tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
+                       tc.i0, tc.s0);
         bulk_commit();
         bulk_wait_read0();
         mbar_arrive(stg_free);
@@ -958,38 +958,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
       __nv_bfloat16* stgb = reinterpret_cast<__nv_bfloat16*>(stg);  // bf16 buffers (bf16 plans)
-      if (!OBF && !p.gate && p.out_t) {
-        // fused egress: finish the tile in registers (the residual comes from the frame-major
-        // staging), then — once every epilogue thread has read its residual — write it back
-        // channel-major: slab k holds [G][32 channels][R frames] (frame contiguous), the layout
-        // of the caller's [stream][C][T] box
-        const bool fast = p.post_act != ACT_TANH && p.res_act != ACT_TANH;
-        const float ps = slope_of(p.post_act, p.post_alpha);
-        const float rs = slope_of(p.res_act, p.res_alpha);
-        const bool pmax = ps <= 1.f, rmax = rs <= 1.f;
-        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
-#pragma unroll
-        for (int u = 0; u < COLS; u += 4) {
-          float rv[4] = {0.f, 0.f, 0.f, 0.f};
-          if (p.res) {  // float4 reads of the swizzled frame-major residual slab
-            const float4 v = *reinterpret_cast<const float4*>(stg + stg_off(r, col0 + u));
-            rv[0] = v.x, rv[1] = v.y, rv[2] = v.z, rv[3] = v.w;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            float o = fast ? lin(acc[u + k], ps, pmax) : act_apply(acc[u + k], p.post_act, p.post_alpha);
-            if (p.res) o += fast ? lin(rv[k], rs, rmax) : act_apply(rv[k], p.res_act, p.res_alpha);
-            acc[u + k] = o;
-          }
-        }
-        if (p.res) named_bar(1, 256);  // the 8 epilogue warps
-        const int gi = r / p.R, ri = r - gi * p.R;
-#pragma unroll
-        for (int u = 0; u < COLS; ++u) {
-          const int col = col0 + u;
-          stg[(col >> 5) * (BM * 32) + (gi * 32 + (col & 31)) * p.R + ri] = acc[u];
-        }
-      } else if (p.gate) {
+      if (p.gate) {
 #pragma unroll
         for (int u = 0; u < COLS; u += 2) {
           const float o = gate_ool(acc[u], acc[u + 1]);
@@ -1123,8 +1092,6 @@ void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUten
 }
 
 }  // namespace
-
-int tc_num_threads() { return NUM_THREADS; }
 
 void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 12 * 256); }
 

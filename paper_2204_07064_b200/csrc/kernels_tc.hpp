@@ -47,8 +47,6 @@ struct TcParams {
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
   int a_bf, r_bf, o_bf;  // bf16 plans: input / residual / output buffer holds bf16 (else fp32)
   int cbmaj;  // 1: K-slabs channel-block major (layers that may run in window mode), else tap major
-  int out_t;  // 1: fused egress — the tile is stored channel-major straight into the caller's
-              // [stream][C][T] output (map_out dims T x C x streams, box R x 32 x G, no swizzle)
   int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)
 };
 
@@ -57,7 +55,6 @@ struct TcParams {
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st);
 
-void tc_trace_dump(long long* host);
-int tc_num_threads();  // block size of every conv_tc_kernel launch  // experiments: SC_TC_DEBUG & 32 timestamps
+void tc_trace_dump(long long* host);  // experiments: SC_TC_DEBUG & 32 timestamps
 
 }  // namespace scb

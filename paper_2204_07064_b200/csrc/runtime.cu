@@ -47,8 +47,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D tensor map (fp32 with 128B swizzle: inner box = 32 floats = 128 bytes; or bf16 with
 // 64B swizzle: inner box = 32 bf16 = 64 bytes).
 CUtensorMap make_map3(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
-                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2, bool bf16 = false,
-                      bool plain = false) {
+                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2, bool bf16 = false) {
   CUtensorMap m;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {s1_bytes, s2_bytes};
@@ -56,8 +55,7 @@ CUtensorMap make_map3(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, u
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                            const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           plain ? CU_TENSOR_MAP_SWIZZLE_NONE : bf16 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                                 : CU_TENSOR_MAP_SWIZZLE_128B,
+                           bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(SC_ERR_CUDA_BASE, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -86,11 +84,6 @@ bool bf16_store_disabled() {
 bool win_disabled() {
   const char* e = std::getenv("SC_DISABLE_WIN");
   return e && std::atoi(e) != 0;
-}
-
-bool fuse_egress_disabled() {
-  const char* e = std::getenv("SC_FUSE_EGRESS");
-  return e && std::atoi(e) == 0;  // SC_FUSE_EGRESS=0: keep the separate egress launch
 }
 
 bool tc_disabled() {
@@ -314,30 +307,7 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
         }
     }
   }
-  // fused egress: when the sink buffer is written by one tensor-core op and read by nobody
-  // else, that op's epilogue stores its tile channel-major straight into the caller's
-  // [stream][C][T] output (the TMA store box is (frames, 32 channels, streams)) and the
-  // separate egress transpose — a full read + write of the output — disappears
-  {
-    const Program& pg = plan->prog;
-    const int sb = pg.sink_buf;
-    int w = -1;
-    bool read = false;
-    for (size_t i = 0; i < nops; ++i) {
-      const ConvOp& op = pg.ops[i];
-      if (op.out_buf == sb) w = static_cast<int>(i);
-      read = read || op.in_buf == sb || op.res_buf == sb;
-      for (const SumIn& si : op.sum_in) read = read || si.buf == sb;
-    }
-    if (w >= 0 && !read && !fuse_egress_disabled() && plan->dops[w].kernel == KERNEL_TC && !plan->buf_bf16[sb]) {
-      const ConvOp& op = pg.ops[w];
-      if (!op.gate && !op.convt && pg.sink_off == 0 && pg.sink_C == op.nout && op.out_rstride == op.nout &&
-          pg.sink_act == ACT_ID && pg.sink_delay == 0 && !(op.res_buf >= 0 && plan->buf_bf16[op.res_buf]))
-        plan->fuse_egress = w;
-    }
-  }
   plan->desc = plan->prog.describe();
-  if (plan->fuse_egress >= 0) plan->desc += "egress fused into op" + std::to_string(plan->fuse_egress) + "\n";
   ck(cudaSetDevice(prev), "cudaSetDevice");
   return plan;
 }
@@ -559,12 +529,6 @@ CallPlan& State::call_plan(int64_t F) {
   cp->carry_items = items;
   cp->n_launch = 2 + (desc.empty() ? 0 : 1);
   for (int64_t t : cp->t_out) cp->n_launch += t > 0 ? 1 : 0;
-  {
-    const int fe = plan->fuse_egress;
-    cp->fused = fe >= 0 && !phase_mode && cp->t_out[fe] > 0 && cp->egress_row == cache[sb] &&
-                cp->egress_T == cp->t_out[fe] && cp->egress_T % 4 == 0;
-    if (cp->fused) cp->n_launch -= 1;
-  }
   if (!desc.empty()) {
     ck(cudaMalloc(&cp->d_desc, desc.size() * sizeof(BufDesc)), "cudaMalloc(desc)");
     ck(cudaMemcpy(cp->d_desc, desc.data(), desc.size() * sizeof(BufDesc), cudaMemcpyHostToDevice),
@@ -800,19 +764,9 @@ EgressArgs State::egress_args(float* out, const CallPlan& cp) const {
   return a;
 }
 
-TcLaunch State::fused_launch(float* out, const CallPlan& cp) const {
-  const Program& pg = plan->prog;
-  TcLaunch t = cp.tc[plan->fuse_egress];
-  t.p.out_t = 1;
-  const uint64_t T = static_cast<uint64_t>(cp.egress_T), C = static_cast<uint64_t>(pg.sink_C);
-  t.map_out = make_map3(out, T, C, static_cast<uint64_t>(streams), T * 4, C * T * 4, static_cast<uint32_t>(t.p.R), 32,
-                        static_cast<uint32_t>(t.p.G), false, true);
-  return t;
-}
-
 int State::launches(int64_t F) {
   CallPlan& cp = call_plan(F);
-  int n = 2 + (carry_slot ? 1 : 0) - (cp.fused ? 1 : 0);
+  int n = 2 + (carry_slot ? 1 : 0);
   for (int64_t t : cp.t_out) n += t > 0 ? 1 : 0;
   return n;
 }
@@ -829,17 +783,15 @@ std::string State::launch_name(int64_t F, int i) {
       const DevOp& d = plan->dops[j];
       return "op" + std::to_string(j) + " " + op.name + " [" +
              (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
-              : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]" +
-             (cp.fused && static_cast<int>(j) == plan->fuse_egress ? " +egress" : "");
+              : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";
     }
   }
-  if (!cp.fused && i == k++) return "egress";
+  if (i == k++) return "egress";
   return "";
 }
 
 void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, cudaEvent_t* ev) {
   int e = 0;
-  const bool fz = fused_call(cp, out);
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   if (carry_slot) {  // wrapped buffers first move their cache to the strip start
     if (cp.n_desc > 0) launch_carry(cp.d_desc, cp.n_desc, streams, cp.carry_items, s);
@@ -850,13 +802,8 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
     if (cp.t_out[i] == 0) continue;
     if (plan->dops[i].kernel == KERNEL_TC) {
-      if (fz && static_cast<int>(i) == plan->fuse_egress) {
-        const TcLaunch t = fused_launch(out, cp);
-        launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
-      } else {
-        const TcLaunch& t = cp.tc[i];
-        launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
-      }
+      const TcLaunch& t = cp.tc[i];
+      launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
     } else if (plan->dops[i].kernel == KERNEL_SUM) {
       launch_sum(sum_params(i, cp), s);
     } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {
@@ -866,10 +813,8 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     }
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
-  if (!fz) {
-    launch_egress(egress_args(out, cp), s);
-    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
-  }
+  launch_egress(egress_args(out, cp), s);
+  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
 }
 
 void State::check_frames(int64_t F) const {
@@ -893,19 +838,16 @@ void State::profile(const float* in, float* out, int64_t F, int steps, float* ms
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
-  // profile layout: launches(F) slots (the carry slot is always present when the state has
-  // caches), plus the egress slot when this output pointer cannot take the fused egress
-  auto slots = [&](const CallPlan& c) { return launches(F) + ((c.fused && !fused_call(c, out)) ? 1 : 0); };
-  const int n = slots(call_plan(F));
+  const int n = launches(F);  // the layout (the carry slot is present whenever the state has caches)
   for (int i = 0; i < n; ++i) ms[i] = 0.f;
   std::vector<cudaEvent_t> ev(static_cast<size_t>(n + 1) * steps);
   for (auto& e : ev) ck(cudaEventCreate(&e), "EventCreate");
   int done = 0;
   for (int k = 0; k < steps; ++k) {
     CallPlan& cp = call_plan(F);
-    const bool same = slots(cp) == n;
+    const bool same = launches(F) == n;
     enqueue(in, out, cp, s, same ? ev.data() + static_cast<size_t>(k) * (n + 1) : nullptr);
-    launched += call_launches(cp, out);
+    launched += cp.n_launch;
     advance(F, cp);
     if (same) ++done;
   }
@@ -934,7 +876,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   if (!use_graphs) {
     enqueue(in, out, cp, s, nullptr);
     ck(cudaGetLastError(), "launch");
-    launched += call_launches(cp, out);
+    launched += cp.n_launch;
   } else {
     const auto key = std::make_pair(in, out);
     auto it = cp.graphs.find(key);
@@ -943,17 +885,6 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
       // pointers change: a capture happens once per CallPlan (the strip cycle's few plans are
       // all met within the first calls), never again in steady state.
       GraphEntry g;
-      const bool fz = fused_call(cp, out);
-      if (cp.graphs.size() >= static_cast<size_t>(graphs_per_plan())) {
-        auto lru = cp.graphs.begin();
-        for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
-          if (jt->second.last_use < lru->second.last_use) lru = jt;
-        if (lru->second.fused != fz) {  // other launch shape: drop it, capture anew below
-          cudaGraphExecDestroy(lru->second.exec);
-          cudaGraphDestroy(lru->second.graph);
-          cp.graphs.erase(lru);
-        }
-      }
       if (cp.graphs.size() >= static_cast<size_t>(graphs_per_plan())) {
         auto lru = cp.graphs.begin();
         for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
@@ -961,27 +892,17 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         g = lru->second;
         cp.graphs.erase(lru);
         g.ia = ingest_args(in, cp);
+        g.ea = egress_args(out, cp);
         void* a1[] = {&g.ia};
         cudaKernelNodeParams kp = g.ingest_params;
         kp.kernelParams = a1;
         kp.extra = nullptr;
         ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
-        if (fz) {  // the fused conv's output tensor map follows the caller's buffer
-          g.fl = fused_launch(out, cp);
-          CUtensorMap mw = plan->dops[plan->fuse_egress].map_w;
-          void* a3[] = {&g.fl.map_a, &mw, &g.fl.map_out, &g.fl.map_res, &g.fl.p};
-          kp = g.fused_params;
-          kp.kernelParams = a3;
-          kp.extra = nullptr;
-          ck(cudaGraphExecKernelNodeSetParams(g.exec, g.fused_node, &kp), "ExecKernelNodeSetParams");
-        } else {
-          g.ea = egress_args(out, cp);
-          void* a2[] = {&g.ea};
-          kp = g.egress_params;
-          kp.kernelParams = a2;
-          kp.extra = nullptr;
-          ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
-        }
+        void* a2[] = {&g.ea};
+        kp = g.egress_params;
+        kp.kernelParams = a2;
+        kp.extra = nullptr;
+        ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
       } else {
         ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
         enqueue(in, out, cp, capture_stream, nullptr);
@@ -1009,26 +930,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
             g.egress_params = kp;
           }
         }
-        g.fused = fz;
-        if (fz) {
-          // the fused conv: the one tensor-core launch (480 threads, 5 parameters) whose TcParams
-          // carries out_t
-          for (cudaGraphNode_t nd : nodes) {
-            cudaGraphNodeType ty;
-            ck(cudaGraphNodeGetType(nd, &ty), "NodeGetType");
-            if (ty != cudaGraphNodeTypeKernel) continue;
-            cudaKernelNodeParams kp;
-            ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-            if (kp.blockDim.x != static_cast<unsigned>(tc_num_threads()) || !kp.kernelParams) continue;
-            const TcParams* tp = static_cast<const TcParams*>(kp.kernelParams[4]);
-            if (tp->out_t) {
-              g.fused_node = nd;
-              g.fused_params = kp;
-            }
-          }
-        }
-        if (!g.ingest_node || (!g.egress_node && !g.fused_node))
-          fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
+        if (!g.ingest_node || !g.egress_node) fail(SC_ERR_INVALID_ARGUMENT, "graph I/O nodes not found");
         ck(cudaGraphInstantiate(&g.exec, graph, 0), "GraphInstantiate");
         ck(cudaGraphUpload(g.exec, s), "GraphUpload");
         g.ia = ingest_args(in, cp);
@@ -1038,7 +940,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
     }
     it->second.last_use = ++use_clock;
     ck(cudaGraphLaunch(it->second.exec, s), "GraphLaunch");
-    launched += call_launches(cp, out);
+    launched += cp.n_launch;
   }
   advance(F, cp);
   ck(cudaSetDevice(prev), "cudaSetDevice");

@@ -43,18 +43,9 @@ struct Plan {
   float* wmem = nullptr;
   std::vector<DevOp> dops;
   std::vector<uint8_t> buf_bf16;  // bf16 plans: buffers touched only by tensor-core ops hold bf16
-  int fuse_egress = -1;  // op whose tensor-core epilogue stores the sink channel-major into the
-                         // caller's output (no egress launch), or -1
   std::string desc;
   int fw(size_t b) const { return buf_bf16[b] ? prog.bufs[b].C / 2 : prog.bufs[b].C; }  // words/frame
   ~Plan();
-};
-
-struct TcLaunch {
-  CUtensorMap map_a{};
-  CUtensorMap map_out{};
-  CUtensorMap map_res{};
-  TcParams p{};
 };
 
 struct GraphEntry {
@@ -64,11 +55,14 @@ struct GraphEntry {
   cudaKernelNodeParams ingest_params{}, egress_params{};
   IngestArgs ia{};
   EgressArgs ea{};
-  cudaGraphNode_t fused_node = nullptr;  // fused-egress conv (its output map follows `out`)
-  cudaKernelNodeParams fused_params{};
-  TcLaunch fl{};
-  bool fused = false;  // captured with the fused egress (16-byte aligned output)
   uint64_t last_use = 0;
+};
+
+struct TcLaunch {
+  CUtensorMap map_a{};
+  CUtensorMap map_out{};
+  CUtensorMap map_res{};
+  TcParams p{};
 };
 
 // One call's launch geometry.  Calls whose buffer length F is a multiple of the compression
@@ -87,7 +81,6 @@ struct CallPlan {
   int n_desc = 0;
   int64_t carry_items = 0;
   int n_launch = 0;           // kernels one call of this plan launches
-  bool fused = false;         // the sink op stores into the caller's output (no egress launch)
   std::vector<TcLaunch> tc;
   std::map<std::pair<const float*, float*>, GraphEntry> graphs;
 };
@@ -133,15 +126,6 @@ struct State {
   SumParams sum_params(size_t op, const CallPlan& cp) const;
   IngestArgs ingest_args(const float* in, const CallPlan& cp) const;
   EgressArgs egress_args(float* out, const CallPlan& cp) const;
-  TcLaunch fused_launch(float* out, const CallPlan& cp) const;  // the sink op, storing into `out`
-  // the fused egress runs when the plan allows it and the caller's output is 16-byte aligned
-  // (a TMA requirement); otherwise the sink op writes its buffer and egress transposes it
-  bool fused_call(const CallPlan& cp, const void* out) const {
-    return cp.fused && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  }
-  int call_launches(const CallPlan& cp, const void* out) const {
-    return cp.n_launch + ((cp.fused && !fused_call(cp, out)) ? 1 : 0);
-  }
   void check_frames(int64_t frames) const;
   void enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, cudaEvent_t* ev);
   void profile(const float* in, float* out, int64_t frames, int steps, float* ms, cudaStream_t s);
