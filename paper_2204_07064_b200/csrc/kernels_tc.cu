@@ -45,6 +45,14 @@ __device__ long long g_tc_trace[12 * 256];  // SC_TC_DEBUG & 32: per-K-block tim
 
 __device__ __forceinline__ long long clk() { return clock64(); }  // SM cycles (per-SM counter)
 
+// Experiment hooks (per-slab trace timestamps, MMA / prefetch switches: TcParams::debug) are
+// compiled in only with -DSC_TC_EXPERIMENTS=1 — even untaken, their branches cost the hot
+// loops measurable time.
+#ifndef SC_TC_EXPERIMENTS
+#define SC_TC_EXPERIMENTS 0
+#endif
+#define TC_DBG(p) (SC_TC_EXPERIMENTS ? (p).debug : 0)
+
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzled row
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_out)) : "memory");
   }
-  if ((p.debug & 32) && threadIdx.x == 0 && blockIdx.x < 256) {
+  if ((TC_DBG(p) & 32) && threadIdx.x == 0 && blockIdx.x < 256) {
     g_tc_trace[7 * 256 + blockIdx.x] = clk();
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -489,7 +497,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
         const int sa = u % L::AST;
         if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
-        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
         mbar_expect_tx_w(&wa_full[sa], a_bytes);
         tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
         if (p.wres) continue;
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
             const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
             const int ws = p.wres ? kb : s;
-            if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
             const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
             // corrections first (2^-10 of the signal), then the main product, all into this
             // chunk's accumulator: the truncating accumulation meets the large terms only in
@@ -556,7 +564,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
           }
           if (!p.wres) mma_commit_w(&empty[s]);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
             mma_commit_w(&tfull[b]);
             ++c;
@@ -576,7 +584,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
         const int sa = u % L::AST;
         mbar_wait(&wa_full[sa], (u / L::AST) & 1);
-        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
         if (BF) {
           // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
           // (SW64 rows of 64 B, 16B chunk jo at jo ^ ((w >> 1) & 3)); item = (row, output chunk)
@@ -672,7 +680,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async();  // generic smem writes -> read by the tensor core (async proxy)
         __syncwarp();
         if (lane == 0) mbar_arrive(&wa_ready[sa]);
-        if ((p.debug & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[2 * 256 + u] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[2 * 256 + u] = clk();
       }
     }
   } else if (warp == 0) {
@@ -687,13 +695,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
           // K-slab order: a layer that may also run in window mode (cbmaj) takes the window
           // mode's order (32-channel block major, tap minor), so its outputs do not depend on
           // the per-call tile geometry (bit-identical across buffer partitions);
           // the others take tap-major order (2% faster: the taps of one row block stay in L2)
           const int kw = (q * p.cblocks + cb) * BK;
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
           mbar_expect_tx_w(&full[s], bytes);
           tma_load_3d_w(&tmap_a, &full[s], a_hi(s), p.a_c0 + cb * BK, p.a_row0 + tc.i0 + q * p.a_tap_rows, tc.s0);
           if (BF) {
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
           if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
           mbar_wait(&xform[s], (g / STAGES) & 1);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
           tc_fence_after();
           const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
           if (BF) {
@@ -749,7 +757,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
             const uint32_t ahi = tbase + A_COL + 64 * (g % TS);
             const uint32_t alo = ahi + 32;
-            if (!(p.debug & 2)) {
+            if (!(TC_DBG(p) & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) {
                 const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
@@ -759,13 +767,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
-              const uint32_t acc0 = (!chunk_first || kk > 0 || !(p.debug & 2)) ? 1u : 0u;
+              const uint32_t acc0 = (!chunk_first || kk > 0 || !(TC_DBG(p) & 2)) ? 1u : 0u;
               mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
             }
             mma_commit_w(&aempty[g % TS]);
           }
           mma_commit_w(&empty[s]);
-          if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
             mma_commit_w(&tfull[b]);
             ++c;
@@ -789,7 +797,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
           // warm L2 with the next tile's residual: its load is issued only once this tile's
           // output has left staging, so it must not also pay the DRAM latency
-          if (tile + static_cast<int>(gridDim.x) < n_tiles && !(p.debug & 4)) {
+          if (tile + static_cast<int>(gridDim.x) < n_tiles && !(TC_DBG(p) & 4)) {
             const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n2, BN);
             for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
           }
@@ -813,7 +821,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
-        if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[1 * 256 + g] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[1 * 256 + g] = clk();
         if (BF) {
           // thread = tile row r (= TMEM lane): fp32 SW128 row (16B chunk j at j ^ (r & 7)) ->
           // pre-activation -> bf16 pairs (low half = even k) -> this stage's TMEM A columns
@@ -906,7 +914,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&xform[s]);
-        if ((p.debug & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[2 * 256 + g] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[2 * 256 + g] = clk();
       }
     }
   } else if (warp >= EP_WARP0) {
@@ -929,7 +937,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool first = (kb / CK) == 0;
         const int b = c % NB;
         mbar_wait(&tfull[b], (c / NB) & 1);
-        if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < COLS; cc += (COLS >= 32 ? 32 : 16)) {  // main chunk, 32 columns per wait
@@ -945,11 +953,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
-        if ((p.debug & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
         ++c;
       }
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
-      const bool trace = (p.debug & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
+      const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
       if (p.res) {
         mbar_wait(res_full, tcount & 1);
@@ -1042,7 +1050,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if ((p.debug & 32) && threadIdx.x == 0 && blockIdx.x < 256) g_tc_trace[8 * 256 + blockIdx.x] = clk();
+  if ((TC_DBG(p) & 32) && threadIdx.x == 0 && blockIdx.x < 256) g_tc_trace[8 * 256 + blockIdx.x] = clk();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)

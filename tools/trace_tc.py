@@ -1,4 +1,5 @@
-"""Experiment: per-K-block timeline of CTA 0 of the LAST launched TC conv (SC_TC_DEBUG=32)."""
+"""Experiment: per-K-block timeline of CTA 0 of the LAST launched TC conv (SC_TC_DEBUG=32).
+Needs a library built with -DSC_TC_EXPERIMENTS=1 (the trace hooks are compiled out otherwise)."""
 import ctypes as C
 import os
 import sys
