@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--io", default="fp32", choices=["fp32", "bf16"],
+                    help="host buffer type of the e2e leg (bf16: sc_process_host_bf16, half the PCIe bytes)")
     return ap.parse_args()
 
 
@@ -257,18 +259,21 @@ def main():
     # ---- e2e through the public C-ABI host-buffer call (sc_process_host): every step's
     # input is copied H2D from pinned host memory and its output D2H inside the timed region;
     # the library overlaps call k's copies with call k-1/k+1's compute on separate streams
-    hx = [xs[k].cpu().pin_memory() for k in range(2)]
-    hy = [torch.empty((streams, cout, out_call), pin_memory=True) for _ in range(2)]
+    io16 = args.io == "bf16"
+    io_dt = torch.bfloat16 if io16 else torch.float32
+    hx = [xs[k].to(io_dt).cpu().pin_memory() for k in range(2)]
+    hy = [torch.empty((streams, cout, out_call), dtype=io_dt, pin_memory=True) for _ in range(2)]
+    host_call = st.process_host_bf16 if io16 else st.process_host
     st.reset(stream=stream)
     for k in range(2):
-        st.process_host(hx[k], hy[k], frames, stream)
+        host_call(hx[k], hy[k], frames, stream)
     st.host_wait(stream)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):
-        st.process_host(hx[k % 2], hy[k % 2], frames, stream)
+        host_call(hx[k % 2], hy[k % 2], frames, stream)
     st.host_wait(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -343,8 +348,8 @@ def main():
                               "note": "whole-step bound max(F/P_bf16_sustained, bytes/HBM); path_ms uses "
                                       "the precision's tensor ceiling (3xTF32: P_bf16_sustained / 6)"},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": in_bytes,
-                    "d2h_bytes_per_step": out_bytes},
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": hx[0].numel() * hx[0].element_size(),
+                    "d2h_bytes_per_step": hy[0].numel() * hy[0].element_size(), "host_io": args.io},
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "profile_ms": {n: round(t, 4) for n, t in prof},

@@ -176,6 +176,11 @@ SC_API int sc_process(sc_state* state, const float* d_in, float* d_out, int64_t 
 SC_API int sc_process_host(sc_state* state, const float* h_in, float* h_out, int64_t frames,
                            void* stream);
 SC_API int sc_process_host_wait(sc_state* state, void* stream);
+/* sc_process_host with bf16 host buffers (uint16 bit patterns, same [stream][C][T] layouts):
+ * half the PCIe bytes; the device widens the input to fp32 and rounds the fp32 output to bf16
+ * (nearest-even) — for the bf16-operand variant, whose stated error bound covers it. */
+SC_API int sc_process_host_bf16(sc_state* state, const uint16_t* h_in, uint16_t* h_out,
+                                int64_t frames, void* stream);
 /* Launch slots of one sc_process call (profile layout): carry (wrap-around calls only, see
  * DESIGN.md §3 strips), ingest, one per firing op, egress. */
 SC_API int sc_process_launches(const sc_state* state, int64_t frames, int32_t* n);

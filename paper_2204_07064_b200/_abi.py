@@ -141,6 +141,7 @@ _SIGS = {
     "sc_process": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_host_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sc_process_host_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_launches": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32)]),
     "sc_state_launch_total": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_state_set_graphs": (C.c_int, [C.c_void_p, C.c_int32]),

@@ -396,6 +396,13 @@ int sc_process_host(sc_state* state, const float* h_in, float* h_out, int64_t fr
   });
 }
 
+int sc_process_host_bf16(sc_state* st, const uint16_t* h_in, uint16_t* h_out, int64_t frames, void* stream) {
+  return guard([&] {
+    need(st != nullptr, "null state");
+    st->s->process_host_bf16(h_in, h_out, frames, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int sc_process_host_wait(sc_state* state, void* stream) {
   return guard([&] {
     need(state != nullptr, "null state");

@@ -55,6 +55,10 @@ struct SumParams {
 };
 void launch_sum(const SumParams& p, cudaStream_t st);
 
+// bf16 <-> fp32 element casts for the bf16 host I/O path (to_f32: bf16 -> fp32, else fp32 ->
+// bf16 round-to-nearest-even).
+void launch_cast(uint16_t* bf, float* f, int64_t n, bool to_f32, cudaStream_t st);
+
 // Batched cache carry: for every buffer with cache > 0, frames [T, T+cache) -> [0, cache)
 // for every stream.  `items` = sum over buffers of streams*C (precomputed).
 void launch_carry(const BufDesc* d_bufs, int nbuf, int streams, int64_t items, cudaStream_t st);

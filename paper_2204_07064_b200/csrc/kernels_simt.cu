@@ -501,6 +501,16 @@ __global__ void __launch_bounds__(256) sum_kernel(const SumParams p) {
   }
 }
 
+__global__ void __launch_bounds__(256) cast_kernel(uint16_t* bf, float* f, int64_t n, int to_f32) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (to_f32)
+      f[i] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(bf)[i]);
+    else
+      reinterpret_cast<__nv_bfloat16*>(bf)[i] = __float2bfloat16_rn(f[i]);
+  }
+}
+
 int grid_for(int64_t items, int threads) {
   int64_t g = (items + threads - 1) / threads;
   const int64_t cap = 148 * 32;
@@ -547,6 +557,11 @@ void launch_conv_simt(const ConvParams& p, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>((M + 255) / 256), (p.nout + 15) / 16);
     conv_simt_kernel<256, 16, 4, 4><<<grid, 256, 0, st>>>(p);
   }
+}
+
+void launch_cast(uint16_t* bf, float* f, int64_t n, bool to_f32, cudaStream_t st) {
+  if (n <= 0) return;
+  cast_kernel<<<grid_for(n, 256), 256, 0, st>>>(bf, f, n, to_f32 ? 1 : 0);
 }
 
 void launch_sum(const SumParams& p, cudaStream_t st) {

@@ -328,6 +328,8 @@ State::~State() {
   for (int k = 0; k < 2; ++k) {
     if (io_in[k]) cudaFree(io_in[k]);
     if (io_out[k]) cudaFree(io_out[k]);
+    if (io_in16[k]) cudaFree(io_in16[k]);
+    if (io_out16[k]) cudaFree(io_out16[k]);
     if (ev_entry[k]) cudaEventDestroy(ev_entry[k]);
     if (ev_h2d[k]) cudaEventDestroy(ev_h2d[k]);
     if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
@@ -951,6 +953,16 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
 // call k+1's H2D and call k-1's D2H overlap call k's compute.  The H2D is ordered after the
 // work already on `s` (entry event); host_wait(s) orders `s` after the last call's D2H.
 void State::process_host(const float* h_in, float* h_out, int64_t F, cudaStream_t s) {
+  process_host_io(h_in, h_out, F, s, false);
+}
+
+void State::process_host_bf16(const uint16_t* h_in, uint16_t* h_out, int64_t F, cudaStream_t s) {
+  process_host_io(h_in, h_out, F, s, true);
+}
+
+// bf16 = true: the host buffers hold bf16 ([stream][C][T] like the fp32 ones) — half the PCIe
+// bytes; the device widens the input to fp32 before the call and rounds the output (RN) after.
+void State::process_host_io(const void* h_in, void* h_out, int64_t F, cudaStream_t s, bool bf16) {
   check_frames(F);
   if (!h_in || !h_out) fail(SC_ERR_INVALID_ARGUMENT, "null host pointer");
   const Program& pg = plan->prog;
@@ -974,23 +986,35 @@ void State::process_host(const float* h_in, float* h_out, int64_t F, cudaStream_
     io_in_floats = in_f;
     io_out_floats = out_f;
   }
+  if (bf16 && !io_in16[0]) {
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaMalloc(&io_in16[k], sizeof(uint16_t) * in_f), "cudaMalloc(io bf16)");
+      ck(cudaMalloc(&io_out16[k], sizeof(uint16_t) * std::max<int64_t>(out_f, 1)), "cudaMalloc(io bf16)");
+    }
+  }
   const int k = static_cast<int>(host_calls & 1);
-  const size_t in_bytes = sizeof(float) * static_cast<size_t>(streams) * pg.in_C * F;
-  const size_t out_bytes =
-      sizeof(float) * static_cast<size_t>(streams) * pg.sink_C * (F * pg.sink_rate.num / pg.sink_rate.den);
+  const size_t es = bf16 ? sizeof(uint16_t) : sizeof(float);
+  const int64_t n_in = static_cast<int64_t>(streams) * pg.in_C * F;
+  const int64_t n_out = static_cast<int64_t>(streams) * pg.sink_C * (F * pg.sink_rate.num / pg.sink_rate.den);
+  const size_t in_bytes = es * static_cast<size_t>(n_in);
+  const size_t out_bytes = es * static_cast<size_t>(n_out);
   ck(cudaEventRecord(ev_entry[k], s), "EventRecord");
   ck(cudaStreamWaitEvent(s_h2d, ev_entry[k], 0), "StreamWaitEvent");
   if (host_calls >= 2) ck(cudaStreamWaitEvent(s_h2d, ev_comp[k], 0), "StreamWaitEvent");  // slot k read
-  ck(cudaMemcpyAsync(io_in[k], h_in, in_bytes, cudaMemcpyHostToDevice, s_h2d), "H2D");
+  ck(cudaMemcpyAsync(bf16 ? static_cast<void*>(io_in16[k]) : static_cast<void*>(io_in[k]), h_in, in_bytes,
+                     cudaMemcpyHostToDevice, s_h2d), "H2D");
   ck(cudaEventRecord(ev_h2d[k], s_h2d), "EventRecord");
   ck(cudaStreamWaitEvent(s_comp, ev_h2d[k], 0), "StreamWaitEvent");
   if (host_calls >= 2) ck(cudaStreamWaitEvent(s_comp, ev_d2h[k], 0), "StreamWaitEvent");  // slot k drained
+  if (bf16) launch_cast(io_in16[k], io_in[k], n_in, true, s_comp);  // bf16 -> fp32
   ck(cudaSetDevice(prev), "cudaSetDevice");
   process(io_in[k], io_out[k], F, s_comp);
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
+  if (bf16) launch_cast(io_out16[k], io_out[k], n_out, false, s_comp);  // fp32 -> bf16 (RN)
   ck(cudaEventRecord(ev_comp[k], s_comp), "EventRecord");
   ck(cudaStreamWaitEvent(s_d2h, ev_comp[k], 0), "StreamWaitEvent");
-  ck(cudaMemcpyAsync(h_out, io_out[k], out_bytes, cudaMemcpyDeviceToHost, s_d2h), "D2H");
+  ck(cudaMemcpyAsync(h_out, bf16 ? static_cast<void*>(io_out16[k]) : static_cast<void*>(io_out[k]), out_bytes,
+                     cudaMemcpyDeviceToHost, s_d2h), "D2H");
   ck(cudaEventRecord(ev_d2h[k], s_d2h), "EventRecord");
   ++host_calls;
   ck(cudaSetDevice(prev), "cudaSetDevice");

@@ -135,8 +135,12 @@ struct State {
   // host-buffer path: H2D / compute / D2H on three streams, double-buffered across calls
   void process_host(const float* h_in, float* h_out, int64_t frames, cudaStream_t s);
   void host_wait(cudaStream_t s);
+  void process_host_bf16(const uint16_t* h_in, uint16_t* h_out, int64_t frames, cudaStream_t s);
+  void process_host_io(const void* h_in, void* h_out, int64_t frames, cudaStream_t s, bool bf16);
   float* io_in[2] = {nullptr, nullptr};
   float* io_out[2] = {nullptr, nullptr};
+  uint16_t* io_in16[2] = {nullptr, nullptr};   // bf16 host I/O staging (sc_process_host_bf16)
+  uint16_t* io_out16[2] = {nullptr, nullptr};
   int64_t io_in_floats = 0, io_out_floats = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_entry[2] = {}, ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};

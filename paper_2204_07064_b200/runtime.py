@@ -149,6 +149,12 @@ class StreamState:
         check(lib().sc_process_host(self._h, C.c_void_p(_hptr(x)), C.c_void_p(_hptr(y)), frames,
                                     C.c_void_p(_stream_handle(stream))))
 
+    def process_host_bf16(self, x, y, frames: int, stream=None) -> None:
+        """process_host with bf16 host buffers (torch.bfloat16 pinned tensors or uint16 arrays):
+        half the PCIe bytes; outputs rounded to bf16 on the device."""
+        check(lib().sc_process_host_bf16(self._h, C.c_void_p(_hptr(x)), C.c_void_p(_hptr(y)), frames,
+                                         C.c_void_p(_stream_handle(stream))))
+
     def host_wait(self, stream=None) -> None:
         """Order `stream` after the last process_host call's device->host copy."""
         check(lib().sc_process_host_wait(self._h, C.c_void_p(_stream_handle(stream))))

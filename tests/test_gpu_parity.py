@@ -251,6 +251,30 @@ def test_process_host_matches_device():
     assert np.array_equal(y_host, y_dev)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_process_host_bf16_io(precision):
+    """sc_process_host_bf16: bf16 host buffers in and out == the fp32 host path on the same
+    (bf16-representable) input, its output rounded to bf16 (nearest-even) on the device."""
+    m = configs.build(2, seed=3)
+    x = configs.batch_input(2, range(2), 128, 1024, seed=3)
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    x32 = xb.to(torch.float32).numpy()  # exactly representable in bf16
+    plan = Plan(m, precision=precision)
+    y32, _, _ = run_gpu(m, x32, [512, 512], plan=plan)
+    st = StreamState(plan, 2, 512)
+    outs = []
+    for k in range(2):
+        hx = xb[:, :, 512 * k:512 * (k + 1)].contiguous().pin_memory()
+        hy = torch.empty((2, 128, 512), dtype=torch.bfloat16).pin_memory()
+        st.process_host_bf16(hx, hy, 512)
+        outs.append(hy)
+    st.host_wait()
+    torch.cuda.synchronize()
+    yb = torch.cat(outs, 2)
+    assert torch.equal(yb, torch.from_numpy(y32).to(torch.bfloat16))
+
+
 def _pqmf_model():
     from paper_2204_07064_b200.graph import Model
     m = Model(in_channels=1)

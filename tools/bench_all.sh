@@ -6,6 +6,7 @@ out=gpurun_out/bench_all.jsonl
 run() { timeout 300 python bench.py "$@" --no-cpu-baseline 2>/dev/null | tail -1 >> $out || echo "{\"failed\": \"$*\"}" >> $out; }
 run --config 2 --steps 20 --warmup 5
 run --config 2 --steps 20 --warmup 5 --precision bf16
+run --config 2 --steps 20 --warmup 5 --precision bf16 --io bf16
 run --config 1 --steps 20 --warmup 5
 run --config 3 --steps 20 --warmup 5
 run --config 3 --steps 20 --warmup 5 --precision bf16
