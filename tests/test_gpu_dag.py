@@ -90,3 +90,67 @@ def test_dag_plan_reports_sum_launches():
     assert rel_err(y_gpu, po.run(g, x, [16, 48], "stream"))[0] <= FP32_TOL
     names = st.launch_names(16)
     assert any("simt-sum" in n for n in names), names
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [2, 5, 11, 17])
+def test_random_dags_phase_state(seed):
+    """Buffers shorter than the compression ratio (phase state) on DAGs whose branches keep
+    their rate: the GPU stream equals the oracle's phase-mode stream delayed by the fixed lag."""
+    for k in range(40):  # find a strided DAG without rate changes inside a Sum branch
+        g = random_graph(100 * seed + k, max_den=4)
+        r = g.compression_ratio()
+        if r < 2:
+            continue
+        try:
+            p = Plan(g)
+            from paper_2204_07064_b200.runtime import StreamState
+            StreamState(p, 2, 1)
+        except Exception:  # noqa: BLE001  (UnsupportedFormat: rate-changing Sum branch)
+            continue
+        break
+    else:
+        pytest.skip("no suitable graph")
+    B = 1
+    parts = [B] * (8 * r)
+    x = np.random.default_rng(seed).standard_normal((2, g.in_channels, sum(parts))).astype(np.float32)
+    y_or = po.run(g, x, parts, "phase")
+    y_gpu, plan, _ = run_gpu(g, x, parts)
+    D = r - B  # the sink lag of phase state (DESIGN.md §3), in sink frames at rate 1
+    num, den, _ = plan.sink
+    Ds = D * num // den
+    err, rms = rel_err(y_gpu[..., Ds:], y_or[..., :y_or.shape[-1] - Ds])
+    assert err <= FP32_TOL, (seed, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4))
+def test_random_dags_bf16(seed):
+    """bf16-operand plans on DAGs (sums stay fp32 SIMT): within the stated bf16 bound."""
+    from test_gpu_parity import BF16_MAX, BF16_NRMSE
+    g = random_graph(2000 + seed, channels=(32, 64), depth=5)
+    r = g.compression_ratio()
+    parts = _parts(r, seed)
+    x = np.random.default_rng(seed).standard_normal((3, g.in_channels, sum(parts))).astype(np.float32)
+    y_or = po.run(g, x, parts, "stream")
+    y_gpu, _, _ = run_gpu(g, x, parts, precision="bf16")
+    diff = (y_gpu - y_or).astype(np.float64)
+    rms = float(np.sqrt(np.mean(y_or.astype(np.float64) ** 2)))
+    assert float(np.sqrt(np.mean(diff ** 2))) / rms <= BF16_NRMSE
+    assert float(np.abs(diff).max()) / rms <= BF16_MAX
+
+
+@pytest.mark.gpu
+def test_ola_bf16_precision():
+    """The OLA baseline over a bf16 plan stays within the bf16 bound of the fp32 oracle OLA."""
+    from paper_2204_07064_b200.runtime import Ola
+    from test_gpu_parity import BF16_NRMSE
+    g = make_synthetic_rave(SynthConfig(base_channels=16, seed=4))
+    T, chunk = 256 * 6, 256
+    x = np.random.default_rng(0).standard_normal((2, 1, T)).astype(np.float32)
+    y_or = po.ola(g, x, chunk, 50)
+    y = torch.empty(y_or.shape, device="cuda")
+    Ola(g, chunk, 50, 2, T, precision="bf16").process(torch.from_numpy(x).cuda(), y, T)
+    torch.cuda.synchronize()
+    d = (y.cpu().numpy() - y_or).astype(np.float64)
+    assert np.sqrt(np.mean(d ** 2)) / np.sqrt(np.mean(y_or.astype(np.float64) ** 2)) <= BF16_NRMSE
