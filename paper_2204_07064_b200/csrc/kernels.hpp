@@ -29,6 +29,8 @@ void launch_ingest(const IngestArgs& a, cudaStream_t st);
 void launch_egress(const EgressArgs& a, cudaStream_t st);
 const void* ingest_kernel_ptr();
 const void* egress_kernel_ptr();
+const void* egress_wide_kernel_ptr();
+bool egress_wide(const EgressArgs& a);  // launch_egress picks egress_wide_kernel
 
 // Generic SIMT cached conv (FFMA, fp32 accumulate): narrow layers and the v0 dense path.
 void launch_conv_simt(const ConvParams& p, cudaStream_t st);

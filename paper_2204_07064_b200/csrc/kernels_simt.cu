@@ -396,6 +396,47 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
   }
 }
 
+// Wide sinks (C a multiple of 32, T a multiple of 128, aligned): 32 channels x 128 frames per
+// tile, 4 float4 per thread each side with the loads issued first — more bytes in flight per
+// barrier than egress_kernel's 64-frame tiles, and 512 B channel-major rows on the write side.
+// A kernel of its own so the narrow paths keep egress_kernel's register budget.
+__global__ void __launch_bounds__(256) egress_wide_kernel(const EgressArgs a) {
+  constexpr int ET = 2 * TT;
+  __shared__ float et[TC][ET + 1];
+  const int ntt = a.T / ET, ntc = a.C / TC;
+  const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  const int tid = threadIdx.x;
+  for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+    const int64_t s = tile_id / (ntt * ntc);
+    const int rem = static_cast<int>(tile_id - s * ntt * ntc);
+    const int t0 = (rem / ntc) * ET, c0 = (rem % ntc) * TC;
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + 256 * k;
+      v[k] = bget4(a.buf, a.bf, s * a.sstride, a.cache + t0 + (e >> 3), a.fstride, a.off + c0 + 4 * (e & 7));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + 256 * k;
+      const int t = e >> 3, c4 = e & 7;
+      et[4 * c4][t] = act_apply(v[k].x, a.act, a.alpha);
+      et[4 * c4 + 1][t] = act_apply(v[k].y, a.act, a.alpha);
+      et[4 * c4 + 2][t] = act_apply(v[k].z, a.act, a.alpha);
+      et[4 * c4 + 3][t] = act_apply(v[k].w, a.act, a.alpha);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + 256 * k;
+      const int c = e >> 5, t4 = e & 31;
+      *reinterpret_cast<float4*>(a.out + (s * a.C + c0 + c) * a.T + t0 + 4 * t4) =
+          make_float4(et[c][4 * t4], et[c][4 * t4 + 1], et[c][4 * t4 + 2], et[c][4 * t4 + 3]);
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------ carry / reset
 // One thread per (buffer, stream, channel column).  Frames move in ascending order in chunks
 // of 8 (all loads of a chunk before its stores): a chunk never reads a frame a previous
@@ -523,6 +564,12 @@ int grid_for(int64_t items, int threads) {
 
 const void* ingest_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_kernel); }
 const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_kernel); }
+const void* egress_wide_kernel_ptr() { return reinterpret_cast<const void*>(&egress_wide_kernel); }
+
+bool egress_wide(const EgressArgs& a) {
+  return a.C % TC == 0 && a.T % (2 * TT) == 0 && a.fstride % 4 == 0 && a.off % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
+}
 
 void launch_ingest(const IngestArgs& a, cudaStream_t st) {
   if (a.C == 1) {
@@ -537,6 +584,11 @@ void launch_ingest(const IngestArgs& a, cudaStream_t st) {
 }
 
 void launch_egress(const EgressArgs& a, cudaStream_t st) {
+  if (egress_wide(a)) {
+    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (2 * TT)) * (a.C / TC);
+    egress_wide_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    return;
+  }
   if (a.C == 1) {
     egress_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
   } else {

@@ -891,6 +891,19 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         auto lru = cp.graphs.begin();
         for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
           if (jt->second.last_use < lru->second.last_use) lru = jt;
+        // the egress kernel (wide or general) is picked per output pointer at launch: a graph
+        // captured with the other one cannot be re-targeted — drop it and capture anew
+        const bool wide = egress_wide(egress_args(out, cp));
+        if ((lru->second.egress_params.func == egress_wide_kernel_ptr()) != wide) {
+          cudaGraphExecDestroy(lru->second.exec);
+          cudaGraphDestroy(lru->second.graph);
+          cp.graphs.erase(lru);
+        }
+      }
+      if (cp.graphs.size() >= static_cast<size_t>(graphs_per_plan())) {
+        auto lru = cp.graphs.begin();
+        for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
+          if (jt->second.last_use < lru->second.last_use) lru = jt;
         g = lru->second;
         cp.graphs.erase(lru);
         g.ia = ingest_args(in, cp);
@@ -927,7 +940,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
           if (kp.func == ingest_kernel_ptr()) {
             g.ingest_node = nd;
             g.ingest_params = kp;
-          } else if (kp.func == egress_kernel_ptr()) {
+          } else if (kp.func == egress_kernel_ptr() || kp.func == egress_wide_kernel_ptr()) {
             g.egress_node = nd;
             g.egress_params = kp;
           }

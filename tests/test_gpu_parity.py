@@ -437,3 +437,25 @@ def test_profile_layout_with_strips(monkeypatch, cfg):
         names = [n for n, _ in prof]
         assert len(names) == len(set(names)) and names[0] == "carry" and names[1] == "ingest"
         assert all(t >= 0 for _, t in prof)
+
+
+@pytest.mark.gpu
+def test_graph_retarget_across_egress_kernels():
+    """Replays alternating an aligned and an unaligned output pointer: the wide egress kernel
+    (aligned, 32-channel multiples) and the general one swap in the cached graph correctly."""
+    m = configs.build(2, seed=8)
+    plan = Plan(m)
+    S, F = 2, 1024
+    x = torch.from_numpy(configs.batch_input(2, range(S), 128, F, seed=8)).cuda()
+    st_ref = StreamState(plan, S, F)
+    st_ref.set_graphs(False)
+    st = StreamState(plan, S, F)
+    raw = torch.empty(S * 128 * F + 1, device="cuda")
+    outs_a = [torch.empty((S, 128, F), device="cuda"), raw[1:].view(S, 128, F)]
+    for k in range(6):
+        y_ref = torch.empty((S, 128, F), device="cuda")
+        st_ref.process_buffer(x, y_ref, F)
+        y = outs_a[k % 2]
+        st.process_buffer(x, y, F)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref), k
