@@ -30,6 +30,8 @@ void launch_egress(const EgressArgs& a, cudaStream_t st);
 const void* ingest_kernel_ptr();
 const void* egress_kernel_ptr();
 const void* egress_wide_kernel_ptr();
+const void* ingest_wide_kernel_ptr();
+bool ingest_wide(const IngestArgs& a);  // launch_ingest picks ingest_wide_kernel
 bool egress_wide(const EgressArgs& a);  // launch_egress picks egress_wide_kernel
 
 // Generic SIMT cached conv (FFMA, fp32 accumulate): narrow layers and the v0 dense path.

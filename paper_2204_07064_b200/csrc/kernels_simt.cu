@@ -293,6 +293,46 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
   }
 }
 
+// Wide sources (C a multiple of 32, T a multiple of 128, aligned): 32 channels x 128 frames
+// per tile, the 512 B channel rows read with all of a thread's float4 loads in flight before
+// the barrier (ingest_kernel's 64-frame tiles keep two).
+__global__ void __launch_bounds__(256) ingest_wide_kernel(const IngestArgs a) {
+  constexpr int IT = 2 * TT;
+  __shared__ float it_[TC][IT + 1];
+  const int ntt = a.T / IT, ntc = a.C / TC;
+  const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
+  const int tid = threadIdx.x;
+  for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
+    const int64_t s = tile_id / (ntt * ntc);
+    const int rem = static_cast<int>(tile_id - s * ntt * ntc);
+    const int t0 = (rem / ntc) * IT, c0 = (rem % ntc) * TC;
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // 1024 float4 = 32 channel rows x 32
+      const int e = tid + 256 * k;
+      v[k] = *reinterpret_cast<const float4*>(a.in + (s * a.C + c0 + (e >> 5)) * a.T + t0 + 4 * (e & 31));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = tid + 256 * k;
+      const int c = e >> 5, t4 = e & 31;
+      it_[c][4 * t4] = v[k].x;
+      it_[c][4 * t4 + 1] = v[k].y;
+      it_[c][4 * t4 + 2] = v[k].z;
+      it_[c][4 * t4 + 3] = v[k].w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // 1024 float4 = 128 frames x 8
+      const int e = tid + 256 * k;
+      const int t = e >> 3, c4 = e & 7;
+      bput4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.C, c0 + 4 * c4,
+            make_float4(it_[4 * c4][t], it_[4 * c4 + 1][t], it_[4 * c4 + 2][t], it_[4 * c4 + 3][t]));
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
   if (a.C == 1) {
     if (a.T % 4 == 0 && a.fstride == 1 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) {  // float4 writes
@@ -565,6 +605,11 @@ int grid_for(int64_t items, int threads) {
 const void* ingest_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_kernel); }
 const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_kernel); }
 const void* egress_wide_kernel_ptr() { return reinterpret_cast<const void*>(&egress_wide_kernel); }
+const void* ingest_wide_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_wide_kernel); }
+
+bool ingest_wide(const IngestArgs& a) {
+  return a.C % TC == 0 && a.T % (2 * TT) == 0 && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
+}
 
 bool egress_wide(const EgressArgs& a) {
   return a.C % TC == 0 && a.T % (2 * TT) == 0 && a.fstride % 4 == 0 && a.off % 4 == 0 &&
@@ -572,6 +617,11 @@ bool egress_wide(const EgressArgs& a) {
 }
 
 void launch_ingest(const IngestArgs& a, cudaStream_t st) {
+  if (ingest_wide(a)) {
+    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (2 * TT)) * (a.C / TC);
+    ingest_wide_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    return;
+  }
   if (a.C == 1) {
     ingest_kernel<<<grid_for(static_cast<int64_t>(a.streams) * a.T, 256), 256, 0, st>>>(a);
   } else if (a.T < 16) {

@@ -891,10 +891,12 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         auto lru = cp.graphs.begin();
         for (auto jt = cp.graphs.begin(); jt != cp.graphs.end(); ++jt)
           if (jt->second.last_use < lru->second.last_use) lru = jt;
-        // the egress kernel (wide or general) is picked per output pointer at launch: a graph
-        // captured with the other one cannot be re-targeted — drop it and capture anew
+        // the ingest / egress kernels (wide or general) are picked per I/O pointer at launch: a
+        // graph captured with the other one cannot be re-targeted — drop it and capture anew
         const bool wide = egress_wide(egress_args(out, cp));
-        if ((lru->second.egress_params.func == egress_wide_kernel_ptr()) != wide) {
+        const bool iwide = ingest_wide(ingest_args(in, cp));
+        if ((lru->second.egress_params.func == egress_wide_kernel_ptr()) != wide ||
+            (lru->second.ingest_params.func == ingest_wide_kernel_ptr()) != iwide) {
           cudaGraphExecDestroy(lru->second.exec);
           cudaGraphDestroy(lru->second.graph);
           cp.graphs.erase(lru);
@@ -937,7 +939,7 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
           if (ty != cudaGraphNodeTypeKernel) continue;
           cudaKernelNodeParams kp;
           ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-          if (kp.func == ingest_kernel_ptr()) {
+          if (kp.func == ingest_kernel_ptr() || kp.func == ingest_wide_kernel_ptr()) {
             g.ingest_node = nd;
             g.ingest_params = kp;
           } else if (kp.func == egress_kernel_ptr() || kp.func == egress_wide_kernel_ptr()) {
