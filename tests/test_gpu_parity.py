@@ -421,8 +421,8 @@ def test_bf16_phase_state_and_reset():
 @pytest.mark.parametrize("cfg", [2, 4])
 def test_profile_layout_with_strips(monkeypatch, cfg):
     """sc_state_profile across a strip cycle (calls with and without a carry; the carry slot is
-    always in the layout) and with an output pointer that cannot take the fused egress: one
-    timing per launch name, no slot overrun."""
+    always in the layout), for an aligned and an unaligned output pointer (the wide and the
+    general egress kernel): one timing per launch name, no slot overrun."""
     monkeypatch.setenv("SC_STRIP_K", "3")
     m = configs.build(cfg, seed=1)
     plan = Plan(m)
