@@ -29,8 +29,8 @@ void launch_ingest(const IngestArgs& a, cudaStream_t st);
 void launch_egress(const EgressArgs& a, cudaStream_t st);
 const void* ingest_kernel_ptr();
 const void* egress_kernel_ptr();
-const void* egress_wide_kernel_ptr();
-const void* ingest_wide_kernel_ptr();
+bool is_egress_wide_kernel(const void* f);
+bool is_ingest_wide_kernel(const void* f);
 bool ingest_wide(const IngestArgs& a);  // launch_ingest picks ingest_wide_kernel
 bool egress_wide(const EgressArgs& a);  // launch_egress picks egress_wide_kernel
 

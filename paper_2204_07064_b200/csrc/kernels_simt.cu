@@ -293,29 +293,30 @@ __global__ void __launch_bounds__(256) ingest_kernel(const IngestArgs a) {
   }
 }
 
-// Wide sources (C a multiple of 32, T a multiple of 128, aligned): 32 channels x 128 frames
-// per tile, the 512 B channel rows read with all of a thread's float4 loads in flight before
-// the barrier (ingest_kernel's 64-frame tiles keep two).
+// Wide sources (C a multiple of TCH = 32 or 16, T a multiple of 4096 / TCH, aligned): tiles of
+// TCH channels x 4096 / TCH frames, the channel rows read with all of a thread's four float4
+// loads in flight before the barrier (ingest_kernel's 64-frame tiles keep two).
+template <int TCH>
 __global__ void __launch_bounds__(256) ingest_wide_kernel(const IngestArgs a) {
-  constexpr int IT = 2 * TT;
-  __shared__ float it_[TC][IT + 1];
-  const int ntt = a.T / IT, ntc = a.C / TC;
+  constexpr int FR = 4096 / TCH, R4 = FR / 4, C4 = TCH / 4;
+  __shared__ float it_[TCH][FR + 1];
+  const int ntt = a.T / FR, ntc = a.C / TCH;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
   const int tid = threadIdx.x;
   for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
     const int64_t s = tile_id / (ntt * ntc);
     const int rem = static_cast<int>(tile_id - s * ntt * ntc);
-    const int t0 = (rem / ntc) * IT, c0 = (rem % ntc) * TC;
+    const int t0 = (rem / ntc) * FR, c0 = (rem % ntc) * TCH;
     float4 v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // 1024 float4 = 32 channel rows x 32
+    for (int k = 0; k < 4; ++k) {  // 1024 float4 = TCH channel rows x FR / 4
       const int e = tid + 256 * k;
-      v[k] = *reinterpret_cast<const float4*>(a.in + (s * a.C + c0 + (e >> 5)) * a.T + t0 + 4 * (e & 31));
+      v[k] = *reinterpret_cast<const float4*>(a.in + (s * a.C + c0 + e / R4) * a.T + t0 + 4 * (e % R4));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int e = tid + 256 * k;
-      const int c = e >> 5, t4 = e & 31;
+      const int c = e / R4, t4 = e % R4;
       it_[c][4 * t4] = v[k].x;
       it_[c][4 * t4 + 1] = v[k].y;
       it_[c][4 * t4 + 2] = v[k].z;
@@ -323,9 +324,9 @@ __global__ void __launch_bounds__(256) ingest_wide_kernel(const IngestArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // 1024 float4 = 128 frames x 8
+    for (int k = 0; k < 4; ++k) {  // 1024 float4 = FR frames x TCH / 4
       const int e = tid + 256 * k;
-      const int t = e >> 3, c4 = e & 7;
+      const int t = e / C4, c4 = e % C4;
       bput4(a.buf, a.bf, s * a.sstride, a.cache + t0 + t, a.C, c0 + 4 * c4,
             make_float4(it_[4 * c4][t], it_[4 * c4 + 1][t], it_[4 * c4 + 2][t], it_[4 * c4 + 3][t]));
     }
@@ -436,30 +437,32 @@ __global__ void __launch_bounds__(256) egress_kernel(const EgressArgs a) {
   }
 }
 
-// Wide sinks (C a multiple of 32, T a multiple of 128, aligned): 32 channels x 128 frames per
-// tile, 4 float4 per thread each side with the loads issued first — more bytes in flight per
-// barrier than egress_kernel's 64-frame tiles, and 512 B channel-major rows on the write side.
-// A kernel of its own so the narrow paths keep egress_kernel's register budget.
+// Wide sinks (C a multiple of TCH = 32 or 16, T a multiple of 4096 / TCH, aligned): tiles of
+// TCH channels x 4096 / TCH frames, 4 float4 per thread each side with the loads issued first
+// — more bytes in flight per barrier than egress_kernel's 64-frame tiles, and long channel-
+// major rows on the write side.  Kernels of their own so the general paths keep their
+// register budget.
+template <int TCH>
 __global__ void __launch_bounds__(256) egress_wide_kernel(const EgressArgs a) {
-  constexpr int ET = 2 * TT;
-  __shared__ float et[TC][ET + 1];
-  const int ntt = a.T / ET, ntc = a.C / TC;
+  constexpr int FR = 4096 / TCH, R4 = FR / 4, C4 = TCH / 4;
+  __shared__ float et[TCH][FR + 1];
+  const int ntt = a.T / FR, ntc = a.C / TCH;
   const int64_t ntiles = static_cast<int64_t>(a.streams) * ntt * ntc;
   const int tid = threadIdx.x;
   for (int64_t tile_id = blockIdx.x; tile_id < ntiles; tile_id += gridDim.x) {
     const int64_t s = tile_id / (ntt * ntc);
     const int rem = static_cast<int>(tile_id - s * ntt * ntc);
-    const int t0 = (rem / ntc) * ET, c0 = (rem % ntc) * TC;
+    const int t0 = (rem / ntc) * FR, c0 = (rem % ntc) * TCH;
     float4 v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int e = tid + 256 * k;
-      v[k] = bget4(a.buf, a.bf, s * a.sstride, a.cache + t0 + (e >> 3), a.fstride, a.off + c0 + 4 * (e & 7));
+      v[k] = bget4(a.buf, a.bf, s * a.sstride, a.cache + t0 + e / C4, a.fstride, a.off + c0 + 4 * (e % C4));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int e = tid + 256 * k;
-      const int t = e >> 3, c4 = e & 7;
+      const int t = e / C4, c4 = e % C4;
       et[4 * c4][t] = act_apply(v[k].x, a.act, a.alpha);
       et[4 * c4 + 1][t] = act_apply(v[k].y, a.act, a.alpha);
       et[4 * c4 + 2][t] = act_apply(v[k].z, a.act, a.alpha);
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(256) egress_wide_kernel(const EgressArgs a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int e = tid + 256 * k;
-      const int c = e >> 5, t4 = e & 31;
+      const int c = e / R4, t4 = e % R4;
       *reinterpret_cast<float4*>(a.out + (s * a.C + c0 + c) * a.T + t0 + 4 * t4) =
           make_float4(et[c][4 * t4], et[c][4 * t4 + 1], et[c][4 * t4 + 2], et[c][4 * t4 + 3]);
     }
@@ -604,22 +607,39 @@ int grid_for(int64_t items, int threads) {
 
 const void* ingest_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_kernel); }
 const void* egress_kernel_ptr() { return reinterpret_cast<const void*>(&egress_kernel); }
-const void* egress_wide_kernel_ptr() { return reinterpret_cast<const void*>(&egress_wide_kernel); }
-const void* ingest_wide_kernel_ptr() { return reinterpret_cast<const void*>(&ingest_wide_kernel); }
+bool is_egress_wide_kernel(const void* f) {
+  return f == reinterpret_cast<const void*>(&egress_wide_kernel<32>) ||
+         f == reinterpret_cast<const void*>(&egress_wide_kernel<16>);
+}
+bool is_ingest_wide_kernel(const void* f) {
+  return f == reinterpret_cast<const void*>(&ingest_wide_kernel<32>) ||
+         f == reinterpret_cast<const void*>(&ingest_wide_kernel<16>);
+}
+
+// channels per wide tile (0: the general kernel)
+int wide_tch(int C, int T) {
+  if (C % 32 == 0 && T % 128 == 0) return 32;
+  if (C % 16 == 0 && T % 256 == 0) return 16;
+  return 0;
+}
 
 bool ingest_wide(const IngestArgs& a) {
-  return a.C % TC == 0 && a.T % (2 * TT) == 0 && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
+  return wide_tch(a.C, a.T) > 0 && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
 }
 
 bool egress_wide(const EgressArgs& a) {
-  return a.C % TC == 0 && a.T % (2 * TT) == 0 && a.fstride % 4 == 0 && a.off % 4 == 0 &&
+  return wide_tch(a.C, a.T) > 0 && a.fstride % 4 == 0 && a.off % 4 == 0 &&
          (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
 }
 
 void launch_ingest(const IngestArgs& a, cudaStream_t st) {
   if (ingest_wide(a)) {
-    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (2 * TT)) * (a.C / TC);
-    ingest_wide_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    const int tch = wide_tch(a.C, a.T);
+    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (4096 / tch)) * (a.C / tch);
+    if (tch == 32)
+      ingest_wide_kernel<32><<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    else
+      ingest_wide_kernel<16><<<grid_for(tiles, 1), 256, 0, st>>>(a);
     return;
   }
   if (a.C == 1) {
@@ -635,8 +655,12 @@ void launch_ingest(const IngestArgs& a, cudaStream_t st) {
 
 void launch_egress(const EgressArgs& a, cudaStream_t st) {
   if (egress_wide(a)) {
-    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (2 * TT)) * (a.C / TC);
-    egress_wide_kernel<<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    const int tch = wide_tch(a.C, a.T);
+    const int64_t tiles = static_cast<int64_t>(a.streams) * (a.T / (4096 / tch)) * (a.C / tch);
+    if (tch == 32)
+      egress_wide_kernel<32><<<grid_for(tiles, 1), 256, 0, st>>>(a);
+    else
+      egress_wide_kernel<16><<<grid_for(tiles, 1), 256, 0, st>>>(a);
     return;
   }
   if (a.C == 1) {

@@ -895,8 +895,8 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         // graph captured with the other one cannot be re-targeted — drop it and capture anew
         const bool wide = egress_wide(egress_args(out, cp));
         const bool iwide = ingest_wide(ingest_args(in, cp));
-        if ((lru->second.egress_params.func == egress_wide_kernel_ptr()) != wide ||
-            (lru->second.ingest_params.func == ingest_wide_kernel_ptr()) != iwide) {
+        if (is_egress_wide_kernel(lru->second.egress_params.func) != wide ||
+            is_ingest_wide_kernel(lru->second.ingest_params.func) != iwide) {
           cudaGraphExecDestroy(lru->second.exec);
           cudaGraphDestroy(lru->second.graph);
           cp.graphs.erase(lru);
@@ -939,10 +939,10 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
           if (ty != cudaGraphNodeTypeKernel) continue;
           cudaKernelNodeParams kp;
           ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-          if (kp.func == ingest_kernel_ptr() || kp.func == ingest_wide_kernel_ptr()) {
+          if (kp.func == ingest_kernel_ptr() || is_ingest_wide_kernel(kp.func)) {
             g.ingest_node = nd;
             g.ingest_params = kp;
-          } else if (kp.func == egress_kernel_ptr() || kp.func == egress_wide_kernel_ptr()) {
+          } else if (kp.func == egress_kernel_ptr() || is_egress_wide_kernel(kp.func)) {
             g.egress_node = nd;
             g.egress_params = kp;
           }
