@@ -1079,6 +1079,60 @@ struct DagLowerer {
 
 }  // namespace
 
+namespace {
+bool densify_disabled() {
+  const char* e = std::getenv("SC_DENSIFY");
+  return e && std::atoi(e) == 0;  // SC_DENSIFY=0: keep narrow convs in their plain form
+}
+
+// Narrow stride-1 convs on the tensor cores waste most of a tile: N <= 64 columns (the MMA
+// issue cost is per instruction, not per column) or a channel count padded to 32.  A
+// densified op reads the input as 2-frame super-rows (the strided convs' view) and emits both
+// output frames of a row at once: y[2i + phi] = b + sum_k w[k] x[2i + phi - P + k] becomes one
+// GEMM row with N' = 2N columns (phase-major) over the window's super-rows; MACs are unchanged
+// for the padded-channel case and grow by (K + 1) / K otherwise.  Ops with a residual epilogue
+// keep their form (their skip must stay in lockstep under phase state).
+void densify(Program& p) {
+  for (ConvOp& op : p.ops) {
+    const BufferSpec& bi = p.bufs[op.in_buf];
+    if (op.kind != OPK_CONV || op.convt || op.S != 1 || op.tap_step != 1 || op.row_step != 1 || op.pqmf ||
+        op.res_buf >= 0 || op.in_off != 0 || op.cin != bi.C || op.taps > 16 || op.nout > 1024)
+      continue;
+    const bool narrow = op.nout <= 64 || (op.cin % 32 != 0 && (2 * op.cin) % 32 == 0);
+    // every non-phase call delivers an even frame count to this op
+    const bool even = (p.ratio * op.in_rate.num / op.in_rate.den) % 2 == 0 &&
+                      (p.ratio * op.in_rate.num) % op.in_rate.den == 0;
+    if (!narrow || !even) continue;
+    const int64_t extra = op.look % 2;  // window start on a super-row boundary
+    const int T0 = op.taps, N = op.nout, T1 = T0 + 1 + static_cast<int>(extra);
+    std::vector<float> w(static_cast<size_t>(T1) * op.cin * 2 * N, 0.f);
+    for (int q = 0; q < T1; ++q)
+      for (int ph = 0; ph < 2; ++ph) {
+        const int k = q - ph - static_cast<int>(extra);
+        if (k < 0 || k >= T0) continue;
+        for (int c = 0; c < op.cin; ++c)
+          for (int n = 0; n < N; ++n)
+            w[(static_cast<size_t>(q) * op.cin + c) * 2 * N + ph * N + n] =
+                op.w[(static_cast<size_t>(k) * op.cin + c) * N + n];
+      }
+    op.w.swap(w);
+    std::vector<float> b(op.bias);
+    b.insert(b.end(), op.bias.begin(), op.bias.end());
+    op.bias.swap(b);
+    op.look += extra;
+    op.taps = T1;
+    op.S = 2;
+    op.row_step = 2;
+    op.phases = 2;
+    op.nout = 2 * N;
+    op.out_rstride *= 2;
+    p.bufs[op.in_buf].cache = std::max(p.bufs[op.in_buf].cache, op.look);
+    p.bufs[op.in_buf].align = Lowerer::lcm(p.bufs[op.in_buf].align, 2);
+    op.name += " x2";
+  }
+}
+}  // namespace
+
 Program lower_dag(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, const float* W,
                   int64_t nW, int in_C, bool offline) {
   if (in_C < 1) fail(SC_ERR_INVALID_ARGUMENT, "in_channels must be >= 1");
@@ -1095,8 +1149,9 @@ Program lower_dag(const sc_gnode* nodes, int n, const sc_edge* edges, int ne, co
   p.offline = offline;
   DagLowerer dl{nodes, edges, g, lw, p, std::vector<Value>(ne)};
   dl.run();
-  for (BufferSpec& b : p.bufs) b.cache = (b.cache + b.align - 1) / b.align * b.align;
   p.ratio = g.ratio;
+  if (!offline && !densify_disabled()) densify(p);
+  for (BufferSpec& b : p.bufs) b.cache = (b.cache + b.align - 1) / b.align * b.align;
   for (const ConvOp& op : p.ops) p.macs_per_sample += op.macs_per_sample;
   return p;
 }
@@ -1114,6 +1169,8 @@ Program lower_graph(const sc_node* nodes, int n_nodes, const float* W, int64_t n
   Value v;
   v.C = in_C;
   lw.parse(v, 0);
+  p.ratio = lw.ratio;
+  if (!densify_disabled()) densify(p);
   for (BufferSpec& b : p.bufs) b.cache = (b.cache + b.align - 1) / b.align * b.align;
   p.sink_buf = v.buf;
   p.sink_off = v.off;

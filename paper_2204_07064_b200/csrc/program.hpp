@@ -58,6 +58,8 @@ struct ConvOp {
   std::vector<int> pq_idx;           // synthesis class of (q, phi) [Q][M]
   int pq_period = 0;                 // synthesis canonical classes (graph.cpp); 0: irregular
   int pq_mirror = 0;
+  int phases = 1;            // output frames per GEMM row: 2 for a densified stride-1 conv
+                             // (2-frame super-rows in, 2 output phases out: N doubles)
   std::vector<float> w;      // [taps][cin][nout]  (polyphase / gate-interleaved)
   std::vector<float> bias;   // [nout]
   Rate in_rate;              // frames of the input buffer per input sample

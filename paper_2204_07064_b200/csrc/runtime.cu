@@ -373,7 +373,7 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
       n[0] += 1;
       for (const ConvOp& op : pg.ops) {
         const int64_t nin = n[op.in_buf];
-        n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? nin / op.S : nin);
+        n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? (nin / op.S) * op.phases : nin);
         bool ok = op.res_buf < 0 || n[op.res_buf] == n[op.out_buf];
         for (const SumIn& si : op.sum_in) ok = ok && n[si.buf] == nin;
         if (!ok)
@@ -464,7 +464,7 @@ std::vector<int64_t> State::next_counts(int64_t F) const {
   n[0] = N[0] + F;
   for (const ConvOp& op : pg.ops) {
     const int64_t nin = n[op.in_buf];
-    n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? nin / op.S : nin);
+    n[op.out_buf] = op.convt ? nin * op.r : (op.S > 1 ? (nin / op.S) * op.phases : nin);
   }
   return n;
 }
@@ -505,7 +505,7 @@ CallPlan& State::call_plan(int64_t F) {
   for (size_t b = 0; b < n.size(); ++b) cp->T.push_back(n[b] - N[b]);
   for (const ConvOp& op : pg.ops) {
     cp->pend.push_back(op.S > 1 && !op.convt ? N[op.in_buf] % op.S : 0);
-    cp->t_out.push_back(op.convt ? cp->T[op.in_buf] : cp->T[op.out_buf]);
+    cp->t_out.push_back(op.convt ? cp->T[op.in_buf] : cp->T[op.out_buf] / op.phases);
   }
   for (size_t b = 0; b < pg.bufs.size(); ++b)
     if (cache[b] > static_cast<int64_t>(buf_sstride[b] / plan->fw(b)) - cp->T[b])

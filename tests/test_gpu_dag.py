@@ -106,7 +106,9 @@ def test_random_dags_phase_state(seed):
             p = Plan(g)
             from paper_2204_07064_b200.runtime import StreamState
             StreamState(p, 2, 1)
-        except Exception:  # noqa: BLE001  (UnsupportedFormat: rate-changing Sum branch)
+            # the oracle restatement has the same restriction (Sum operands in lockstep)
+            po.run(g, np.zeros((1, g.in_channels, 2 * r), np.float32), [1] * (2 * r), "phase")
+        except Exception:  # noqa: BLE001  (UnsupportedFormat / LengthMismatch: rate-changing Sum branch)
             continue
         break
     else:
