@@ -1095,20 +1095,24 @@ bool densify_disabled() {
 void densify(Program& p) {
   for (ConvOp& op : p.ops) {
     const BufferSpec& bi = p.bufs[op.in_buf];
-    if (op.kind != OPK_CONV || op.convt || op.S != 1 || op.tap_step != 1 || op.row_step != 1 || op.pqmf ||
-        op.res_buf >= 0 || op.in_off != 0 || op.cin != bi.C || op.taps > 16 || op.nout > 1024)
+    // stride S0 (1, or a strided conv already read as S0-frame super-rows): the densified op
+    // reads 2 S0-frame super-rows and emits the two output frames 2i, 2i + 1 of each row
+    const int S0 = op.S;
+    if (op.kind != OPK_CONV || op.convt || op.tap_step != 1 || op.row_step != S0 || op.pqmf ||
+        op.res_buf >= 0 || op.in_off != 0 || op.cin != bi.C || op.taps > 16 * S0 || op.nout > 1024 ||
+        op.phases != 1 || op.d != 1)
       continue;
-    const bool narrow = op.nout <= 64 || (op.cin % 32 != 0 && (2 * op.cin) % 32 == 0);
-    // every non-phase call delivers an even frame count to this op
-    const bool even = (p.ratio * op.in_rate.num / op.in_rate.den) % 2 == 0 &&
-                      (p.ratio * op.in_rate.num) % op.in_rate.den == 0;
+    const bool narrow = op.nout <= 64 || (S0 * op.cin % 32 != 0 && (2 * S0 * op.cin) % 32 == 0);
+    // every non-phase call delivers a multiple of 2 S0 frames to this op
+    const bool even = (p.ratio * op.in_rate.num) % op.in_rate.den == 0 &&
+                      (p.ratio * op.in_rate.num / op.in_rate.den) % (2 * S0) == 0;
     if (!narrow || !even) continue;
-    const int64_t extra = op.look % 2;  // window start on a super-row boundary
-    const int T0 = op.taps, N = op.nout, T1 = T0 + 1 + static_cast<int>(extra);
+    const int64_t extra = (2 * S0 - op.look % (2 * S0)) % (2 * S0);  // window on a super-row boundary
+    const int T0 = op.taps, N = op.nout, T1 = T0 + S0 + static_cast<int>(extra);
     std::vector<float> w(static_cast<size_t>(T1) * op.cin * 2 * N, 0.f);
     for (int q = 0; q < T1; ++q)
       for (int ph = 0; ph < 2; ++ph) {
-        const int k = q - ph - static_cast<int>(extra);
+        const int k = q - ph * S0 - static_cast<int>(extra);
         if (k < 0 || k >= T0) continue;
         for (int c = 0; c < op.cin; ++c)
           for (int n = 0; n < N; ++n)
@@ -1121,13 +1125,13 @@ void densify(Program& p) {
     op.bias.swap(b);
     op.look += extra;
     op.taps = T1;
-    op.S = 2;
-    op.row_step = 2;
+    op.S = 2 * S0;
+    op.row_step = 2 * S0;
     op.phases = 2;
     op.nout = 2 * N;
     op.out_rstride *= 2;
     p.bufs[op.in_buf].cache = std::max(p.bufs[op.in_buf].cache, op.look);
-    p.bufs[op.in_buf].align = Lowerer::lcm(p.bufs[op.in_buf].align, 2);
+    p.bufs[op.in_buf].align = Lowerer::lcm(p.bufs[op.in_buf].align, 2 * S0);
     op.name += " x2";
   }
 }
