@@ -291,8 +291,9 @@ def main():
     step_ms_prof = sum(t for _, t in prof)
     roof = None
     if dom_name.startswith("op"):
-        oi = int(dom_name.split()[0][2:])
-        flops = 2.0 * op_macs[oi] * frames * streams
+        # "op6+7 ...": a conv with a chained 1x1 conv in the same launch (both GEMMs' FLOPs)
+        ois = [int(k) for k in dom_name.split()[0][2:].split("+")]
+        flops = 2.0 * sum(op_macs[oi] for oi in ois) * frames * streams
         achieved = flops / (dom_ms / 1e3) / 1e12
         # the fp32-accurate path issues 3 tf32 MMAs per product at half the bf16 rate:
         # its tensor-core ceiling is peak_bf16 / 6 (algorithmic FLOPs)

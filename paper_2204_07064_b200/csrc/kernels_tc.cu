@@ -371,7 +371,7 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
 
 // IOB (bf16 plans): bit 0 = the input buffer holds bf16, bit 1 = the output (and residual)
 // buffer holds bf16 — compile-time, so each instance carries only its own load / store paths
-template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB>
+template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB, bool CH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
@@ -400,6 +400,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = bars + 4 * STAGES + 28;  // [NB] main chunk drained
   uint64_t* wres_full = bars + 4 * STAGES + 36;   // resident weights landed (WIN && p.wres)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 37);
+  uint64_t* a2full = bars + 4 * STAGES + 38;   // [2] chained GEMM's A slot written (CH)
+  uint64_t* a2empty = bars + 4 * STAGES + 40;  // [2] chained GEMM's A slot read by its MMAs (CH)
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
@@ -413,6 +415,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = p.n_kblocks;
+  // chained 1x1 conv (CH): nk first-conv K-slabs, then NK2 slabs of the second conv whose A
+  // operand the drain writes from the first conv's finished tile
+  constexpr int NK2 = CH ? BN / BK : 0;
+  const int nkt = nk + NK2;
   const int n_tiles_n = (p.nout + BN - 1) / BN;
   const int n_tiles = p.m_tiles * n_tiles_n;
   // TMEM columns: NB chunk accumulators (BN each) | A ring of TS slots — fp32: A hi (32 cols)
@@ -420,16 +426,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // slot (32 bf16 per row, two per column).  As many chunk accumulators as fit (<= 8), so the
   // MMAs run ahead across a tile-boundary epilogue.
   constexpr int TS = BF ? STAGES : WIN ? 2 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
-  static_assert(4 * STAGES + 38 <= 128, "barrier area");
+  static_assert(4 * STAGES + 42 <= 128, "barrier area");
+  static_assert(!CH || (BN == 128 && CK == 1 && !BF && !WIN), "chained conv: fp32 BN = 128 chunk drains");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
   constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : 64 * TS;
-  constexpr int NB = (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
+  // CH: two chunk accumulators + the A ring + two 64-column A slots of the chained GEMM
+  constexpr int NB = CH ? 2 : (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
   static_assert(NB >= 2, "two chunk accumulators");
-  constexpr uint32_t COLS_USED = NB * BN + OTHER;
+  constexpr uint32_t COLS_USED = NB * BN + OTHER + (CH ? 128 : 0);
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
   constexpr uint32_t A_COL = NB * BN;
+  constexpr uint32_t A2_COL = NB * BN + OTHER;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -442,6 +451,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tempty[b], 8);
     }
     mbar_init(wres_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&a2full[a], 4);  // the four lane-quarter warps of one drain half
+      mbar_init(&a2empty[a], 1);
+    }
     mbar_init(res_full, 1);
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
@@ -471,6 +484,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     g_tc_trace[9 * 256 + blockIdx.x] = smid;
   }
   for (int i = threadIdx.x; i < p.nout; i += NUM_THREADS) sbias[i] = p.bias[i];
+  if (CH)  // first conv's bias at [0, BN) (p.bias), the chained conv's at [BN, 2 BN)
+    for (int i = threadIdx.x; i < BN; i += NUM_THREADS) sbias[BN + i] = p.bias2[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -692,9 +707,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
         int cb = 0, q = 0;  // this slab's 32-channel block and tap (advanced below, no divisions)
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        for (int kb = 0; kb < nkt; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          if (CH && kb >= nk) {  // chained conv's weight slab only (its A comes from the drain)
+            mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
+            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+            continue;
+          }
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
           // K-slab order: a layer that may also run in window mode (cbmaj) takes the window
           // mode's order (32-channel block major, tap minor), so its outputs do not depend on
@@ -726,14 +747,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t fmt = BF ? 1u : 2u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(BM >> 4) << 24);
-      int g = 0, c = 0, tcount = 0;
+      int g = 0, c = 0, tcount = 0, ga = 0;  // ga: A-ring slab counter (first-conv slabs)
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        for (int kb = 0; kb < nkt; ++kb, ++g) {
           const int s = g % STAGES;
           const int b = c % NB;
           const bool chunk_first = (kb % CK) == 0;
-          const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
+          const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
           if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+          if (CH && kb >= nk) {
+            // chained GEMM slab: W from the ring, A (h hi / lo of 32 channels) from the slot
+            // the drain wrote; its own chunk accumulator like every first-conv slab
+            const int u = tcount * NK2 + (kb - nk), sl = u & 1;
+            mbar_wait(&xform[s], (g / STAGES) & 1);
+            mbar_wait(&a2full[sl], (u >> 1) & 1);
+            tc_fence_after();
+            const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+            const uint32_t ahi = tbase + A2_COL + 64 * sl, alo = ahi + 32;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, kk > 0 ? 1u : 0u);
+              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
+            mma_commit_w(&a2empty[sl]);
+            mma_commit_w(&empty[s]);
+            mma_commit_w(&tfull[b]);
+            ++c;
+            continue;
+          }
           mbar_wait(&xform[s], (g / STAGES) & 1);
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
           tc_fence_after();
@@ -741,13 +785,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (BF) {
             // A (bf16 pairs) from this stage's TMEM columns, W from shared memory
             const uint32_t bb = smem_u32(b_bf(s));
-            const uint32_t at = tbase + A_COL + 16 * (g % TS);
+            const uint32_t at = tbase + A_COL + 16 * (ga % TS);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 8 TMEM columns / 32 bytes of the 64B row
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
               mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, acc0);
             }
-            mma_commit_w(&aempty[g % TS]);
+            mma_commit_w(&aempty[ga % TS]);
           } else {
             // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
             // shared-memory operand traffic is the weight tile (A never re-read from smem).
@@ -755,7 +799,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // chunk's accumulator: the truncating accumulation meets the large terms only in
             // its last four steps.
             const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-            const uint32_t ahi = tbase + A_COL + 64 * (g % TS);
+            const uint32_t ahi = tbase + A_COL + 64 * (ga % TS);
             const uint32_t alo = ahi + 32;
             if (!(TC_DBG(p) & 2)) {
 #pragma unroll
@@ -770,8 +814,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t acc0 = (!chunk_first || kk > 0 || !(TC_DBG(p) & 2)) ? 1u : 0u;
               mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
             }
-            mma_commit_w(&aempty[g % TS]);
+            mma_commit_w(&aempty[ga % TS]);
           }
+          ++ga;
           mma_commit_w(&empty[s]);
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
           if (chunk_last) {
@@ -816,11 +861,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= XF_WARP0 && warp < EP_WARP0) {
     // ===================== transform (w2..w5) =====================
     const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
-    int g = 0;
+    int g = 0, ga = 0;  // ga: A-ring slab counter (the chained conv's slabs skip the transform)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++g) {
+      for (int kb = 0; kb < nkt; ++kb, ++g) {
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
+        if (CH && kb >= nk) {  // chained conv's weight slab: nothing to transform, but every
+          __syncwarp();        // stage passes through here once per use (barrier phases)
+          if (lane == 0) mbar_arrive(&xform[s]);
+          continue;
+        }
         if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[1 * 256 + g] = clk();
         if (BF) {
           // thread = tile row r (= TMEM lane): fp32 SW128 row (16B chunk j at j ^ (r & 7)) ->
@@ -875,8 +925,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             pk[2 * j4 + 1] = *reinterpret_cast<uint32_t*>(&hi2);
           }
           }
-          const int a = g % TS;
-          if (g >= TS) mbar_wait(&aempty[a], ((g / TS) + 1) & 1);  // MMAs of g - TS done
+          const int a = ga % TS;
+          if (ga >= TS) mbar_wait(&aempty[a], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
           tc_fence_after();
           tmem_st16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 16 * a, pk);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -902,8 +952,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               lo[4 * j + u] = a - hi[4 * j + u];
             }
           }
-          const int a = g % TS;
-          if (g >= TS) mbar_wait(&aempty[a], ((g / TS) + 1) & 1);  // MMAs of g - TS done
+          const int a = ga % TS;
+          if (ga >= TS) mbar_wait(&aempty[a], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
           tc_fence_after();
           const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 64 * a;
           tmem_st32(ta, hi);
@@ -911,6 +961,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
+        ++ga;
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&xform[s]);
@@ -931,10 +982,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int c = 0, tcount = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
+      for (int kb = 0; kb < nkt; ++kb) {
+        const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
         if (!chunk_last) continue;
-        const bool first = (kb / CK) == 0;
+        const bool first = (kb / CK) == 0 || kb == nk;  // kb == nk: the chained conv's first chunk
+        const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
         const int b = c % NB;
         mbar_wait(&tfull[b], (c / NB) & 1);
         if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
@@ -948,13 +1000,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int u = 0; u < (COLS >= 32 ? 32 : 16); ++u)
             // the bias enters with the first chunk (keeps it off the tile-boundary epilogue)
-            acc[cc + u] = first ? __uint_as_float(v[u]) + sbias[tc.n0 + col0 + cc + u] : acc[cc + u] + __uint_as_float(v[u]);
+            acc[cc + u] = first ? __uint_as_float(v[u]) + sbias[boff + tc.n0 + col0 + cc + u] : acc[cc + u] + __uint_as_float(v[u]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
         if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
         ++c;
+        if (CH && kb == nk - 1) {
+          // the first conv's tile is complete: h = act2(act1(acc)) split hi / lo exactly like
+          // the transform would split it after a round trip through HBM (bit-identical to the
+          // two-launch form), into the chained GEMM's A slots — this half's 64 columns are its
+          // K-slabs 2 half and 2 half + 1
+          const float s1 = slope_of(p.mid_act1, p.mid_alpha1), s2 = slope_of(p.mid_act2, p.mid_alpha2);
+#pragma unroll
+          for (int j = 0; j < COLS / 32; ++j) {
+            const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u & 1;
+            if (u >= 2) mbar_wait(&a2empty[sl], ((u >> 1) + 1) & 1);  // MMAs of use u - 2 done
+            tc_fence_after();
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A2_COL + 64 * sl;
+#pragma unroll
+            for (int h16 = 0; h16 < 2; ++h16) {
+              uint32_t hv[16], lv[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const float a = act_lin(act_lin(acc[32 * j + 16 * h16 + e], s1), s2);
+                const float hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+                hv[e] = __float_as_uint(hi);
+                lv[e] = __float_as_uint(a - hi);
+              }
+              tmem_st16(ta + 16 * h16, hv);
+              tmem_st16(ta + 32 + 16 * h16, lv);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a2full[sl]);
+          }
+        }
       }
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
       const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
@@ -1060,14 +1143,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0>
+template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0, bool CH = false>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
   using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          L::BYTES);
     attr = true;
   }
@@ -1078,7 +1161,7 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   }
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
-  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 
 template <int IOB>
@@ -1122,6 +1205,10 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
       launch_bn<32, 14, 1, false, true>(map_a, map_w, map_out, map_res, p, st);
     else
       launch_bn<64, 7, 1, false, true>(map_a, map_w, map_out, map_res, p, st);
+    return;
+  }
+  if (p.chain) {  // k3 conv + chained 1x1 conv in one launch (fp32, BN = 128)
+    launch_bn<128, 3, 1, false, false, 0, true>(map_a, map_w, map_out, map_res, p, st);
     return;
   }
   switch (p.BN) {

@@ -47,6 +47,14 @@ struct TcParams {
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: 3xTF32
   int a_bf, r_bf, o_bf;  // bf16 plans: input / residual / output buffer holds bf16 (else fp32)
   int cbmaj;  // 1: K-slabs channel-block major (layers that may run in window mode), else tap major
+  // chained 1x1 conv (fp32, BN = 128, one N tile): the drain turns the first conv's tile
+  // h = act2(act1(acc + bias)) into the A operand of a second GEMM (chain K-slabs of 32
+  // channels, weights at K offset n_kblocks x 32 of the same weight map) whose tile goes
+  // through the epilogue above (bias2, post act, residual, output of the second conv).
+  int chain;            // 0: single conv; else K-slabs of the second conv (cin2 / 32)
+  const float* bias2;   // second conv's bias (nout)
+  int mid_act1, mid_act2;
+  float mid_alpha1, mid_alpha2;
   int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)
 };
 

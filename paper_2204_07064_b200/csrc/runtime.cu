@@ -154,6 +154,51 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
 }
 }  // namespace
 
+bool chain_disabled() {
+  const char* e = std::getenv("SC_CHAIN");
+  return e && e[0] == '0';
+}
+
+// Chained 1x1 convs (fp32 tensor-core path): a BN = 128 conv whose output buffer is read only
+// by the next op, a K = 1 conv over the same 128 channels, runs both GEMMs in one launch — the
+// intermediate tile never leaves the SM (kernels_tc.cu CH; cfg2's residual blocks: LReLU ->
+// conv K3 -> LReLU -> conv 1x1 + skip).  The 1x1 weights are appended along K of the first
+// conv's packed weights ([2][128][Kpad + 128]), so one weight map serves both GEMMs.
+void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::vector<float>>& wtc) {
+  for (size_t i = 0; i + 1 < pg.ops.size(); ++i) {
+    const size_t j = i + 1;
+    const ConvOp& a = pg.ops[i];
+    const ConvOp& b = pg.ops[j];
+    DevOp& da = dops[i];
+    const DevOp& db = dops[j];
+    if (da.kernel != KERNEL_TC || db.kernel != KERNEL_TC || da.bf16 || db.bf16 || da.chain >= 0) continue;
+    if (da.BN != 128 || db.BN != 128 || da.view_S != 1 || db.view_S != 1 || db.taps_view != 1) continue;
+    if (a.kind != OPK_CONV || b.kind != OPK_CONV || a.convt || b.convt || a.phases != 1 || b.phases != 1) continue;
+    if (a.nout != 128 || a.out_rstride != 128 || pg.bufs[a.out_buf].C != 128 || a.gate || a.res_buf >= 0) continue;
+    if (a.post_act == ACT_TANH || b.pre_act == ACT_TANH) continue;
+    if (b.in_buf != a.out_buf || b.in_off != 0 || b.cin != 128 || b.look != 0 || b.nout != 128 || b.gate) continue;
+    if (b.out_buf == a.out_buf || b.res_buf == a.out_buf || a.out_buf == pg.sink_buf) continue;
+    bool other = false;  // the intermediate buffer has no other reader
+    for (size_t k = 0; k < pg.ops.size() && !other; ++k) {
+      if (k == j) continue;
+      const ConvOp& o = pg.ops[k];
+      other = o.in_buf == a.out_buf || o.res_buf == a.out_buf;
+      for (const SumIn& si : o.sum_in) other = other || si.buf == a.out_buf;
+    }
+    if (other) continue;
+    const size_t N = 128, K1 = static_cast<size_t>(da.taps_view) * da.cin_view_pad, K2 = 128;
+    std::vector<float> w(2 * N * (K1 + K2));
+    for (size_t h = 0; h < 2; ++h)
+      for (size_t n = 0; n < N; ++n) {
+        std::copy_n(wtc[i].begin() + (h * N + n) * K1, K1, w.begin() + (h * N + n) * (K1 + K2));
+        std::copy_n(wtc[j].begin() + (h * N + n) * K2, K2, w.begin() + (h * N + n) * (K1 + K2) + K1);
+      }
+    wtc[i] = std::move(w);
+    da.chain = static_cast<int>(j);
+    da.k_chain = static_cast<int>(K2);
+  }
+}
+
 Plan::~Plan() {
   if (wmem && device >= 0) {
     int prev = 0;
@@ -199,6 +244,7 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
   plan->dops.assign(nops, DevOp{});
   std::vector<std::vector<float>> wtc(nops);
   for (size_t i = 0; i < nops; ++i) plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i]);
+  if (precision == SC_PREC_FP32 && !chain_disabled()) find_chains(plan->prog, plan->dops, wtc);
   // PQMF fast form: the factor arrays (S, C, class index as float) follow the op's blob slots
   std::vector<std::vector<float>> pqv(nops);
   for (size_t i = 0; i < nops; ++i) {
@@ -263,7 +309,7 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
     if (d.kernel == KERNEL_TC) {
       const ConvOp& op = plan->prog.ops[i];
       d.wtc = plan->wmem + toff[i];
-      const uint64_t Kpad = static_cast<uint64_t>(d.taps_view) * d.cin_view_pad;
+      const uint64_t Kpad = static_cast<uint64_t>(d.taps_view) * d.cin_view_pad + d.k_chain;
       if (d.bf16)
         d.map_w = make_map3(d.wtc, Kpad, op.nout, 1, Kpad * 2, static_cast<uint64_t>(op.nout) * Kpad * 2, 32,
                             d.BN, 1, true);
@@ -634,6 +680,42 @@ CallPlan& State::call_plan(int64_t F) {
       cp->tc[i].map_res = cp->tc[i].map_out;  // unused
     }
   }
+  // chained 1x1 convs (find_chains): one launch computes both when this call gives them the
+  // same tile geometry; the second conv's epilogue (bias, act, residual, output) moves over
+  cp->chained.assign(pg.ops.size(), -1);
+  for (size_t i = 0; i < pg.ops.size(); ++i) {
+    const int j = plan->dops[i].chain;
+    if (j < 0 || cp->t_out[i] == 0 || cp->t_out[j] != cp->t_out[i]) continue;
+    TcParams& a = cp->tc[i].p;
+    const TcParams& b = cp->tc[j].p;
+    if (a.win || b.win || a.R != b.R || a.G != b.G || a.m_tiles != b.m_tiles) continue;
+    a.chain = 128 / 32;
+    a.bias2 = b.bias;
+    a.mid_act1 = a.post_act;
+    a.mid_alpha1 = a.post_alpha;
+    a.mid_act2 = b.pre_act;
+    a.mid_alpha2 = b.pre_alpha;
+    a.post_act = b.post_act;
+    a.post_alpha = b.post_alpha;
+    a.gate = b.gate;
+    a.nout = b.nout;
+    a.out = b.out;
+    a.out_sstride = b.out_sstride;
+    a.out_base = b.out_base;
+    a.out_rstride = b.out_rstride;
+    a.res = b.res;
+    a.res_sstride = b.res_sstride;
+    a.res_fstride = b.res_fstride;
+    a.res_off = b.res_off;
+    a.res_f0 = b.res_f0;
+    a.res_act = b.res_act;
+    a.res_alpha = b.res_alpha;
+    cp->tc[i].map_out = cp->tc[j].map_out;
+    cp->tc[i].map_res = cp->tc[j].map_res;
+    cp->t_out[j] = 0;  // not launched: op i's launch writes its output
+    cp->chained[i] = j;
+    cp->n_launch -= 1;
+  }
   return *plans.emplace(key, std::move(cp)).first->second;
 }
 
@@ -783,6 +865,10 @@ std::string State::launch_name(int64_t F, int i) {
     if (i == k++) {
       const ConvOp& op = plan->prog.ops[j];
       const DevOp& d = plan->dops[j];
+      const int jc = cp.chained.empty() ? -1 : cp.chained[j];
+      if (jc >= 0)
+        return "op" + std::to_string(j) + "+" + std::to_string(jc) + " " + op.name + " + " +
+               plan->prog.ops[jc].name + " [tc]";
       return "op" + std::to_string(j) + " " + op.name + " [" +
              (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
               : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";

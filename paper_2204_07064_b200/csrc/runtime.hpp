@@ -29,6 +29,8 @@ struct DevOp {
   bool bf16 = false;
   int view_S = 1;            // super-row factor of the input view (conv stride, or 1)
   int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
+  int chain = -1;            // fp32: index of the K = 1 conv chained into this op's launch
+  int k_chain = 0;           // its K (weights appended along K of this op's weight map)
   // PQMF fast form (kernel == KERNEL_PQMF_*): factor arrays inside the weight blob
   float* pq_S = nullptr;
   float* pq_C = nullptr;
@@ -81,6 +83,7 @@ struct CallPlan {
   int n_desc = 0;
   int64_t carry_items = 0;
   int n_launch = 0;           // kernels one call of this plan launches
+  std::vector<int> chained;   // per op: the op chained into its launch this call (-1: none)
   std::vector<TcLaunch> tc;
   std::map<std::pair<const float*, float*>, GraphEntry> graphs;
 };

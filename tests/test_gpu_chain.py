@@ -1,0 +1,59 @@
+"""Chained 1x1 convs (fp32 tensor-core path): a 128-channel conv whose output only feeds a
+K = 1 conv runs both GEMMs in one launch (kernels_tc.cu CH, runtime.cu find_chains).  The
+chained launch splits the intermediate tile exactly as the second conv's transform would after
+the HBM round trip, so it must be bit-identical to the two-launch form (SC_CHAIN=0), and both
+within the north-star tolerance of the oracle."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2204_07064_b200 import configs
+from paper_2204_07064_b200.runtime import Plan
+
+from test_gpu_parity import FP32_TOL, rel_err, run_gpu
+
+
+def _plans(model, monkeypatch):
+    monkeypatch.setenv("SC_CHAIN", "0")
+    p0 = Plan(model, device=0)
+    monkeypatch.delenv("SC_CHAIN")
+    p1 = Plan(model, device=0)
+    return p0, p1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [[2048, 2048], [640, 64, 1344], [96, 32, 128, 256], [1] * 12 + [300]])
+def test_cfg2_chain_bit_identical(parts, monkeypatch):
+    m = configs.build(2, seed=1)
+    p0, p1 = _plans(m, monkeypatch)
+    x = configs.batch_input(2, range(5), 128, sum(parts), seed=2)
+    y0, _, _ = run_gpu(m, x, parts, plan=p0)
+    y1, _, st = run_gpu(m, x, parts, plan=p1)
+    assert np.array_equal(y0, y1), float(np.abs(y0 - y1).max())
+    names = st.launch_names(parts[0])
+    assert sum("+" in n.split()[0] for n in names) == 4, names  # four chained residual blocks
+    assert not any(n.startswith("op1 ") for n in names), names
+    if sum(parts) <= 2048:
+        err, rms = rel_err(y1, po.run(m, x, parts, "stream"))
+        assert err <= FP32_TOL, f"{err:.3e} x RMS ({rms:.3e})"
+
+
+@pytest.mark.gpu
+def test_chain_full_streams_bit_identical(monkeypatch):
+    """At the bench's stream count (256 x 2048 frames): chained == two launches, bit for bit."""
+    import torch
+    from paper_2204_07064_b200.runtime import StreamState
+    m = configs.build(2, seed=0)
+    p0, p1 = _plans(m, monkeypatch)
+    S, T = 256, 2048
+    x = torch.randn((S, 128, T), device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    outs = []
+    for p in (p0, p1):
+        st = StreamState(p, S, T)
+        y = torch.empty_like(x)
+        st.process_buffer(x, y, T)
+        st.process_buffer(x, y, T)  # second call: the cached rows of the first
+        torch.cuda.synchronize()
+        outs.append(y)
+        assert p is p0 or st.launches(T) == StreamState(p0, 1, T).launches(T) - 4
+    assert torch.equal(outs[0], outs[1])
