@@ -752,8 +752,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nkt; ++kb, ++g) {
           const int s = g % STAGES;
           const int b = c % NB;
-          const bool chunk_first = (kb % CK) == 0;
-          const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
+          const bool one2 = CH && p.chain_one && kb >= nk;  // chained GEMM in one accumulator
+          const bool chunk_first = one2 ? kb == nk : (kb % CK) == 0;
+          const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
           if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
           if (CH && kb >= nk) {
             // chained GEMM slab: W from the ring, A (h hi / lo of 32 channels) from the slot
@@ -767,15 +768,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t ahi = tbase + A2_COL + 64 * sl, alo = ahi + 32;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, kk > 0 ? 1u : 0u);
+              mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
               mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
             }
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
             mma_commit_w(&a2empty[sl]);
             mma_commit_w(&empty[s]);
-            mma_commit_w(&tfull[b]);
-            ++c;
+            if (chunk_last) {
+              mma_commit_w(&tfull[b]);
+              ++c;
+            }
             continue;
           }
           mbar_wait(&xform[s], (g / STAGES) & 1);
@@ -983,9 +986,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
       for (int kb = 0; kb < nkt; ++kb) {
-        const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
+        const bool one2 = CH && p.chain_one && kb >= nk;
+        const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
         if (!chunk_last) continue;
-        const bool first = (kb / CK) == 0 || kb == nk;  // kb == nk: the chained conv's first chunk
+        const bool first = (kb / CK) == 0 || kb == (one2 ? nkt - 1 : nk);  // + the chained conv's first chunk
         const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
         const int b = c % NB;
         mbar_wait(&tfull[b], (c / NB) & 1);

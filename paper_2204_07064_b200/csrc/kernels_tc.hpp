@@ -53,6 +53,8 @@ struct TcParams {
   // through the epilogue above (bias2, post act, residual, output of the second conv).
   int chain;            // 0: single conv; else K-slabs of the second conv (cin2 / 32)
   const float* bias2;   // second conv's bias (nout)
+  int chain_one;
+  int ck;               // fp32 BN = 128: K-slabs per TMEM chunk accumulator (1, 2, 4)        // 1: the chained GEMM accumulates its K-slabs in one TMEM chunk
   int mid_act1, mid_act2;
   float mid_alpha1, mid_alpha2;
   int debug;  // experiments only (SC_TC_DEBUG): 2 no correction MMAs (timing only), 4 no residual L2 prefetch, 32 trace (SC_TC_TRACE_OP)

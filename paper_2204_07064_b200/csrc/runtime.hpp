@@ -31,6 +31,7 @@ struct DevOp {
   int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
   int chain = -1;            // fp32: index of the K = 1 conv chained into this op's launch
   int k_chain = 0;           // its K (weights appended along K of this op's weight map)
+  int chain_one = 1;         // the chained GEMM accumulates in one TMEM chunk (SC_CHAIN_ONE)
   // PQMF fast form (kernel == KERNEL_PQMF_*): factor arrays inside the weight blob
   float* pq_S = nullptr;
   float* pq_C = nullptr;

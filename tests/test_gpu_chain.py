@@ -1,8 +1,9 @@
 """Chained 1x1 convs (fp32 tensor-core path): a 128-channel conv whose output only feeds a
 K = 1 conv runs both GEMMs in one launch (kernels_tc.cu CH, runtime.cu find_chains).  The
 chained launch splits the intermediate tile exactly as the second conv's transform would after
-the HBM round trip, so it must be bit-identical to the two-launch form (SC_CHAIN=0), and both
-within the north-star tolerance of the oracle."""
+the HBM round trip; with per-slab chunk accumulators (SC_CHAIN_ONE=0) it is bit-identical to
+the two-launch form (SC_CHAIN=0).  The default accumulates the chained GEMM in one TMEM chunk:
+within CHAIN_TOL of the two-launch form and within the north-star tolerance of the oracle."""
 import numpy as np
 import pytest
 
@@ -13,12 +14,31 @@ from paper_2204_07064_b200.runtime import Plan
 from test_gpu_parity import FP32_TOL, rel_err, run_gpu
 
 
-def _plans(model, monkeypatch):
+CHAIN_TOL = 3e-5  # max |one-chunk chained - two launches| / RMS (measured 1.4e-5 vs the oracle)
+
+
+def _plans(model, monkeypatch, one="0"):
     monkeypatch.setenv("SC_CHAIN", "0")
     p0 = Plan(model, device=0)
     monkeypatch.delenv("SC_CHAIN")
+    monkeypatch.setenv("SC_CHAIN_ONE", one)
     p1 = Plan(model, device=0)
+    monkeypatch.delenv("SC_CHAIN_ONE")
     return p0, p1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [[2048], [96, 32, 128, 256]])
+def test_cfg2_chain_one_accumulator(parts, monkeypatch):
+    """The default chained form (one accumulator for the 1x1 GEMM) vs two launches and oracle."""
+    m = configs.build(2, seed=3)
+    p0, p1 = _plans(m, monkeypatch, one="1")
+    x = configs.batch_input(2, range(4), 128, sum(parts), seed=4)
+    y0, _, _ = run_gpu(m, x, parts, plan=p0)
+    y1, _, _ = run_gpu(m, x, parts, plan=p1)
+    assert rel_err(y1, y0)[0] <= CHAIN_TOL
+    err, rms = rel_err(y1, po.run(m, x, parts, "stream"))
+    assert err <= FP32_TOL, f"{err:.3e} x RMS ({rms:.3e})"
 
 
 @pytest.mark.gpu
