@@ -400,8 +400,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = bars + 4 * STAGES + 28;  // [NB] main chunk drained
   uint64_t* wres_full = bars + 4 * STAGES + 36;   // resident weights landed (WIN && p.wres)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 37);
-  uint64_t* a2full = bars + 4 * STAGES + 38;   // [2] chained GEMM's A slot written (CH)
-  uint64_t* a2empty = bars + 4 * STAGES + 40;  // [2] chained GEMM's A slot read by its MMAs (CH)
+  uint64_t* a2full = bars + 4 * STAGES + 38;   // [<= 4] chained GEMM's A slot written (CH)
+  uint64_t* a2empty = bars + 4 * STAGES + 42;  // [<= 4] chained GEMM's A slot read by its MMAs (CH)
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
@@ -426,14 +426,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // slot (32 bf16 per row, two per column).  As many chunk accumulators as fit (<= 8), so the
   // MMAs run ahead across a tile-boundary epilogue.
   constexpr int TS = BF ? STAGES : WIN ? 2 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
-  static_assert(4 * STAGES + 42 <= 128, "barrier area");
-  static_assert(!CH || (BN == 128 && CK == 1 && !BF && !WIN), "chained conv: fp32 BN = 128 chunk drains");
+  static_assert(4 * STAGES + 46 <= 128, "barrier area");
+  static_assert(!CH || (BN == 128 && CK == (BF ? 4 : 1) && (BF || !WIN)), "chained conv: BN = 128 (windows: bf16)");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
   constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : 64 * TS;
-  // CH: two chunk accumulators + the A ring + two 64-column A slots of the chained GEMM
-  constexpr int NB = CH ? 2 : (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
+  // CH: two chunk accumulators + the A ring + the chained GEMM's A slots — fp32: two slots of
+  // 64 columns (32 channels hi | lo); bf16: four of 16 (32 channels as bf16 pairs, one per slab)
+  constexpr int NS2 = BF ? 4 : 2;
+  constexpr int W2 = BF ? 16 : 64;
+  constexpr int NB = CH ? (WIN ? 3 : 2) : (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
   static_assert(NB >= 2, "two chunk accumulators");
-  constexpr uint32_t COLS_USED = NB * BN + OTHER + (CH ? 128 : 0);
+  constexpr uint32_t COLS_USED = NB * BN + OTHER + (CH ? NS2 * W2 : 0);
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tempty[b], 8);
     }
     mbar_init(wres_full, 1);
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NS2; ++a) {
       mbar_init(&a2full[a], 4);  // the four lane-quarter warps of one drain half
       mbar_init(&a2empty[a], 1);
     }
@@ -525,6 +528,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (!BF) tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
         }
       }
+      for (int k2 = 0; k2 < NK2; ++k2, ++g) {  // chained conv's weight slabs (bf16)
+        const int s = g % STAGES;
+        if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+        mbar_expect_tx_w(&full[s], L::B_TILE);
+        tma_load_3d_w(&tmap_w, &full[s], b_hi(s), (nk + k2) * BK, tc.n0, 0);
+      }
     }
   } else if (WIN && warp == 1) {
     // ===================== MMA issuer, window mode (SS-MMAs at a per-tap row offset) ========
@@ -586,6 +595,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit_w(&wa_empty[sa]);
+      }
+      if (CH) {  // chained 1x1 GEMM (bf16): A from the drain's TMEM slots, one chunk accumulator
+        const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                  (static_cast<uint32_t>(BM >> 4) << 24);
+        for (int k2 = 0; k2 < NK2; ++k2, ++g) {
+          const int s = g % STAGES;
+          const int b = c % NB;
+          const int u2 = tcount * NK2 + k2, sl = u2 % NS2;
+          if (k2 == 0 && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          mbar_wait(&a2full[sl], (u2 / NS2) & 1);
+          tc_fence_after();
+          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+          const uint32_t bb = smem_u32(b_hi(s)), at = tbase + A2_COL + W2 * sl;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc_bf, (k2 > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_w(&a2empty[sl]);
+          mma_commit_w(&empty[s]);
+          if (k2 == NK2 - 1) {
+            mma_commit_w(&tfull[b]);
+            ++c;
+          }
+        }
       }
     }
   } else if (WIN && warp >= XF_WARP0 && warp < EP_WARP0) {
@@ -711,9 +744,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
           if (CH && kb >= nk) {  // chained conv's weight slab only (its A comes from the drain)
-            mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
-            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
-            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+            if (BF) {
+              mbar_expect_tx_w(&full[s], L::B_TILE);
+              tma_load_3d_w(&tmap_w, &full[s], b_bf(s), kb * BK, tc.n0, 0);
+            } else {
+              mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
+              tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kb * BK, tc.n0, 0);
+              tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kb * BK, tc.n0, 1);
+            }
             continue;
           }
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[4 * 256 + g] = clk();
@@ -759,20 +797,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (CH && kb >= nk) {
             // chained GEMM slab: W from the ring, A (h hi / lo of 32 channels) from the slot
             // the drain wrote; its own chunk accumulator like every first-conv slab
-            const int u = tcount * NK2 + (kb - nk), sl = u & 1;
+            const int u = tcount * NK2 + (kb - nk), sl = u % NS2;
             mbar_wait(&xform[s], (g / STAGES) & 1);
-            mbar_wait(&a2full[sl], (u >> 1) & 1);
+            mbar_wait(&a2full[sl], (u / NS2) & 1);
             tc_fence_after();
             const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-            const uint32_t ahi = tbase + A2_COL + 64 * sl, alo = ahi + 32;
+            if (BF) {
+              const uint32_t bb = smem_u32(b_bf(s)), at = tbase + A2_COL + W2 * sl;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
-              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+              for (int kk = 0; kk < BK / 16; ++kk)
+                mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
+            } else {
+              const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+              const uint32_t ahi = tbase + A2_COL + W2 * sl, alo = ahi + 32;
+#pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
+                mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+              }
+#pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
             }
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
             mma_commit_w(&a2empty[sl]);
             mma_commit_w(&empty[s]);
             if (chunk_last) {
@@ -1019,12 +1064,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const float s1 = slope_of(p.mid_act1, p.mid_alpha1), s2 = slope_of(p.mid_act2, p.mid_alpha2);
 #pragma unroll
           for (int j = 0; j < COLS / 32; ++j) {
-            const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u & 1;
-            if (u >= 2) mbar_wait(&a2empty[sl], ((u >> 1) + 1) & 1);  // MMAs of use u - 2 done
+            const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u % NS2;
+            if (u >= NS2) mbar_wait(&a2empty[sl], ((u / NS2) + 1) & 1);  // MMAs of use u - NS2 done
             tc_fence_after();
-            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A2_COL + 64 * sl;
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A2_COL + W2 * sl;
+            if (BF) {
+              // the two-launch form rounds h to bf16 once in the first conv's epilogue when the
+              // intermediate buffer holds bf16 (p.mid_bf), then applies act2 and rounds again
+              uint32_t pk[16];
 #pragma unroll
-            for (int h16 = 0; h16 < 2; ++h16) {
+              for (int e = 0; e < 16; ++e) {
+                float v0 = act_lin(acc[32 * j + 2 * e], s1), v1 = act_lin(acc[32 * j + 2 * e + 1], s1);
+                if (p.mid_bf) {
+                  v0 = __bfloat162float(__float2bfloat16_rn(v0));
+                  v1 = __bfloat162float(__float2bfloat16_rn(v1));
+                }
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(act_lin(v0, s2), act_lin(v1, s2));
+                pk[e] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              tmem_st16(ta, pk);
+            }
+#pragma unroll
+            for (int h16 = 0; h16 < (BF ? 0 : 2); ++h16) {
               uint32_t hv[16], lv[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
@@ -1175,14 +1236,24 @@ void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUten
     switch (p.BN) {
       case 32: launch_bn<32, 12, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
       case 64: launch_bn<64, 10, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
-      default: launch_bn<128, 8, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+      default:
+        if (p.chain)
+          launch_bn<128, 8, 4, true, true, IOB, true>(map_a, map_w, map_out, map_res, p, st);
+        else
+          launch_bn<128, 8, 4, true, true, IOB>(map_a, map_w, map_out, map_res, p, st);
+        break;
     }
     return;
   }
   switch (p.BN) {
     case 32: launch_bn<32, 10, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
     case 64: launch_bn<64, 8, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
-    default: launch_bn<128, 6, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st); break;
+    default:
+      if (p.chain)  // k3 conv + chained 1x1 conv in one launch
+        launch_bn<128, 6, 4, true, false, IOB, true>(map_a, map_w, map_out, map_res, p, st);
+      else
+        launch_bn<128, 6, 4, true, false, IOB>(map_a, map_w, map_out, map_res, p, st);
+      break;
   }
 }
 

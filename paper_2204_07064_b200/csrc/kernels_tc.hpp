@@ -54,6 +54,7 @@ struct TcParams {
   int chain;            // 0: single conv; else K-slabs of the second conv (cin2 / 32)
   const float* bias2;   // second conv's bias (nout)
   int chain_one;
+  int mid_bf;           // bf16 plans: the two-launch form stores the intermediate as bf16
   int ck;               // fp32 BN = 128: K-slabs per TMEM chunk accumulator (1, 2, 4)        // 1: the chained GEMM accumulates its K-slabs in one TMEM chunk
   int mid_act1, mid_act2;
   float mid_alpha1, mid_alpha2;

@@ -179,7 +179,7 @@ void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::v
     const ConvOp& b = pg.ops[j];
     DevOp& da = dops[i];
     const DevOp& db = dops[j];
-    if (da.kernel != KERNEL_TC || db.kernel != KERNEL_TC || da.bf16 || db.bf16 || da.chain >= 0) continue;
+    if (da.kernel != KERNEL_TC || db.kernel != KERNEL_TC || da.bf16 != db.bf16 || da.chain >= 0) continue;
     if (da.BN != 128 || db.BN != 128 || da.view_S != 1 || db.view_S != 1 || db.taps_view != 1) continue;
     if (a.kind != OPK_CONV || b.kind != OPK_CONV || a.convt || b.convt || a.phases != 1 || b.phases != 1) continue;
     if (a.nout != 128 || a.out_rstride != 128 || pg.bufs[a.out_buf].C != 128 || a.gate || a.res_buf >= 0) continue;
@@ -195,12 +195,24 @@ void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::v
     }
     if (other) continue;
     const size_t N = 128, K1 = static_cast<size_t>(da.taps_view) * da.cin_view_pad, K2 = 128;
-    std::vector<float> w(2 * N * (K1 + K2));
-    for (size_t h = 0; h < 2; ++h)
+    std::vector<float> w;
+    if (da.bf16) {  // [N][K] bf16 (packed two per float slot)
+      w.assign((N * (K1 + K2) + 1) / 2, 0.f);
+      const uint16_t* w1 = reinterpret_cast<const uint16_t*>(wtc[i].data());
+      const uint16_t* w2 = reinterpret_cast<const uint16_t*>(wtc[j].data());
+      uint16_t* o = reinterpret_cast<uint16_t*>(w.data());
       for (size_t n = 0; n < N; ++n) {
-        std::copy_n(wtc[i].begin() + (h * N + n) * K1, K1, w.begin() + (h * N + n) * (K1 + K2));
-        std::copy_n(wtc[j].begin() + (h * N + n) * K2, K2, w.begin() + (h * N + n) * (K1 + K2) + K1);
+        std::copy_n(w1 + n * K1, K1, o + n * (K1 + K2));
+        std::copy_n(w2 + n * K2, K2, o + n * (K1 + K2) + K1);
       }
+    } else {  // [2 (hi, lo)][N][K] fp32
+      w.assign(2 * N * (K1 + K2), 0.f);
+      for (size_t h = 0; h < 2; ++h)
+        for (size_t n = 0; n < N; ++n) {
+          std::copy_n(wtc[i].begin() + (h * N + n) * K1, K1, w.begin() + (h * N + n) * (K1 + K2));
+          std::copy_n(wtc[j].begin() + (h * N + n) * K2, K2, w.begin() + (h * N + n) * (K1 + K2) + K1);
+        }
+    }
     wtc[i] = std::move(w);
     da.chain = static_cast<int>(j);
     da.k_chain = static_cast<int>(K2);
@@ -253,7 +265,7 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
   plan->dops.assign(nops, DevOp{});
   std::vector<std::vector<float>> wtc(nops);
   for (size_t i = 0; i < nops; ++i) plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i]);
-  if (precision == SC_PREC_FP32 && !chain_disabled()) find_chains(plan->prog, plan->dops, wtc);
+  if (!chain_disabled()) find_chains(plan->prog, plan->dops, wtc);
   // PQMF fast form: the factor arrays (S, C, class index as float) follow the op's blob slots
   std::vector<std::vector<float>> pqv(nops);
   for (size_t i = 0; i < nops; ++i) {
@@ -637,7 +649,7 @@ CallPlan& State::call_plan(int64_t F) {
     // order in every mode (bit-identity across partitions); a static property of the layer
     p.cbmaj = ((d.bf16 || d.BN <= 64) && d.taps_view > 1) ? 1 : 0;
     p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
-             !win_disabled()) ? 1 : 0;
+             !win_disabled() && !(plan->dops[i].chain >= 0 && !d.bf16)) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
     p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
               op.nout == d.BN) ? 1 : 0;
@@ -697,9 +709,12 @@ CallPlan& State::call_plan(int64_t F) {
     if (j < 0 || cp->t_out[i] == 0 || cp->t_out[j] != cp->t_out[i]) continue;
     TcParams& a = cp->tc[i].p;
     const TcParams& b = cp->tc[j].p;
-    if (a.win || b.win || a.R != b.R || a.G != b.G || a.m_tiles != b.m_tiles) continue;
+    if ((a.win && !a.bf16) || b.win || a.R != b.R || a.G != b.G || a.m_tiles != b.m_tiles) continue;
     a.chain = 128 / 32;
-    a.chain_one = plan->dops[i].chain_one;
+    a.chain_one = plan->dops[i].chain_one || a.bf16;  // bf16: K = 128 is one CK = 4 chunk anyway
+    a.mid_bf = plan->buf_bf16[pg.ops[i].out_buf];
+    a.o_bf = b.o_bf;
+    a.r_bf = b.r_bf;
     a.bias2 = b.bias;
     a.mid_act1 = a.post_act;
     a.mid_alpha1 = a.post_alpha;

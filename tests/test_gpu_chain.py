@@ -17,14 +17,28 @@ from test_gpu_parity import FP32_TOL, rel_err, run_gpu
 CHAIN_TOL = 3e-5  # max |one-chunk chained - two launches| / RMS (measured 1.4e-5 vs the oracle)
 
 
-def _plans(model, monkeypatch, one="0"):
+def _plans(model, monkeypatch, one="0", precision="fp32"):
     monkeypatch.setenv("SC_CHAIN", "0")
-    p0 = Plan(model, device=0)
+    p0 = Plan(model, device=0, precision=precision)
     monkeypatch.delenv("SC_CHAIN")
     monkeypatch.setenv("SC_CHAIN_ONE", one)
-    p1 = Plan(model, device=0)
+    p1 = Plan(model, device=0, precision=precision)
     monkeypatch.delenv("SC_CHAIN_ONE")
     return p0, p1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [[2048, 2048], [96, 32, 128, 256], [1] * 6 + [300]])
+def test_cfg2_chain_bf16_bit_identical(parts, monkeypatch):
+    """bf16 plans: the chained launch rounds the intermediate like the bf16-stored two-launch
+    form and accumulates the 1x1 GEMM in the same single K = 128 chunk — bit-identical."""
+    m = configs.build(2, seed=5)
+    p0, p1 = _plans(m, monkeypatch, precision="bf16")
+    x = configs.batch_input(2, range(6), 128, sum(parts), seed=6)
+    y0, _, _ = run_gpu(m, x, parts, plan=p0, precision="bf16")
+    y1, _, st = run_gpu(m, x, parts, plan=p1, precision="bf16")
+    assert np.array_equal(y0, y1), float(np.abs(y0 - y1).max())
+    assert sum("+" in n.split()[0] for n in st.launch_names(parts[0])) == 4
 
 
 @pytest.mark.gpu
