@@ -893,7 +893,7 @@ std::string State::launch_name(int64_t F, int i) {
       const int jc = cp.chained.empty() ? -1 : cp.chained[j];
       if (jc >= 0)
         return "op" + std::to_string(j) + "+" + std::to_string(jc) + " " + op.name + " + " +
-               plan->prog.ops[jc].name + " [tc]";
+               plan->prog.ops[jc].name + (plan->dops[j].bf16 ? " [tc-bf16]" : " [tc]");
       return "op" + std::to_string(j) + " " + op.name + " [" +
              (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
               : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";
