@@ -434,9 +434,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // 64 columns (32 channels hi | lo); bf16: four of 16 (32 channels as bf16 pairs, one per slab)
   constexpr int NS2 = BF ? 4 : 2;
   constexpr int W2 = BF ? 16 : 64;
-  constexpr int NB = CH ? (WIN ? 3 : 2) : (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
+  // fp32 (SHR): the chained GEMM's A slabs take their turn in the first conv's TMEM A ring
+  // (ring positions nk .. nk + 3 of each tile), which leaves room for three chunk accumulators
+  constexpr bool SHR = CH && !BF;
+  constexpr int NB = CH ? (SHR || WIN ? 3 : 2) : (512 - OTHER) / BN > 8 ? 8 : (512 - OTHER) / BN;
   static_assert(NB >= 2, "two chunk accumulators");
-  constexpr uint32_t COLS_USED = NB * BN + OTHER + (CH ? NS2 * W2 : 0);
+  constexpr uint32_t COLS_USED = NB * BN + OTHER + (CH && !SHR ? NS2 * W2 : 0);
   constexpr uint32_t TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                  : COLS_USED <= 256 ? 256 : 512;
   static_assert(COLS_USED <= 512, "TMEM budget");
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
             } else {
               const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-              const uint32_t ahi = tbase + A2_COL + W2 * sl, alo = ahi + 32;
+              const uint32_t ahi = tbase + (SHR ? A_COL + 64 * (ga % TS) : A2_COL + W2 * sl), alo = ahi + 32;
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) {
                 mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
@@ -818,7 +821,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
             }
-            mma_commit_w(&a2empty[sl]);
+            if (SHR) {
+              mma_commit_w(&aempty[ga % TS]);
+              ++ga;
+            } else {
+              mma_commit_w(&a2empty[sl]);
+            }
             mma_commit_w(&empty[s]);
             if (chunk_last) {
               mma_commit_w(&tfull[b]);
@@ -1010,6 +1018,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_before();
         }
         ++ga;
+        if (SHR && kb == nk - 1) ga += NK2;  // the chained slabs' ring positions (drain-written)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&xform[s]);
@@ -1065,9 +1074,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < COLS / 32; ++j) {
             const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u % NS2;
-            if (u >= NS2) mbar_wait(&a2empty[sl], ((u / NS2) + 1) & 1);  // MMAs of use u - NS2 done
+            const int pa = tcount * (nk + NK2) + nk + half * (COLS / 32) + j;  // A-ring position (SHR)
+            if (SHR) mbar_wait(&aempty[pa % TS], ((pa / TS) + 1) & 1);  // MMAs of position pa - TS done
+            else if (u >= NS2) mbar_wait(&a2empty[sl], ((u / NS2) + 1) & 1);  // MMAs of use u - NS2 done
             tc_fence_after();
-            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A2_COL + W2 * sl;
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                (SHR ? A_COL + 64 * (pa % TS) : A2_COL + W2 * sl);
             if (BF) {
               // the two-launch form rounds h to bf16 once in the first conv's epilogue when the
               // intermediate buffer holds bf16 (p.mid_bf), then applies act2 and rounds again
