@@ -91,3 +91,36 @@ def test_chain_full_streams_bit_identical(monkeypatch):
         outs.append(y)
         assert p is p0 or st.launches(T) == StreamState(p0, 1, T).launches(T) - 4
     assert torch.equal(outs[0], outs[1])
+
+
+def _dag(second_reader: bool, seed: int = 7):
+    """source(128) -> LReLU -> conv K3 128->128 -> LReLU -> conv 1x1 128->128 -> + source ->
+    sink; with `second_reader` the K3 conv's output also feeds the Sum (no chain allowed)."""
+    from paper_2204_07064_b200.graph import Graph
+    g = Graph(128, seed=seed)
+    a = g.conv(g.leaky_relu(g.source, 0.2), 128, 128, 3, padding=(1, 1))
+    h = g.leaky_relu(a, 0.2)
+    b = g.conv(h, 128, 128, 1, padding=(0, 0))
+    g.sink(g.sum(b, g.source, a) if second_reader else g.sum(b, g.source))
+    return g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("second_reader", [False, True])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_dag_chain_selection(second_reader, precision):
+    """find_chains on graph_ir DAGs: chained only when the 1x1 conv is the sole reader of the
+    K3 conv's output; parity with the oracle either way."""
+    from test_gpu_parity import BF16_NRMSE
+    g = _dag(second_reader)
+    parts = [256, 64, 704]
+    x = np.random.default_rng(1).standard_normal((3, 128, sum(parts))).astype(np.float32)
+    y, plan, st = run_gpu(g, x, parts, precision=precision)
+    chained = any("+" in n.split()[0] for n in st.launch_names(parts[0]))
+    assert chained == (not second_reader), st.launch_names(parts[0])
+    y_or = po.run(g, x, parts, "stream")
+    if precision == "fp32":
+        assert rel_err(y, y_or)[0] <= FP32_TOL
+    else:
+        d = (y - y_or).astype(np.float64)
+        assert np.sqrt(np.mean(d ** 2)) / np.sqrt(np.mean(y_or.astype(np.float64) ** 2)) <= BF16_NRMSE
