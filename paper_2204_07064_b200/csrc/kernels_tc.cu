@@ -521,9 +521,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
         mbar_expect_tx_w(&wa_full[sa], a_bytes);
         tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
-        // warm L2 with the next tile's window of this channel block: two window slots cannot
-        // cover the DRAM latency of the next load on their own
-        if (tile + static_cast<int>(gridDim.x) < n_tiles && lane == 0) {
+        // warm L2 with the next tile's window of this channel block: two fp32 window slots
+        // cannot cover the DRAM latency of the next load on their own (bf16 tiles hold three
+        // slots; there the prefetch cost 15-25% on cfg3's strided / ConvT layers)
+        if (!BF && tile + static_cast<int>(gridDim.x) < n_tiles && lane == 0) {
           const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n, BN);
           tma_prefetch_3d(&tmap_a, p.a_c0 + cb * BK, p.a_row0 + tn.i0, tn.s0);
         }
