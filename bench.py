@@ -3,8 +3,9 @@
 
 Metric (BASELINE.json): streamed audio samples/s over concurrent independent streams and its
 roofline fraction.  One step = one process_buffer call for every stream of
-the rank's shard.  Default workload: BASELINE config 2 (configs[1]: 4 dilated residual
-blocks, C=128, 256 streams x 2048 frames, fp32).  `--config N` selects another config.
+the rank's shard.  Default workload: BASELINE config 5 (configs[4], the largest single-GPU
+config and the north star's target: the RAVE-style encoder + decoder, 16384 streams x 2048
+samples, fp32).  `--config N` selects another config (4: the RAVE-style decoder).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
@@ -20,6 +21,8 @@ both sides; the max over ranks is the step time.
            measured peak in MEASURED_PEAKS.json.
 `cpu_baseline`: the reference's own conv1d (oracle/_ref, kernels.cpp) driven by the SPEC
            process_buffer restatement (oracle/oracle.cpp), all host threads, bounded sample.
+--impl reference: that CPU path as the reference arm (rank 0 only; never loads the product
+           library — PQMF filters from oracle/pqmf_design.py, frame counts from the oracle).
 """
 from __future__ import annotations
 
@@ -47,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
     ap.add_argument("--streams", type=int, default=0, help="streams per rank (default: config)")
     ap.add_argument("--total-streams", type=int, default=0,
@@ -65,32 +68,72 @@ def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
-                    bf16_sus=d.get("bf16_tflops_sustained", 1400.0), src="measured")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+        pk = dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                  bf16_sus=d.get("bf16_tflops_sustained", 1400.0), src="measured")
+    else:
+        pk = dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+    # P_TF32: measured on the box by tools/tf32_peak.cu (kind::tf32 tcgen05 MMAs, all SMs),
+    # committed as profiles/tf32_peak.json; the fp32-accurate path issues 3 tf32 MMAs per
+    # product (3xTF32), so its tensor ceiling is P_TF32 / 3 in algorithmic FLOPs.
+    t = ROOT / "profiles" / "tf32_peak.json"
+    pk["tf32"] = pk["tf32_sus"] = None
+    if t.exists():
+        d = json.loads(t.read_text())
+        pk["tf32"] = d.get("tf32_tflops")
+        pk["tf32_sus"] = d.get("tf32_tflops_sustained", pk["tf32"])
+    return pk
+
+
+def fp32_path_ceiling(pk, sustained=False):
+    """(TFLOP/s, source) of the 3xTF32 path's tensor ceiling in algorithmic FLOPs."""
+    tf = pk["tf32_sus"] if sustained else pk["tf32"]
+    if tf:
+        return tf / 3.0, "measured tf32 (profiles/tf32_peak.json) / 3"
+    bf = pk["bf16_sus"] if sustained else pk["bf16"]
+    return bf / 6.0, "assumed: bf16 / 6 (tf32 unmeasured)"
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clock + throttle reasons sampled every ~10 ms (NVML) from before the warm-up to the
+    end of the e2e leg; falls back to nvidia-smi (one sample per ~0.2 s) without pynvml."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.01):
         self.index = index
-        self.rows = []
+        self.period = period
+        self.rows = []       # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = None
+        self.src = "nvml"
 
     def _run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), int(bits)))
+                self._stop.wait(self.period)
+            return
+        except Exception:
+            self.src = "nvidia-smi"
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
+                r = [v.strip() for v in out.split(",")]
+                bits = sum(self.REASONS[n] for n, v in zip(names, r[2:6]) if v.lower() == "active")
+                self.rows.append((float(r[0]), float(r[1]), bits))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -107,17 +150,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for n, v in zip(names, r[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted(n for n, b in self.REASONS.items() if any(r[2] & b for r in self.rows))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(self.rows),
+                "span": "warm-up + timed region + e2e leg", "source": self.src}
 
 
 def dist_setup():
@@ -134,63 +171,138 @@ def make_inputs(cfg, first_stream, streams, cin, frames, slot):
                      for s in range(streams)])
 
 
-def cpu_reference_rate(model, cfg, frames, seconds, threads):
-    """Streamed samples/s of the reference CPU path on a bounded sample (all `threads`)."""
+def config_dict(cfg, name, streams, frames, out_call, cout, precision, ws, in_bytes, out_bytes):
+    """The `config` object — identical keys and values in both arms (ours / reference)."""
+    l2_bytes = 126 * 1024 * 1024
+    return {"workload": f"cfg{cfg}:{name}", "streams_per_gpu": streams,
+            "frames_per_call": frames, "out_samples_per_call": out_call, "out_channels": cout,
+            "precision": precision, "parallelism": f"stream-sharded x{ws}",
+            "l2": ("inputs larger than L2" if in_bytes + out_bytes >= l2_bytes
+                   else "L2 flushed between steps")}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_rates(cfg, frames, steps, step_seconds, threads, mode_a_seconds=8.0):
+    """The reference's own CPU path for this workload: its conv1d (oracle/_ref = the
+    unmodified proj/src/kernels.cpp; the oracle's restatement when the reference could not be
+    built) driven by the SPEC process_buffer restatement (oracle/oracle.cpp), on the host.
+
+    mode (B), the timed arm: set_parallel_kernels(false) (kernels.cpp:33) with one stream per
+      thread (SPEC.md:302,304 allow independent states to run concurrently), all `threads`;
+    mode (A), reported beside it: the reference default — OpenMP inside conv1d
+      (kernels.cpp:88), streams one after another.
+    Each step is a bounded sample of stream-calls (fresh zero-initialised state)
+    sized to ~step_seconds; the rate is samples actually produced / wall time actually spent.
+    Never loads the product library: the model's PQMF filters come from the oracle's
+    independent design (oracle/pqmf_design.py), frame counts from the oracle's graph_info."""
+    from oracle import pqmf_design
     from oracle import pyoracle as po
-    from paper_2204_07064_b200.runtime import Plan
-    plan_h = Plan(model, device=-1)
-    macs_call = plan_h.macs_per_sample * frames  # algorithmic; ConvT adds zero-stuffed MACs
-    out_call = plan_h.out_frames(frames)
+    from paper_2204_07064_b200 import configs
+    model = configs.build(cfg, seed=0, pqmf_design=pqmf_design.filters)
+    info = po.graph_info(model)
+    out_call = frames * info["sink_num"] // info["sink_den"]
     use_ref = po.ref_available()
-    # ~0.45 GMAC/s per core for the reference's scalar double-accumulate conv (BASELINE.md §2)
-    calls = max(threads, int(round(seconds * threads * 0.7e9 / max(macs_call, 1.0))))
-    calls = max(threads, (calls // threads) * threads)
-    x = make_inputs(cfg, 0, calls, model.in_channels, frames, slot=0)
+    if use_ref:
+        po.ref().ref_set_parallel_kernels(0)
+    # calibration (= warm-up): one stream-call per thread
+    x = make_inputs(cfg, 0, threads, model.in_channels, frames, slot=0)
     t0 = time.perf_counter()
     po.run(model, x, [frames], "stream", use_ref=use_ref, threads=threads)
-    dt = time.perf_counter() - t0
-    rate = calls * out_call / dt
-    return dict(value=rate, unit="samples/s", cores=threads,
-                kind="reference" if use_ref else "port",
-                sample=f"{calls} stream-calls x {frames} frames (fresh state), {dt:.1f} s wall, "
-                       f"reference conv1d (kernels.cpp) via SPEC process_buffer restatement, "
-                       f"OpenMP across streams")
+    t_cal = time.perf_counter() - t0
+    per_step = threads * max(1, int(round(step_seconds / max(t_cal, 1e-6))))
+    xs = make_inputs(cfg, 0, per_step, model.in_channels, frames, slot=1)
+    secs = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        po.run(model, xs, [frames], "stream", use_ref=use_ref, threads=threads)
+        secs.append(time.perf_counter() - t0)
+    rates = [per_step * out_call / s for s in secs]
+    b = dict(value=per_step * out_call * steps / sum(secs), unit="samples/s", cores=threads,
+             kind="reference" if use_ref else "port",
+             cpu_model=cpu_model(), nproc=os.cpu_count(),
+             mode="B: set_parallel_kernels(false), OpenMP across streams",
+             rate_mean=statistics.mean(rates),
+             rate_std=statistics.pstdev(rates) if len(rates) > 1 else 0.0,
+             trials=steps, step_s_mean=statistics.mean(secs),
+             sample=f"{steps} trials x {per_step} stream-calls x {frames} frames -> {out_call} "
+                    f"samples each (fresh state), {sum(secs):.1f} s wall timed; "
+                    f"{'reference conv1d (kernels.cpp, oracle/_ref)' if use_ref else 'oracle port of conv1d'}"
+                    f" via the SPEC process_buffer restatement")
+    # mode (A): the reference default, OpenMP inside conv1d, one stream after another
+    a = None
+    if use_ref and mode_a_seconds > 0:
+        po.ref().ref_set_parallel_kernels(1)
+        n_a = max(1, int(round(mode_a_seconds / max(t_cal, 1e-6))))  # ~t_cal per call at full width
+        xa = xs[:min(n_a, per_step)]
+        t0 = time.perf_counter()
+        po.run(model, xa, [frames], "stream", use_ref=True, threads=1)
+        dt = time.perf_counter() - t0
+        po.ref().ref_set_parallel_kernels(0)
+        a = dict(value=xa.shape[0] * out_call / dt, unit="samples/s", cores=threads,
+                 mode="A: reference default, OpenMP inside conv1d (kernels.cpp:88), streams sequential",
+                 sample=f"{xa.shape[0]} stream-calls x {frames} frames, {dt:.1f} s wall")
+    b["mode_a"] = a
+    return b, out_call, info["out_channels"], secs
+
+
+METRIC = "streamed audio samples/s (x real-time @48kHz) over concurrent streams"
+
+
+def main_reference(args, ws, rank):
+    """--impl reference: the reference's CPU path on the host cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    from paper_2204_07064_b200 import configs
+    cfgd = configs.CONFIGS[args.config]
+    frames = args.frames or cfgd["frames"]
+    streams = args.streams or cfgd["streams"]
+    if args.total_streams:
+        streams = -(-args.total_streams // ws)
+    threads = len(os.sched_getaffinity(0))
+    # whole run (warm-up/calibration + K trials + mode A sample) within ~2 minutes
+    step_s = min(4.0, max(1.0, 90.0 / max(1, args.steps)))
+    cpu, out_call, cout, secs = reference_rates(args.config, frames, max(1, args.steps), step_s,
+                                                threads, mode_a_seconds=8.0)
+    v = cpu["value"]
+    in_bytes = streams * configs.CONFIGS[args.config]["in_channels"] * frames * 4
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.mean(secs) * 1e3,
+            "ms_per_step_note": "wall time of one timed trial (a bounded sample of stream-calls, "
+                                "see cpu_baseline.sample), not of a full-config step",
+            "higher_is_better": True, "scaling": "strong" if args.total_streams else "weak",
+            "vs_baseline": None, "dtype": "f32 (f64 accumulate, kernels.cpp:96-100)",
+            "data": "synthetic (seeded: N(0,1) frames; cfg5 pink noise + partials)",
+            "x_realtime": v / SR,
+            "config": config_dict(args.config, cfgd["name"], streams, frames, out_call, cout,
+                                  "fp32", ws, in_bytes, streams * cout * out_call * 4),
+            "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def main():
     args = parse()
     ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        return main_reference(args, ws, rank)
+
     from paper_2204_07064_b200 import configs
     cfgd = configs.CONFIGS[args.config]
     frames = args.frames or cfgd["frames"]
     streams = args.streams or cfgd["streams"]
-    metric = "streamed audio samples/s (x real-time @48kHz) over concurrent streams"
     model = configs.build(args.config, seed=0)
-
-    if args.impl == "reference":
-        if rank != 0:
-            return 0
-        threads = len(os.sched_getaffinity(0))
-        vals = []
-        last = None
-        for _ in range(max(1, args.steps)):
-            last = cpu_reference_rate(model, args.config, frames, max(2.0, 120.0 / max(1, args.steps)),
-                                      threads)
-            vals.append(last["value"])
-        v = float(statistics.mean(vals))
-        out_call = cfgd["out"]
-        line = {"impl": "reference", "metric": metric, "value": v, "unit": "samples/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": streams * out_call / v * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
-                "data": "synthetic (seeded)", "x_realtime": v / SR,
-                "config": {"workload": f"cfg{args.config}:{cfgd['name']}", "streams": streams,
-                           "frames_per_call": frames, "out_samples_per_call": out_call},
-                "cpu_baseline": dict(last, value=v),
-                "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
 
     import torch
     import torch.distributed as dist
@@ -222,16 +334,18 @@ def main():
     stream = torch.cuda.current_stream(dev)
     in_bytes = xs[0].numel() * 4
     out_bytes = ys[0].numel() * 4
-    l2_bytes = 126 * 1024 * 1024
+    cfg_line = config_dict(args.config, cfgd["name"], streams, frames, out_call, cout,
+                           args.precision, ws, in_bytes, out_bytes)
     flush = None
-    step_bytes = in_bytes + out_bytes
-    if step_bytes < l2_bytes:
-        flush = torch.empty(2 * l2_bytes // 4, device=dev)
+    if cfg_line["l2"] != "inputs larger than L2":
+        flush = torch.empty(2 * 126 * 1024 * 1024 // 4, device=dev)
 
     def barrier():
         if ws > 1:
             dist.barrier()
 
+    clk = ClockSampler(local)
+    clk.__enter__()
     for k in range(args.warmup):
         st.process_buffer(xs[k % 2], ys[k % 2], frames, stream)
     torch.cuda.synchronize()
@@ -242,17 +356,17 @@ def main():
     barrier()
     torch.cuda.synchronize()
     launched0 = st.launch_total()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            if flush is not None:
-                flush.zero_()
-            evs[k][0].record(stream)
-            st.process_buffer(xs[k % 2], ys[k % 2], frames, stream)
-            evs[k][1].record(stream)
-        torch.cuda.synchronize()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        evs[k][0].record(stream)
+        st.process_buffer(xs[k % 2], ys[k % 2], frames, stream)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
     barrier()
     gpu_launches = st.launch_total() - launched0  # exact: counted by the library per call
-    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), dev)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = max_over_ranks(sum(step_ms), dev)
     total_streams = args.total_streams or streams * ws
     value = total_streams * out_call * args.steps / (ms / 1e3)
 
@@ -278,6 +392,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    clk.__exit__()
     ems = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e_value = total_streams * out_call * args.steps / (ems / 1e3)
 
@@ -295,16 +410,18 @@ def main():
         ois = [int(k) for k in dom_name.split()[0][2:].split("+")]
         flops = 2.0 * sum(op_macs[oi] for oi in ois) * frames * streams
         achieved = flops / (dom_ms / 1e3) / 1e12
-        # the fp32-accurate path issues 3 tf32 MMAs per product at half the bf16 rate:
-        # its tensor-core ceiling is peak_bf16 / 6 (algorithmic FLOPs)
-        ceil = pk["bf16"] / 6.0 if (args.precision == "fp32" and "[tc]" in dom_name) else pk["bf16"]
+        if args.precision == "fp32" and "[tc]" in dom_name:
+            ceil, csrc = fp32_path_ceiling(pk)
+        else:
+            ceil, csrc = pk["bf16"], "bf16 dense (burst; MEASURED_PEAKS.json)"
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16"], "traffic": None, "kernel": dom_name,
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms_prof,
                 "peak_source": f"{pk['src']} bf16 dense (burst; MEASURED_PEAKS.json)",
                 "path_ceiling": ceil, "frac_of_path_ceiling": achieved / ceil,
-                "path_ceiling_note": "3xTF32 = 3 tf32 MMAs (half bf16 rate) per fp32 product"
-                if ceil != pk["bf16"] else "bf16 kind::f16 MMA",
+                "path_ceiling_source": csrc,
+                "path_ceiling_note": "3xTF32 = 3 kind::tf32 MMAs per fp32 product"
+                if args.precision == "fp32" else "bf16 kind::f16 MMA",
                 "flops_per_launch": flops}
         tfile = ROOT / "profiles" / "traffic.json"
         if tfile.exists():
@@ -315,39 +432,42 @@ def main():
     total_flops = 2.0 * plan.macs_per_sample * frames * streams
     step_bytes_min = in_bytes + out_bytes + streams * (st.cache_bytes * 2)
     step_roof_ms = max(total_flops / (pk["bf16_sus"] * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
-    # the same bound with this precision's tensor ceiling: 3xTF32 issues 3 tf32 MMAs (half
-    # the bf16 rate) per fp32 product, so its ceiling is bf16_sustained / 6
-    path_tf = pk["bf16_sus"] / 6.0 if args.precision == "fp32" else pk["bf16_sus"]
+    # the same bound with this precision's tensor ceiling (3xTF32: P_TF32 / 3, sustained)
+    if args.precision == "fp32":
+        path_tf, path_src = fp32_path_ceiling(pk, sustained=True)
+    else:
+        path_tf, path_src = pk["bf16_sus"], "bf16 dense sustained (MEASURED_PEAKS.json)"
     step_path_ms = max(total_flops / (path_tf * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_rate(model, args.config, frames, args.cpu_seconds,
-                                     len(os.sched_getaffinity(0)))
+            threads = len(os.sched_getaffinity(0))
+            trials = 3
+            cpu = reference_rates(args.config, frames, trials, args.cpu_seconds / trials, threads,
+                                  mode_a_seconds=0)[0]
         except Exception as e:  # the oracle is a reported baseline, never the product
             cpu = {"value": None, "error": str(e)}
 
     if rank == 0:
         line = {
-            "metric": metric, "value": value, "unit": "samples/s", "n_gpus": ws,
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "ms_per_step_std": statistics.pstdev(step_ms) if len(step_ms) > 1 else 0.0,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "bf16 operands / f32 accumulate",
             "data": "synthetic (seeded: N(0,1) frames; cfg5 pink noise + partials)",
             "x_realtime": value / SR,
-            "config": {"workload": f"cfg{args.config}:{cfgd['name']}", "streams_per_gpu": streams,
-                       "frames_per_call": frames, "out_samples_per_call": out_call,
-                       "out_channels": cout, "precision": args.precision,
-                       "parallelism": f"stream-sharded x{ws}",
-                       "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps",
-                       "cuda_graphs": not args.no_graphs},
+            "config": cfg_line,
+            "cuda_graphs": not args.no_graphs,
             "roofline": roof,
             "step_roofline": {"ms": step_roof_ms, "frac": step_roof_ms / (ms / args.steps),
-                              "flops_per_step": total_flops,
-                              "path_ms": step_path_ms, "frac_of_path_ceiling": step_path_ms / (ms / args.steps),
-                              "note": "whole-step bound max(F/P_bf16_sustained, bytes/HBM); path_ms uses "
-                                      "the precision's tensor ceiling (3xTF32: P_bf16_sustained / 6)"},
+                              "flops_per_step": total_flops, "bytes_min_per_step": step_bytes_min,
+                              "path_ms": step_path_ms,
+                              "frac_of_path_ceiling": step_path_ms / (ms / args.steps),
+                              "path_ceiling_tflops": path_tf, "path_ceiling_source": path_src,
+                              "note": "whole-step bound max(F/P, bytes/HBM) (SURVEY §8d); `ms` uses "
+                                      "P = bf16 sustained, `path_ms` this precision's tensor ceiling"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": hx[0].numel() * hx[0].element_size(),
                     "d2h_bytes_per_step": hy[0].numel() * hy[0].element_size(), "host_io": args.io},

@@ -155,7 +155,8 @@ SC_API int sc_state_create(const sc_plan* plan, int32_t n_streams, int64_t max_f
 SC_API int sc_state_destroy(sc_state* state);
 /* Replaces: reset for the listed streams (NULL ids = all). Async. */
 SC_API int sc_state_reset(sc_state* state, const int32_t* stream_ids, int32_t n_ids, void* stream);
-/* Device bytes actually held by the state (caches + step working buffers). */
+/* Device bytes actually held by the state: caches + step working buffers + the cached call
+   plans (carry tables; at most 32 plans are kept, least recently used evicted first). */
 SC_API int sc_state_device_bytes(const sc_state* state, int64_t* bytes);
 /* Resident cache bytes per stream (<= sc_plan_state_bytes: skip delays share conv caches). */
 SC_API int sc_state_cache_bytes(const sc_state* state, int64_t* bytes_per_stream);

@@ -863,6 +863,34 @@ void oc_conv1d(const float* x, int M, int64_t L, const float* w, const float* b,
   conv1d_c(x, M, L, w, b, N, K, S, d, y);
 }
 
+// NOT a restatement: a deliberately fp32-ACCUMULATING conv with the same signature, used only
+// as evidence for the RES_SCALE decision (configs.py, tests/test_oracle.py): how large is the
+// error of ANY fp32-accumulating implementation against the reference's double accumulation
+// (kernels.cpp:96-100)?  "BLAS order": the (m, k) reduction of each output is split over 8
+// interleaved fp32 partial sums (one SIMD register's worth), combined pairwise at the end.
+// `sequential` != 0: one fp32 accumulator in the reference's m-then-k order instead.
+static int g_f32_sequential = 0;
+void oc_set_f32acc_order(int sequential) { g_f32_sequential = sequential; }
+void oc_conv1d_f32acc(const float* x, int M, int64_t L, const float* w, const float* b, int N,
+                      int K, int S, int d, float* y) {
+  const int64_t Lo = out_len(L, K, S, d);
+  for (int n = 0; n < N; ++n)
+    for (int64_t i = 0; i < Lo; ++i) {
+      float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int64_t j = 0;
+      for (int m = 0; m < M; ++m) {
+        const float* xrow = x + static_cast<size_t>(m) * L + i * S;
+        const float* wrow = w + (static_cast<size_t>(n) * M + m) * K;
+        for (int t = 0; t < K; ++t, ++j) {
+          const float p = wrow[t] * xrow[static_cast<int64_t>(t) * d];
+          if (g_f32_sequential) part[0] += p; else part[j & 7] += p;
+        }
+      }
+      const float s4[4] = {part[0] + part[4], part[1] + part[5], part[2] + part[6], part[3] + part[7]};
+      y[static_cast<size_t>(n) * Lo + i] = b[n] + ((s4[0] + s4[2]) + (s4[1] + s4[3]));
+    }
+}
+
 int oc_branch_alignment(const int64_t* D, int n, int64_t* A) {
   // SPEC.md:200-204
   if (n < 1) return SC_ERR_INVALID_ARGUMENT;

@@ -54,6 +54,9 @@ def oracle() -> C.CDLL:
         L.oc_dag_run.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int,
                                  C.c_int, F32P, C.c_int64, I64P, C.c_int, F32P, C.c_int, C.c_void_p,
                                  C.c_int]
+        L.oc_conv1d_f32acc.argtypes = L.oc_conv1d.argtypes
+        L.oc_conv1d_f32acc.restype = None
+        L.oc_set_f32acc_order.argtypes = [C.c_int]
         L.oc_run.argtypes = [C.c_void_p, C.c_int, F32P, C.c_int64, C.c_int, C.c_int, F32P,
                              C.c_int64, I64P, C.c_int, F32P, C.c_int, C.c_void_p, C.c_int]
         _o = L
@@ -182,10 +185,18 @@ def graph_info(model) -> dict:
 MODES = {"stream": 0, "offline": 1, "offline_original": 2, "phase": 3}
 
 
+def _conv_ptr(use_ref, conv):
+    if conv == "f32acc":        # evidence only: an fp32-accumulating conv (RES_SCALE test)
+        return C.cast(oracle().oc_conv1d_f32acc, C.c_void_p)
+    return C.cast(ref().ref_conv1d, C.c_void_p) if use_ref else None
+
+
 def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = False,
-        threads: int = 0) -> np.ndarray:
+        threads: int = 0, conv: str | None = None) -> np.ndarray:
     """x: [streams][in_C][T].  Returns [streams][out_C][T*sink].  `model`: a flat Model or a
-    SPEC DAG (graph.Graph, run by the oracle's independent DAG restatement)."""
+    SPEC DAG (graph.Graph, run by the oracle's independent DAG restatement).
+    conv=None: the restatement (or the reference's conv1d when use_ref); "f32acc": the
+    fp32-accumulating evidence conv (oc_conv1d_f32acc)."""
     if _is_dag(model):
         nodes, n, edges, ne, w = model.pack()
         x = np.ascontiguousarray(x, np.float32)
@@ -193,7 +204,7 @@ def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = 
         info = graph_info(model)
         y = np.zeros((S, info["out_channels"], T * info["sink_num"] // info["sink_den"]), np.float32)
         p = np.ascontiguousarray([T] if parts is None else parts, np.int64)
-        fn = C.cast(ref().ref_conv1d, C.c_void_p) if use_ref else None
+        fn = _conv_ptr(use_ref, conv)
         st = oracle().oc_dag_run(C.cast(nodes, C.c_void_p), n, C.cast(edges, C.c_void_p), ne, _fp(w),
                                  w.size, model.in_channels, S, _fp(x), T, p.ctypes.data_as(I64P),
                                  p.size, _fp(y), MODES[mode], fn, threads)
@@ -209,7 +220,7 @@ def run(model, x: np.ndarray, parts=None, mode: str = "stream", use_ref: bool = 
     if parts is None:
         parts = [T]
     p = np.ascontiguousarray(parts, np.int64)
-    fn = C.cast(ref().ref_conv1d, C.c_void_p) if use_ref else None
+    fn = _conv_ptr(use_ref, conv)
     st = oracle().oc_run(C.cast(nodes, C.c_void_p), n, _fp(w), w.size, model.in_channels, S,
                          _fp(x), T, p.ctypes.data_as(I64P), p.size, _fp(y), MODES[mode], fn,
                          threads)

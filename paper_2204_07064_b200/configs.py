@@ -14,12 +14,17 @@
         LReLU.2, strided conv K=2r+1 doubling] -> LReLU.2 -> conv K3 1024->256 (mean|var)
         -> slice mean 128 -> cfg4 decoder -> PQMF synthesis           16384 streams x
                                                                        {512, 2048, 8192}
-All weights Kaiming-uniform from the seed (LeakyReLU(0.2) gain) with zero bias; in the
-RAVE-style residual stacks of cfg4/cfg5 the residual-branch convs are additionally scaled by
-RES_SCALE = 0.5 [decision]: with plain Kaiming the 15 residual units compound to a pre-gate
-RMS of ~66, where the sigmoid gate turns fp32-level relative errors into output errors far
-above the 1e-4 x RMS tolerance for ANY fp32-accumulating implementation; at 0.5 every layer
+All weights Kaiming-uniform from the seed (LeakyReLU(0.2) gain) with zero bias — the literal
+BASELINE init for cfg1-cfg4.  cfg5 only [decision, evidenced]: its 27 residual-branch convs
+(12 encoder + 15 decoder units) are additionally scaled by RES_SCALE_CFG5 = 0.5.  With plain
+Kaiming the stacks compound to a pre-gate RMS of O(100), where the sigmoid gate turns
+fp32-level relative errors into output errors above the 1e-4 x RMS tolerance for ANY
+fp32-accumulating implementation: tests/test_oracle.py::test_res_scale_evidence runs the
+oracle with an fp32-accumulating conv (oc_conv1d_f32acc) and asserts exactly that (cfg5 at
+scale 1 fails the bound, at 0.5 passes; cfg4 at the literal init passes).  At 0.5 every layer
 stays at RMS O(0.1-1) and the tolerance measures the kernels, not the model's conditioning.
+`build(cfg, res_scale=...)` overrides the scale (the evidence test; cfg4 with 0.5 is the
+round-1 variant).
 Inputs are seeded synthetic (no dataset exists for this path; BASELINE.json names none).
 """
 from __future__ import annotations
@@ -31,7 +36,7 @@ import numpy as np
 from .graph import Model
 
 SR = 48000
-RES_SCALE = 0.5
+RES_SCALE_CFG5 = 0.5
 
 # frames = input frames per call per stream; out = output samples per call per stream
 CONFIGS = {
@@ -77,7 +82,7 @@ def cfg3(seed: int = 0, mirror: bool = True) -> Model:
     return m
 
 
-def _decoder(m: Model, latent: int = 128) -> Model:
+def _decoder(m: Model, latent: int = 128, res_scale: float = 1.0) -> Model:
     m.conv(latent, 1024, 7, padding=(3, 3))
     c = 1024
     for r in (4, 4, 4, 2):
@@ -87,7 +92,7 @@ def _decoder(m: Model, latent: int = 128) -> Model:
         for d in (1, 3, 5):
             with m.residual():
                 m.leaky_relu(0.2)
-                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=RES_SCALE)
+                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=res_scale)
     m.leaky_relu(0.2)
     m.conv(c, 32, 7, padding=(3, 3))  # 16 wave + 16 amplitude channels
     m.gate()
@@ -95,12 +100,12 @@ def _decoder(m: Model, latent: int = 128) -> Model:
     return m
 
 
-def cfg4(seed: int = 0) -> Model:
-    return _decoder(Model(128, seed))
+def cfg4(seed: int = 0, res_scale: float = 1.0, pqmf_design=None) -> Model:
+    return _decoder(Model(128, seed, pqmf_design=pqmf_design), res_scale=res_scale)
 
 
-def cfg5(seed: int = 0) -> Model:
-    m = Model(1, seed)
+def cfg5(seed: int = 0, res_scale: float = RES_SCALE_CFG5, pqmf_design=None) -> Model:
+    m = Model(1, seed, pqmf_design=pqmf_design)
     m.pqmf_analysis(16, 256)
     m.conv(16, 64, 7, padding=(3, 3))
     c = 64
@@ -108,20 +113,28 @@ def cfg5(seed: int = 0) -> Model:
         for d in (1, 3, 5):
             with m.residual():
                 m.leaky_relu(0.2)
-                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=RES_SCALE)
+                m.conv(c, c, 3, dilation=d, padding=(d, d), scale=res_scale)
         m.leaky_relu(0.2)
         m.conv(c, 2 * c, 2 * r + 1, stride=r, padding=(r, r))
         c *= 2
     m.leaky_relu(0.2)
     m.conv(1024, 256, 3, padding=(1, 1))  # mean | variance (variance computed, dropped)
     m.slice(0, 128)
-    return _decoder(m, 128)
+    return _decoder(m, 128, res_scale=res_scale)
 
 
 BUILDERS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
 
 
-def build(cfg: int, seed: int = 0) -> Model:
+def build(cfg: int, seed: int = 0, res_scale: float | None = None, pqmf_design=None) -> Model:
+    """Config `cfg` with weights from `seed`.  pqmf_design: (bands, taps) -> (analysis,
+    synthesis) for the PQMF stages (None: the library's sc_pqmf_filters; the oracle side passes
+    oracle.pqmf_design.filters).  res_scale: override the residual-branch scale (cfg4/cfg5)."""
+    if cfg in (4, 5):
+        kw = dict(pqmf_design=pqmf_design)
+        if res_scale is not None:
+            kw["res_scale"] = res_scale
+        return BUILDERS[cfg](seed, **kw)
     return BUILDERS[cfg](seed)
 
 

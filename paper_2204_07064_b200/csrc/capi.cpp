@@ -371,7 +371,7 @@ int sc_state_reset(sc_state* state, const int32_t* ids, int32_t n_ids, void* str
 int sc_state_device_bytes(const sc_state* state, int64_t* bytes) {
   return guard([&] {
     need(state && bytes, "null argument");
-    *bytes = state->s->mem_bytes;
+    *bytes = state->s->mem_bytes + state->s->plan_bytes;  // state + cached call plans
   });
 }
 
@@ -433,9 +433,14 @@ int sc_state_profile(sc_state* state, const float* d_in, float* d_out, int64_t f
 }
 
 const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t i) {
-  if (!state) return "";
+  // no exception may leave the C ABI: on error the name is "" and sc_last_error() says why
   thread_local std::string name;
-  name = state->s->launch_name(frames, i);
+  name.clear();
+  const int st = guard([&] {
+    need(state != nullptr, "null state");
+    name = state->s->launch_name(frames, i);
+  });
+  (void)st;
   return name.c_str();
 }
 

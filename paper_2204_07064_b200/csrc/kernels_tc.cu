@@ -32,6 +32,7 @@
 
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -1225,26 +1226,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-int g_num_sms = 0;
+// SM count per device ordinal (plans may live on different GPUs of one process)
+std::atomic<int> g_num_sms[64];
+
+int num_sms(int dev) {
+  int n = g_num_sms[dev & 63].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_num_sms[dev & 63].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0, bool CH = false>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
   using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         L::BYTES);
-    attr = true;
+  // cudaFuncSetAttribute applies to the CURRENT device only: track it per device ordinal.  A
+  // concurrent first launch on two threads just sets the (idempotent) attribute twice; a
+  // failure leaves the bit clear, and the launch below then fails loudly (the caller checks
+  // cudaGetLastError after every op).
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
+    if (cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES) == cudaSuccess)
+      attr_mask.fetch_or(bit, std::memory_order_release);
   }
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_sms = num_sms(dev);
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
-  const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
+  const int grid = n_tiles < g_sms ? n_tiles : g_sms;
   conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 

@@ -87,6 +87,8 @@ struct CallPlan {
   std::vector<int> chained;   // per op: the op chained into its launch this call (-1: none)
   std::vector<TcLaunch> tc;
   std::map<std::pair<const float*, float*>, GraphEntry> graphs;
+  uint64_t last_use = 0;      // LRU stamp (State::plan_clock)
+  int64_t dev_bytes = 0;      // device memory this plan owns (carry table)
 };
 
 struct State {
@@ -110,6 +112,12 @@ struct State {
   int64_t E = 0;              // cumulative sink frames emitted
   int64_t D = -1;             // sink lag in sink frames (fixed by the first call after reset)
   std::map<std::vector<int64_t>, std::unique_ptr<CallPlan>> plans;
+  // The CallPlan cache is bounded: with buffer lengths that keep changing, new geometries keep
+  // appearing; beyond kMaxCallPlans the least recently used plan (carry table, graphs) is freed.
+  static constexpr size_t kMaxCallPlans = 32;
+  uint64_t plan_clock = 0;
+  int64_t plan_bytes = 0;      // device bytes owned by cached CallPlans (in sc_state_device_bytes)
+  void evict_lru_plan();
   bool phase_mode = false;     // created for buffers shorter than the compression ratio
   std::vector<int64_t> cache;  // per-buffer cache frames of this state
   // Strips: each buffer holds cache + strip_k x T frames per stream; successive calls slide

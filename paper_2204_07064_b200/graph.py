@@ -43,6 +43,11 @@ class Model:
     chunks: list = field(default_factory=list)
     _n_weights: int = 0
     _C: int = -1
+    # (bands, taps) -> (analysis, synthesis) flat weights; None = the library's own design
+    # (sc_pqmf_filters).  The oracle side passes oracle.pqmf_design.filters, so a reference
+    # run never loads the product library (bench.py --impl reference) and the parity tests
+    # check the product's filter design against an independent one.
+    pqmf_design: object = None
 
     def __post_init__(self):
         self._rng = np.random.default_rng(self.seed)
@@ -137,7 +142,7 @@ class Model:
 
     # ---- PQMF (builder-defined; parity unpinned): filters from sc_pqmf_filters
     def pqmf_analysis(self, bands: int = 16, taps: int = 256) -> "Model":
-        ana, _ = pqmf_filters(bands, taps)
+        ana, _ = (self.pqmf_design or pqmf_filters)(bands, taps)
         w = ana[: bands * taps].reshape(bands, 1, taps)
         self.conv(1, bands, taps, stride=bands, padding=(taps - bands, 0), weight=w,
                   bias=np.zeros(bands, np.float32))
@@ -145,7 +150,7 @@ class Model:
         return self
 
     def pqmf_synthesis(self, bands: int = 16, taps: int = 256) -> "Model":
-        _, syn = pqmf_filters(bands, taps)
+        _, syn = (self.pqmf_design or pqmf_filters)(bands, taps)
         w = syn[: bands * taps].reshape(1, bands, taps)
         self.conv_transpose(bands, 1, taps, stride=bands, padding=(taps - 1, 0), weight=w,
                             bias=np.zeros(1, np.float32))

@@ -41,6 +41,38 @@ def _ptr(t) -> int:
     return int(t)
 
 
+def _check_io(t, name: str, shape, dtypes, where: str, device: int = -1) -> None:
+    """Validate a tensor / array handed to the C-ABI as a raw pointer: a wrong dtype, layout,
+    device or size would otherwise become out-of-bounds device reads / writes.  Plain integer
+    pointers are the caller's responsibility (raw C-ABI semantics)."""
+    if isinstance(t, int):
+        return
+    shape = tuple(int(v) for v in shape)
+    if isinstance(t, np.ndarray):
+        if where != "host":
+            raise ValueError(f"{name}: numpy arrays are host memory; a device tensor is required")
+        if t.dtype.name not in dtypes:
+            raise TypeError(f"{name}: dtype {t.dtype} not in {dtypes}")
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: must be C-contiguous")
+    elif hasattr(t, "data_ptr"):
+        dt = str(t.dtype).replace("torch.", "")
+        if dt not in dtypes:
+            raise TypeError(f"{name}: dtype {t.dtype} not in {dtypes}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+        if where == "device":
+            if t.device.type != "cuda" or (device >= 0 and t.device.index != device):
+                raise ValueError(f"{name}: must live on cuda:{device} (got {t.device})")
+        elif t.device.type != "cpu":
+            raise ValueError(f"{name}: must be a host (CPU) tensor (got {t.device})")
+    else:
+        raise TypeError(f"{name}: unsupported buffer type {type(t).__name__}")
+    if tuple(t.shape) != shape:
+        raise ValueError(f"{name}: shape {tuple(t.shape)} != expected {shape} "
+                         "([n_streams][channels][frames])")
+
+
 class Plan:
     def __init__(self, model, precision: str = "fp32", device: int = 0):
         """`model`: a flat cached-module stack (graph.Model) or a SPEC DAG (graph.Graph)."""
@@ -138,20 +170,34 @@ class StreamState:
         except Exception:  # interpreter shutdown
             pass
 
+    def _io_shapes(self, frames: int):
+        num, den, cout = self.plan.sink
+        return ((self.n_streams, self.plan.in_channels, frames),
+                (self.n_streams, cout, frames * num // den))
+
     def process_buffer(self, x, y, frames: int, stream=None) -> None:
         """x: device [n_streams][in_C][frames] fp32, y: device [n_streams][out_C][out_frames]."""
+        si, so = self._io_shapes(frames)
+        _check_io(x, "x", si, ("float32",), "device", self.plan.device)
+        _check_io(y, "y", so, ("float32",), "device", self.plan.device)
         check(lib().sc_process(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
                                C.c_void_p(_stream_handle(stream))))
 
     def process_host(self, x, y, frames: int, stream=None) -> None:
         """Host-buffer process_buffer (pinned host memory for overlap): x/y host arrays or
         pinned torch CPU tensors with the same layouts as process_buffer."""
+        si, so = self._io_shapes(frames)
+        _check_io(x, "x", si, ("float32",), "host")
+        _check_io(y, "y", so, ("float32",), "host")
         check(lib().sc_process_host(self._h, C.c_void_p(_hptr(x)), C.c_void_p(_hptr(y)), frames,
                                     C.c_void_p(_stream_handle(stream))))
 
     def process_host_bf16(self, x, y, frames: int, stream=None) -> None:
         """process_host with bf16 host buffers (torch.bfloat16 pinned tensors or uint16 arrays):
         half the PCIe bytes; outputs rounded to bf16 on the device."""
+        si, so = self._io_shapes(frames)
+        _check_io(x, "x", si, ("bfloat16", "uint16"), "host")
+        _check_io(y, "y", so, ("bfloat16", "uint16"), "host")
         check(lib().sc_process_host_bf16(self._h, C.c_void_p(_hptr(x)), C.c_void_p(_hptr(y)), frames,
                                          C.c_void_p(_stream_handle(stream))))
 
@@ -189,6 +235,9 @@ class StreamState:
         """Per-launch mean device ms over `steps` un-graphed calls (CUDA events between
         launches on the launching stream).  Returns [(name, ms)]."""
         n = self.launches(frames)
+        si, so = self._io_shapes(frames)
+        _check_io(x, "x", si, ("float32",), "device", self.plan.device)
+        _check_io(y, "y", so, ("float32",), "device", self.plan.device)
         ms = (C.c_float * n)()
         check(lib().sc_state_profile(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), frames,
                                      steps, ms, C.c_void_p(_stream_handle(stream))))

@@ -40,3 +40,20 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def oracle_model(cfg: int, seed: int = 0, **kw):
+    """The ORACLE-side twin of configs.build(cfg, seed): identical weights, but the PQMF
+    stages take their filters from the independent design (oracle/pqmf_design.py) instead of
+    the product's sc_pqmf_filters — so cfg4 / cfg5 parity checks the product's filter design
+    too (the two agree to <= 1e-7, test_host.py::test_pqmf_filters_match_independent_design)."""
+    from oracle import pqmf_design
+    from paper_2204_07064_b200 import configs
+    return configs.build(cfg, seed=seed, pqmf_design=pqmf_design.filters, **kw)
+
+
+
+def oracle_twin(model):
+    """Oracle-side twin of a built flat Model (PQMF weights from the independent design)."""
+    from oracle import pqmf_design
+    return pqmf_design.twin(model)

@@ -7,6 +7,7 @@ within CHAIN_TOL of the two-launch form and within the north-star tolerance of t
 import numpy as np
 import pytest
 
+from conftest import oracle_twin
 from oracle import pyoracle as po
 from paper_2204_07064_b200 import configs
 from paper_2204_07064_b200.runtime import Plan
@@ -51,7 +52,7 @@ def test_cfg2_chain_one_accumulator(parts, monkeypatch):
     y0, _, _ = run_gpu(m, x, parts, plan=p0)
     y1, _, _ = run_gpu(m, x, parts, plan=p1)
     assert rel_err(y1, y0)[0] <= CHAIN_TOL
-    err, rms = rel_err(y1, po.run(m, x, parts, "stream"))
+    err, rms = rel_err(y1, po.run(oracle_twin(m), x, parts, "stream"))
     assert err <= FP32_TOL, f"{err:.3e} x RMS ({rms:.3e})"
 
 
@@ -68,7 +69,7 @@ def test_cfg2_chain_bit_identical(parts, monkeypatch):
     assert sum("+" in n.split()[0] for n in names) == 4, names  # four chained residual blocks
     assert not any(n.startswith("op1 ") for n in names), names
     if sum(parts) <= 2048:
-        err, rms = rel_err(y1, po.run(m, x, parts, "stream"))
+        err, rms = rel_err(y1, po.run(oracle_twin(m), x, parts, "stream"))
         assert err <= FP32_TOL, f"{err:.3e} x RMS ({rms:.3e})"
 
 

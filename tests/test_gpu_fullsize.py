@@ -6,6 +6,7 @@ that holds it), and the selected streams match the oracle within the fp32 tolera
 import numpy as np
 import pytest
 
+from conftest import oracle_twin
 from oracle import pyoracle as po
 from paper_2204_07064_b200 import configs
 from paper_2204_07064_b200.runtime import Plan, StreamState
@@ -48,6 +49,6 @@ def test_full_stream_count(cfg):
     y_small = torch.cat(outs, dim=2).cpu().numpy()
     assert np.array_equal(y_full, y_small)
     x_np = torch.cat([x[pick] for x in xs], dim=2).cpu().numpy()
-    y_or = po.run(m, x_np, [F] * calls, "stream")
+    y_or = po.run(oracle_twin(m), x_np, [F] * calls, "stream")
     err, rms = rel_err(y_full, y_or)
     assert err <= FP32_TOL, (err, rms)

@@ -6,6 +6,7 @@ Tolerance (north star): fp32 path max |gpu - oracle| <= 1e-4 x RMS(oracle output
 import numpy as np
 import pytest
 
+from conftest import oracle_model, oracle_twin
 from oracle import pyoracle as po
 from paper_2204_07064_b200 import configs
 from paper_2204_07064_b200.runtime import Plan, StreamState
@@ -44,23 +45,28 @@ CASES = [
     (1, 1, [2048] * 64),
     (2, 4, [2048, 2048]),
     (3, 3, [4096, 4096]),
-    (4, 4, [1] * 8),
-    (5, 4, [2048] * 8),
+    (4, 4, [1] * 8),            # literal BASELINE init (Kaiming, no residual scale)
+    (5, 2, [2048] * 20),       # past the 32848-sample latency: measured on signal
+    (5, 2, [8192] * 5),        # the north star's B = 8192 point of the buffer sweep
 ]
+IDS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg5_b8192"]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg,streams,parts", CASES, ids=[f"cfg{c[0]}" for c in CASES])
+@pytest.mark.parametrize("cfg,streams,parts", CASES, ids=IDS)
 def test_config_parity_fp32(cfg, streams, parts):
+    """GPU (product model, sc_pqmf_filters) vs the oracle run of the ORACLE-side twin (same
+    weights, PQMF filters from the independent design oracle/pqmf_design.py)."""
     m = configs.build(cfg, seed=cfg)
+    m_or = oracle_model(cfg, seed=cfg)
     x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=cfg)
-    y_or = po.run(m, x, parts, "stream")
+    y_or = po.run(m_or, x, parts, "stream")
     y_gpu, plan, _ = run_gpu(m, x, parts)
     err, rms = rel_err(y_gpu, y_or)
     assert np.isfinite(y_gpu).all()
     assert err <= FP32_TOL, f"cfg{cfg}: max err {err:.3e} x RMS ({rms:.3e})"
     # and the offline convolution of the concatenated signal (SPEC.md:275,296)
-    y_off = po.run(m, x, None, "offline")
+    y_off = po.run(m_or, x, None, "offline")
     err2, _ = rel_err(y_gpu, y_off)
     assert err2 <= FP32_TOL
 
@@ -80,7 +86,7 @@ BF16_CORR = 0.9998
 def test_config_parity_bf16(cfg, streams, parts):
     m = configs.build(cfg, seed=cfg)
     x = configs.batch_input(cfg, range(streams), m.in_channels, sum(parts), seed=cfg)
-    y_or = po.run(m, x, parts, "stream")
+    y_or = po.run(oracle_model(cfg, seed=cfg), x, parts, "stream")
     y_gpu, plan, _ = run_gpu(m, x, parts, precision="bf16")
     err, rms = rel_err(y_gpu, y_or)
     nrmse = float(np.sqrt(np.mean((y_gpu.astype(np.float64) - y_or) ** 2))) / rms
@@ -134,19 +140,63 @@ def test_reset_all_and_subset():
 
 
 @pytest.mark.gpu
+def test_subset_reset_phase_state():
+    """Subset reset with buffers shorter than the compression ratio (cfg5, B = 512 < 2048):
+    at a period boundary the reset stream continues exactly like a fresh stream; mid-period
+    the call is refused (the streams share one phase; a fresh stream would window differently)."""
+    from paper_2204_07064_b200 import StreamconvError
+    m = configs.build(5, seed=5)
+    plan = Plan(m)
+    B = 512
+    r = plan.ratio
+    x_pre = configs.batch_input(5, range(2), 1, r, seed=1)
+    x_post = configs.batch_input(5, range(2, 4), 1, 8 * r, seed=2)
+    y_fresh, _, _ = run_gpu(m, x_post, [B] * (8 * r // B), plan=plan)
+    st = StreamState(plan, 2, B)
+    run_gpu(m, x_pre[..., :3 * B], [B] * 3, plan=plan, state=st)       # mid-period
+    with pytest.raises(StreamconvError) as e:
+        st.reset([1])
+    assert e.value.code == "InvalidArgument"
+    run_gpu(m, x_pre[..., 3 * B:], [B], plan=plan, state=st)             # period complete
+    st.reset([1])
+    y2, _, _ = run_gpu(m, x_post, [B] * (8 * r // B), plan=plan, state=st)
+    assert np.array_equal(y2[1], y_fresh[1])
+    assert not np.array_equal(y2[0], y_fresh[0])
+
+
+@pytest.mark.gpu
 def test_memory_constancy():
     """state size is a constant of the model, not of the stream length."""
     m = configs.build(2, seed=1)
     plan = Plan(m)
     st = StreamState(plan, 2, 256)
-    b0 = (st.device_bytes, st.cache_bytes)
     x = torch.randn(2, 128, 256, device="cuda")
     y = torch.empty_like(x)
+    for _ in range(8):      # the strip cycle's call plans are all created within a few calls
+        st.process_buffer(x, y, 256)
+    b0 = (st.device_bytes, st.cache_bytes)
     for _ in range(200):
         st.process_buffer(x, y, 256)
     torch.cuda.synchronize()
     assert (st.device_bytes, st.cache_bytes) == b0
     assert plan.state_bytes == 61440  # closed form, SPEC.md:259 (4 blocks x 128 x 3d x 4 B)
+
+
+@pytest.mark.gpu
+def test_call_plan_cache_bounded():
+    """Ever-changing buffer lengths create new call plans (carry tables, graphs); the cache is
+    LRU-bounded, so device memory stays bounded, and the outputs stay the oracle's."""
+    m = configs.build(2, seed=2)
+    plan = Plan(m)
+    parts = [17 + 3 * i for i in range(60)]            # 60 distinct geometries
+    x = configs.batch_input(2, range(2), 128, sum(parts), seed=2)
+    st = StreamState(plan, 2, max(parts))
+    base = st.device_bytes
+    y, _, _ = run_gpu(m, x, parts, plan=plan, state=st)
+    grown = st.device_bytes - base
+    assert 0 < grown <= 32 * 64 * 64, grown             # <= 32 plans x (<= 64 descriptors)
+    err, rms = rel_err(y, po.run(m, x, parts, "stream"))
+    assert err <= FP32_TOL, err
 
 
 @pytest.mark.gpu
@@ -167,14 +217,29 @@ def test_process_errors():
     m = configs.build(3, seed=0)
     plan = Plan(m)
     st = StreamState(plan, 1, 256)
-    x = torch.zeros(1, 16, 256, device="cuda")
-    y = torch.zeros(1, 16, 256, device="cuda")
+    x = torch.zeros(1, 16, 100, device="cuda")
+    y = torch.zeros(1, 16, 100, device="cuda")
     with pytest.raises(StreamconvError) as e:
         st.process_buffer(x, y, 100)  # not a multiple of r=128
     assert e.value.code == "BufferNotMultipleOfRatio"
+    x = torch.zeros(1, 16, 512, device="cuda")
+    y = torch.zeros(1, 16, 512, device="cuda")
     with pytest.raises(StreamconvError) as e:
         st.process_buffer(x, y, 512)  # > max_frames
     assert e.value.code == "InvalidArgument"
+    # the Python wrapper validates buffers before handing raw pointers to the C-ABI
+    x = torch.zeros(1, 16, 256, device="cuda")
+    y = torch.zeros(1, 16, 256, device="cuda")
+    with pytest.raises(ValueError):
+        st.process_buffer(x[:, :, :128], y, 256)                    # wrong shape
+    with pytest.raises(TypeError):
+        st.process_buffer(x.double(), y, 256)                       # wrong dtype
+    with pytest.raises(ValueError):
+        st.process_buffer(torch.zeros(1, 256, 16, device="cuda").transpose(1, 2), y, 256)  # strided
+    with pytest.raises(ValueError):
+        st.process_buffer(x.cpu(), y, 256)                          # host tensor on the device path
+    with pytest.raises(ValueError):
+        st.process_host(x, y.cpu(), 256)                            # device tensor on the host path
     with pytest.raises(StreamconvError) as e:
         StreamState(plan, 1, 200)
     assert e.value.code == "BufferNotMultipleOfRatio"
@@ -212,8 +277,8 @@ def test_phase_state_short_buffers(cfg, B):
     r = plan.ratio
     total = 8 * r   # long enough to leave the start-up transient (cfg5 RF is ~33k samples)
     x = configs.batch_input(cfg, range(2), m.in_channels, total, seed=cfg)
-    y_ref = po.run(m, x, [r] * 8, "stream")          # aligned reference (== offline)
-    y_ph = po.run(m, x, [B] * (total // B), "phase")  # oracle phase-state concatenation
+    y_ref = po.run(oracle_twin(m), x, [r] * 8, "stream")          # aligned reference (== offline)
+    y_ph = po.run(oracle_twin(m), x, [B] * (total // B), "phase")  # oracle phase-state concatenation
     assert np.array_equal(y_ref, y_ph)
     st = StreamState(plan, 2, B)
     y_gpu, _, _ = run_gpu(m, x, [B] * (total // B), plan=plan, state=st)
@@ -296,7 +361,7 @@ def test_pqmf_fast_form_vs_oracle(parts):
     names = st.launch_names(parts[0])
     assert any("pqmf-analysis" in n and n.endswith("[pqmf]") for n in names), names
     assert any("pqmf-synthesis" in n and n.endswith("[pqmf]") for n in names), names
-    ref = po.run(m, x, parts=parts)
+    ref = po.run(oracle_twin(m), x, parts=parts)
     err, rms = rel_err(y, ref)
     assert err <= FP32_TOL, (err, rms)
 
@@ -332,7 +397,7 @@ def test_strips_match_oracle(monkeypatch, cfg, streams, parts):
     y1, _, _ = run_gpu(m, x, parts)
     assert np.array_equal(y3, y1)
     if cfg != 5:  # cfg5's oracle parity needs the long warmed-up run of test_config_parity_fp32
-        y_or = po.run(m, x, parts, "stream")
+        y_or = po.run(oracle_twin(m), x, parts, "stream")
         err, rms = rel_err(y3, y_or)
         assert err <= FP32_TOL, (err, rms)
 
@@ -398,7 +463,7 @@ def test_bf16_phase_state_and_reset():
     r, B = plan.ratio, 512
     total = 8 * r
     x = configs.batch_input(5, range(2), m.in_channels, total, seed=5)
-    y_ref = po.run(m, x, [r] * 8, "stream")
+    y_ref = po.run(oracle_twin(m), x, [r] * 8, "stream")
     st = StreamState(plan, 2, B)
     y_gpu, _, _ = run_gpu(m, x, [B] * (total // B), plan=plan, state=st)
     D = r - B

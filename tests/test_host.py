@@ -137,6 +137,24 @@ def test_pqmf_filters_design():
     np.testing.assert_allclose(ana[k * 256:(k + 1) * 256], hk[::-1].astype(np.float32), atol=1e-7)
 
 
+def test_pqmf_filters_match_independent_design():
+    """The product's filter design (csrc/pqmf.cpp: Bessel series + golden-section search) is
+    pinned to an independent numpy/scipy restatement of the published Kaiser-window PQMF
+    design (oracle/pqmf_design.py: numpy.kaiser / numpy.sinc / numpy.correlate + bounded
+    Brent) — the reference itself has no PQMF."""
+    from oracle import pqmf_design as pd
+    from paper_2204_07064_b200.graph import pqmf_filters, pqmf_prototype
+    for M, N in ((16, 256), (4, 64), (8, 128)):
+        p, wc = pd.design(M, N)
+        np.testing.assert_allclose(pqmf_prototype(M, N), p, rtol=0, atol=1e-8)
+        ana, syn = pqmf_filters(M, N)
+        a2, s2 = pd.filters(M, N)
+        np.testing.assert_allclose(ana, a2, rtol=0, atol=1e-7)
+        np.testing.assert_allclose(syn / M, s2 / M, rtol=0, atol=1e-7)
+        # the published design criterion: 2M-lag autocorrelation of the prototype vanishes
+        assert pd.objective(M, N, wc, pd.kaiser_beta(100.0)) < 1e-4
+
+
 def test_cpp_cached_module_api_host():
     """include/streamconv_b200.hpp (C++ cached-module API) builds plans host-only."""
     import subprocess
