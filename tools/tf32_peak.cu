@@ -7,10 +7,12 @@
 //   mode 0: SS  kind::tf32  (A and B from 128B-swizzled shared memory), K = 8 per MMA
 //   mode 1: TS  kind::tf32  (A from TMEM, B from shared memory)   — the form conv_tc_kernel uses
 //   mode 2: SS  kind::f16 with bf16 operands, K = 16 per MMA
+//   mode 3: TS  kind::f16 with fp16 operands (A from TMEM), K = 16 per MMA — the 3xFP16 path
 // FLOPs per MMA = 2 x 128 x N x K.  Driven by tools/tf32_peak.py (ctypes; CUDA events; burst =
 // one ~20 ms launch, sustained = back-to-back launches for 4 s; NVML clocks sampled alongside).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC
 //        -o tools/bin/libtf32_peak.so tools/tf32_peak.cu
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -48,6 +50,14 @@ __device__ __forceinline__ void mma_ss(int mode, uint32_t d, uint64_t a, uint64_
   }
 }
 
+__device__ __forceinline__ void mma_ts_f16(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -82,7 +92,10 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int n, int iters, float* s
   // permutes 16-byte chunks within a row, irrelevant for random data
   for (int i = tid; i < (128 + n) * 32; i += blockDim.x) {
     const float v = rnd(i * 2654435761u + blockIdx.x);
-    if (mode == 2) {
+    if (mode == 3) {
+      const __half2 h2 = __floats2half2_rn(v, rnd(i + 77777u));
+      reinterpret_cast<__half2*>(sm)[i] = h2;
+    } else if (mode == 2) {
       uint32_t lo = __float_as_uint(v) >> 16, hi = __float_as_uint(rnd(i + 77777u)) >> 16;
       reinterpret_cast<uint32_t*>(sm)[i] = lo | (hi << 16);
     } else {
@@ -104,8 +117,8 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int n, int iters, float* s
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // warp-uniform (shfl) so the MMA operands live in uniform registers: no R2UR waterfall
   const uint32_t tbase = __shfl_sync(0xffffffffu, tslot, 0);
-  if (mode == 1) {
-    // A (128 x 32 tf32) into TMEM columns [256, 288): lane = row, warp w owns lanes 32w..
+  if (mode == 1 || mode == 3) {
+    // A (128 x 32 tf32 / 128 x 64 fp16) into TMEM columns [256, 288): lane = row, warp w owns lanes 32w..
     float v[32];
     for (int j = 0; j < 32; ++j) v[j] = rnd((tid * 32 + j) * 2246822519u + 13u);
     const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + 256;
@@ -123,7 +136,7 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int n, int iters, float* s
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0) {
-    const uint32_t fmt = mode == 2 ? 1u : 2u;
+    const uint32_t fmt = mode == 2 ? 1u : mode == 3 ? 0u : 2u;
     const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
                            (static_cast<uint32_t>(128 >> 4) << 24);
     const uint64_t ad = sw128_desc(__shfl_sync(0xffffffffu, smem_u32(sa), 0));
@@ -137,6 +150,8 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int n, int iters, float* s
         const uint32_t acc = (it > 1 || kk > 0) ? 1u : 0u;
         if (mode == 1)
           mma_ts(d, tbase + 256 + kk * 8, bd + 2 * kk, idesc, acc);   // +32 B = +2 in the address field
+        else if (mode == 3)
+          mma_ts_f16(d, tbase + 256 + kk * 8, bd + 2 * kk, idesc, acc);
         else
           mma_ss(mode, d, ad + 2 * kk, bd + 2 * kk, idesc, acc);
       }
@@ -171,7 +186,7 @@ extern "C" {
 // a negative CUDA error code.
 float tf32_peak_run(int mode, int n, int iters, int blocks, int launches) {
   const size_t smem = 1024 + static_cast<size_t>(128 + n) * 128;
-  auto kern = mode == 0 ? peak_kernel<0> : mode == 1 ? peak_kernel<1> : peak_kernel<2>;
+  auto kern = mode == 0 ? peak_kernel<0> : mode == 1 ? peak_kernel<1> : mode == 2 ? peak_kernel<2> : peak_kernel<3>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   float* sink = nullptr;
   if (cudaMalloc(&sink, sizeof(float) * blocks) != cudaSuccess) return -1.f;
