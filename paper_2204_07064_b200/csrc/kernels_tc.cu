@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <atomic>
 #include <cstdint>
@@ -59,8 +60,43 @@ constexpr int BK = 32;  // fp32 per 128-byte swizzled row
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr int NUM_THREADS = 480;
 constexpr int IO_WARP = 2;    // residual TMA loads + output TMA stores
-constexpr int XF_WARP0 = 3;   // transform warps 3..6
-constexpr int EP_WARP0 = 7;   // drain/epilogue warps 7..14
+constexpr int XF_WARP0 = 3;   // transform warps 3..6 (3..10: two sets, X2)
+constexpr int EP_WARP0 = 7;   // drain/epilogue warps 7..14 (11..18, X2)
+// X2 (3xFP16 non-window tiles): two sets of four transform warps take alternate K-slabs — one
+// set of four (one warp per SM sub-partition) could not split a slab as fast as kind::f16 MMAs
+// consume it (measured ~0.9k cycles per slab vs 384 cycles of MMA)
+template <bool X2> struct Roles {
+  static constexpr int NXF = X2 ? 8 : 4;
+  static constexpr int EP0 = XF_WARP0 + NXF;
+  static constexpr int NT = (EP0 + 8) * 32;
+};
+
+// packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): same round-to-nearest results as
+// the scalar forms, half the instructions
+__device__ __forceinline__ void ffma2_acc(float& a0, float& a1, float v0, float v1, float f) {  // a += v * f
+  asm("{\n\t.reg .b64 A, V, F;\n\tmov.b64 A, {%0, %1};\n\tmov.b64 V, {%2, %3};\n\tmov.b64 F, {%4, %4};\n\t"
+      "fma.rn.f32x2 A, V, F, A;\n\tmov.b64 {%0, %1}, A;\n\t}"
+      : "+f"(a0), "+f"(a1) : "f"(v0), "f"(v1), "f"(f));
+}
+__device__ __forceinline__ void fadd2_acc(float& a0, float& a1, float v0, float v1) {  // a += v
+  asm("{\n\t.reg .b64 A, V;\n\tmov.b64 A, {%0, %1};\n\tmov.b64 V, {%2, %3};\n\t"
+      "add.rn.f32x2 A, A, V;\n\tmov.b64 {%0, %1}, A;\n\t}"
+      : "+f"(a0), "+f"(a1) : "f"(v0), "f"(v1));
+}
+__device__ __forceinline__ float2 fmul2s(float x0, float x1, float f) {  // x * f
+  float2 r;
+  asm("{\n\t.reg .b64 X, F, R;\n\tmov.b64 X, {%2, %3};\n\tmov.b64 F, {%4, %4};\n\t"
+      "mul.rn.f32x2 R, X, F;\n\tmov.b64 {%0, %1}, R;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(x0), "f"(x1), "f"(f));
+  return r;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {  // a - b
+  float2 r;
+  asm("{\n\t.reg .b64 A, B, R;\n\tmov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "sub.rn.f32x2 R, A, B;\n\tmov.b64 {%0, %1}, R;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -304,22 +340,35 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 constexpr int WIN_ROWS = 144;     // fp32 windows: 128 + halo (<= 16)
 constexpr int WIN_ROWS_BF = 192;  // bf16 windows of narrow tiles: 128 + halo (<= 64)
 constexpr uint32_t WREG = 112 * 1024;
-template <int BN, int STAGES, bool BF = false, bool WIN = false, int IOB = 0>
+constexpr uint32_t WREG_H = 56 * 1024;  // 3xFP16 windows: fp16 hi + lo weight planes are half the bytes
+// 3xFP16 (HF): per-row power-of-two scale exponents, one byte per (32-channel row, K-slab):
+// a ring of RS_RING slabs x 128 rows (non-window) or RS_WIN windows x WROWS rows (window mode),
+// deep enough that the transform never overwrites an entry the drain has not read yet
+// (transform of slab g implies the drain finished slab g - STAGES - NB; see HF below)
+constexpr int RS_RING = 32;
+constexpr int RS_WIN = 16;
+template <int BN, int STAGES, bool BF = false, bool WIN = false, int IOB = 0, bool HF = false>
 struct TcSmem {
-  static constexpr uint32_t B_TILE = BF ? BN * BK * 2 : BN * BK * 4;
+  static constexpr uint32_t B_TILE = (BF || HF) ? BN * BK * 2 : BN * BK * 4;
   static constexpr uint32_t STAGE = WIN ? (BF ? B_TILE : 2 * B_TILE) : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
-  // window slots: fp32 = A hi + A lo (SW128); bf16 = the raw fp32 rows + their bf16 copy (SW64)
-  static constexpr int AST = WIN ? (BF ? 3 : 2) : 0;
+  // window slots: fp32 = A hi + A lo (SW128); bf16 = the raw fp32 rows + their bf16 copy (SW64);
+  // 3xFP16 = the raw fp32 rows, converted in place to fp16 hi | lo planes (SW64)
+  static constexpr int AST = WIN ? (BF ? 3 : HF ? 4 : 2) : 0;
   // bf16 windows hold 128 + 64 rows when they fit three slots next to the staging tile (narrow
   // tiles, or bf16 input rows: a raw bf16 row is half the size)
   static constexpr bool ABF = BF && (IOB & 1);
   static constexpr int WROWS = (BF && (BN < 128 || ABF)) ? WIN_ROWS_BF : WIN_ROWS;
-  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * ((ABF ? 2 : 4) + 2) : 2 * WROWS * BK * 4;
+  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * ((ABF ? 2 : 4) + 2) : HF ? WROWS * BK * 4 : 2 * WROWS * BK * 4;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
-  static constexpr uint32_t WBYTES = (WIN && !BF) ? WREG : STAGES * STAGE;
+  // 3xFP16 BN = 128 windows: a W ring of STAGES K-slab tiles (never resident); BN <= 64: the
+  // 56 KB weight region (ring or the whole weight)
+  static constexpr uint32_t WBYTES =
+      (WIN && !BF) ? (HF ? (BN == 128 ? STAGES * STAGE : WREG_H) : WREG) : STAGES * STAGE;
+  static constexpr uint32_t RSB = HF ? (WIN ? RS_WIN * WROWS : RS_RING * BM) : 0;
   static constexpr uint32_t BYTES =
-      WBYTES + AST * WIN_SLOT + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + 1024;
-  static_assert(!WIN || BF || STAGES * STAGE <= WREG, "window ring fits the weight region");
+      WBYTES + AST * WIN_SLOT + STAGING + 1024 /*barriers*/ + 8192 /*bias*/ + RSB + 1024;
+  static_assert(!WIN || BF || (HF && BN == 128) || STAGES * STAGE <= (HF ? WREG_H : WREG),
+                "window ring fits the weight region");
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
@@ -372,12 +421,27 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
 
 // IOB (bf16 plans): bit 0 = the input buffer holds bf16, bit 1 = the output (and residual)
 // buffer holds bf16 — compile-time, so each instance carries only its own load / store paths
-template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB, bool CH>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+//
+// HF (fp32 plans, "3xFP16"): the same three-product split as 3xTF32, in fp16 — kind::f16 runs at
+// twice the kind::tf32 rate and the weight planes are half the bytes.  fp16 has tf32's 11-bit
+// significand but only a 5-bit exponent, so every operand row is block-scaled by a power of two
+// first (exact): the transform scales each (row, 32-channel K-slab) so its largest |a| lands in
+// [2^14, 2^15), splits a = hi + lo (hi = fp16_rn(a), lo = fp16_rn(a - hi): ~22 significant bits,
+// as tf32 hi + lo), and records the unscale exponent; weights carry one power-of-two scale per
+// layer (plan time).  Each K-slab is its own chunk accumulator (CK = 1), so the drain multiplies
+// the chunk by the row's exact 2^-(s + s_w) as it adds it (one fma: the product is exact).  The
+// scale depends only on the row's own 32 values: identical in window and non-window mode, for
+// any tile geometry (bit-identity across buffer partitions).
+template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB, bool CH, bool HF>
+__global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
-  using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
+  using L = TcSmem<BN, STAGES, BF, WIN, IOB, HF>;
+  static_assert(!HF || (!BF && !CH && CK == 1), "3xFP16: fp32 plans, unchained, one K-slab per chunk");
+  constexpr bool X2 = HF && !WIN;
+  constexpr int EP0 = Roles<X2>::EP0;
+  constexpr int NT = Roles<X2>::NT;
   constexpr bool ABF = BF && (IOB & 1);  // input rows are bf16
   constexpr bool OBF = BF && (IOB & 2);  // output / residual rows are bf16
   extern __shared__ uint8_t smem_raw[];
@@ -404,6 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* a2full = bars + 4 * STAGES + 38;   // [<= 4] chained GEMM's A slot written (CH)
   uint64_t* a2empty = bars + 4 * STAGES + 42;  // [<= 4] chained GEMM's A slot read by its MMAs (CH)
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);  // <= 2048 floats
+  uint8_t* rsc = reinterpret_cast<uint8_t*>(bars) + 1024 + 8192;  // HF: per-row unscale exponents
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
   auto b_hi = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE); };
@@ -412,6 +477,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto win_hi = [&](int sa) { return wins + sa * L::WIN_SLOT; };
   auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // fp32: A lo
   auto win_bf = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * (ABF ? 2 : 4); };  // bf16 copy
+  auto win_lo16 = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 2; };  // HF: fp16 lo plane
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -426,11 +492,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // + A lo (32 cols) per slot (none in window mode: A is in shared memory); bf16: 16 cols per
   // slot (32 bf16 per row, two per column).  As many chunk accumulators as fit (<= 8), so the
   // MMAs run ahead across a tile-boundary epilogue.
-  constexpr int TS = BF ? STAGES : WIN ? 2 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
+  constexpr int TS = BF ? STAGES : WIN ? 2 : HF ? 4 : BN == 128 ? 2 : (STAGES < 4 ? STAGES : 4);
   static_assert(4 * STAGES + 46 <= 128, "barrier area");
   static_assert(!CH || (BN == 128 && CK == (BF ? 4 : 1) && (BF || !WIN)), "chained conv: BN = 128 (windows: bf16)");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
-  constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : 64 * TS;
+  constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : HF ? 32 * TS : 64 * TS;
   // CH: two chunk accumulators + the A ring + the chained GEMM's A slots — fp32: two slots of
   // 64 columns (32 channels hi | lo); bf16: four of 16 (32 channels as bf16 pairs, one per slab)
   constexpr int NS2 = BF ? 4 : 2;
@@ -490,9 +556,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     g_tc_trace[9 * 256 + blockIdx.x] = smid;
   }
-  for (int i = threadIdx.x; i < p.nout; i += NUM_THREADS) sbias[i] = p.bias[i];
+  for (int i = threadIdx.x; i < p.nout; i += NT) sbias[i] = p.bias[i];
   if (CH)  // first conv's bias at [0, BN) (p.bias), the chained conv's at [BN, 2 BN)
-    for (int i = threadIdx.x; i < BN; i += NUM_THREADS) sbias[BN + i] = p.bias2[i];
+    for (int i = threadIdx.x; i < BN; i += NT) sbias[BN + i] = p.bias2[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -580,6 +646,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
               mma_bf16_w(dmain, sw64_desc(wb + offb + kk * 32), sw64_desc(bb + kk * 32), idesc_bf, acc0);
             }
+          } else if (HF) {  // fp16 hi / lo window planes (SW64 rows of 64 B), tap q at a row offset
+            const uint32_t idesc_h = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(BM >> 4) << 24);  // F32 += F16 x F16
+            const uint32_t offh = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
+            const int ws = p.wres ? kb : s;
+            const uint32_t ah = smem_u32(win_hi(sa)) + offh, al = smem_u32(win_lo16(sa)) + offh;
+            const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_bf16_w(dmain, sw64_desc(al + kk * 32), sw64_desc(bh + kk * 32), idesc_h, acc0);
+              mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bl + kk * 32), idesc_h, 1u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bh + kk * 32), idesc_h, 1u);
           } else {
             const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
             const int ws = p.wres ? kb : s;
@@ -632,7 +714,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (WIN && warp >= XF_WARP0 && warp < EP_WARP0) {
+  } else if (WIN && warp >= XF_WARP0 && warp < EP0) {
     // ===================== transform, window mode: hi in place, lo to the lo window ==========
     const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
     const bool pre_tanh = p.pre_act == ACT_TANH;
@@ -703,6 +785,100 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               pk[k] = *reinterpret_cast<uint32_t*>(&b2);
             }
             bfr[w * 4 + (jo ^ ((w >> 1) & 3))] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wa_ready[sa]);
+          continue;
+        }
+        if (HF) {
+          // raw fp32 rows (SW128, 16B chunk j of row w at j ^ (w & 7)) -> pre-activation ->
+          // per-row power-of-two scale -> fp16 hi | lo planes written IN PLACE over the raw rows
+          // (SW64 rows of 64 B: 16B chunk jb of row w at jb ^ ((w >> 1) & 3)), once every
+          // thread of the four warps has read its rows (named barrier 1).  Thread t owns row t
+          // whole (no shuffles) plus one 16-byte item of the halo rows 128 .. 143 (8 lanes per
+          // row, max by three shuffles).  Rows past the window are converted too (stale data,
+          // never read by an MMA): no branches, so the two rows' math interleaves.
+          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
+          float4 v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = raw[t * 8 + (j ^ (t & 7))];
+          const int we = BM + (t >> 3), je = t & 7;
+          const float4 ve = raw[we * 8 + (je ^ (we & 7))];
+          named_bar(1, 128);
+          uint8_t* rsw = rsc + (u % RS_WIN) * L::WROWS;
+          const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
+          const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
+          const float scf = (!pre_tanh && pre_s > 1.f) ? pre_s : 1.f;  // scale rule: see the non-window HF
+          {
+            float m = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+            m *= scf;
+            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+            const float scn = sc * pre_s;
+            uint32_t hv[16], lv[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
+              float2 t2;
+              if (pre_tanh) {
+                t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
+              } else {
+                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+              }
+              const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
+              const float2 l = fsub2(t2, __half22float2(h2));
+              const __half2 l2 = __floats2half2_rn(l.x, l.y);
+              hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
+              lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
+            }
+            uint4* hr = reinterpret_cast<uint4*>(win_hi(sa)) + t * 4;
+            uint4* lr = reinterpret_cast<uint4*>(win_lo16(sa)) + t * 4;
+#pragma unroll
+            for (int jb = 0; jb < 4; ++jb) {
+              hr[jb ^ ((t >> 1) & 3)] = make_uint4(hv[4 * jb], hv[4 * jb + 1], hv[4 * jb + 2], hv[4 * jb + 3]);
+              lr[jb ^ ((t >> 1) & 3)] = make_uint4(lv[4 * jb], lv[4 * jb + 1], lv[4 * jb + 2], lv[4 * jb + 3]);
+            }
+            rsw[t] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+          }
+          {
+            float m = fmaxf(fmaxf(fabsf(ve.x), fabsf(ve.y)), fmaxf(fabsf(ve.z), fabsf(ve.w)));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+            m *= scf;
+            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+            const float scn = sc * pre_s;
+            uint32_t hv[2], lv[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const float x0 = k ? ve.z : ve.x, x1 = k ? ve.w : ve.y;
+              float2 t2;
+              if (pre_tanh) {
+                t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
+              } else {
+                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+              }
+              const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
+              const float2 l = fsub2(t2, __half22float2(h2));
+              const __half2 l2 = __floats2half2_rn(l.x, l.y);
+              hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
+              lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
+            }
+            const int po = we * 8 + (((je >> 1) ^ ((we >> 1) & 3)) << 1) + (je & 1);  // uint2 units
+            reinterpret_cast<uint2*>(win_hi(sa))[po] = make_uint2(hv[0], hv[1]);
+            reinterpret_cast<uint2*>(win_lo16(sa))[po] = make_uint2(lv[0], lv[1]);
+            if (je == 0) rsw[we] = static_cast<uint8_t>(127 - sx - p.f16_sw);
           }
           fence_proxy_async();
           __syncwarp();
@@ -780,6 +956,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
             tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
           }
+          // 3xFP16 (cbmaj order): at the first tap of a 32-channel block, warm L2 with the A box
+          // of the block p.pf_dist blocks ahead (the next tile's when past this tile's last):
+          // the ring's few stages cannot cover the input's DRAM latency at the kind::f16 rate
+          if (HF && p.pf_dist > 0 && q == 0 && lane == 0) {
+            int cbn = cb + p.pf_dist, tn = tile;
+            while (cbn >= p.cblocks) cbn -= p.cblocks, tn += gridDim.x;
+            if (tn < n_tiles) {
+              const TileCoord tq = tile_coord(p, tn, n_tiles_n, BN);
+              tma_prefetch_3d(&tmap_a, p.a_c0 + cbn * BK, p.a_row0 + tq.i0, tq.s0);
+            }
+          }
           if (p.cbmaj) {
             if (++q == taps) q = 0, ++cb;
           } else if (++cb == p.cblocks) {
@@ -793,7 +980,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     {
       const uint32_t tbase = warp_uniform(tmem_base);
       // c_format F32 | a,b format TF32 (2) or BF16 (1) | N >> 3 | M >> 4
-      const uint32_t fmt = BF ? 1u : 2u;
+      const uint32_t fmt = BF ? 1u : HF ? 0u : 2u;  // HF: F16
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(BM >> 4) << 24);
       int g = 0, c = 0, tcount = 0, ga = 0;  // ga: A-ring slab counter (first-conv slabs)
@@ -855,6 +1042,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
               mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, acc0);
             }
+            mma_commit_w(&aempty[ga % TS]);
+          } else if (HF) {
+            // fp16 A hi | lo (16 TMEM columns each) from this slab's A slot, W hi / lo planes
+            // (SW64) from shared memory; corrections first, then the main product
+            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+            const uint32_t ahi = tbase + A_COL + 32 * (ga % TS), alo = ahi + 16;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+              mma_bf16_ts_w(dmain, alo + kk * 8, sw64_desc(bh + kk * 32), idesc, acc0);
+              mma_bf16_ts_w(dmain, ahi + kk * 8, sw64_desc(bl + kk * 32), idesc, 1u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) mma_bf16_ts_w(dmain, ahi + kk * 8, sw64_desc(bh + kk * 32), idesc, 1u);
             mma_commit_w(&aempty[ga % TS]);
           } else {
             // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
@@ -922,12 +1123,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       bulk_wait0();
     }
-  } else if (warp >= XF_WARP0 && warp < EP_WARP0) {
-    // ===================== transform (w2..w5) =====================
-    const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
+  } else if (warp >= XF_WARP0 && warp < EP0) {
+    // ===================== transform (w3..w6; X2: w3..w10, set = alternate K-slabs) ==========
+    const int xset = X2 ? (warp - XF_WARP0) >> 2 : 0;
+    const int t = threadIdx.x - XF_WARP0 * 32 - xset * 128;  // 0..127
     int g = 0, ga = 0;  // ga: A-ring slab counter (the chained conv's slabs skip the transform)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int kb = 0; kb < nkt; ++kb, ++g) {
+        if (X2 && (g & 1) != xset) {  // the other set's slab (HF: ga == g, no chained slabs)
+          ++ga;
+          continue;
+        }
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
         if (CH && kb >= nk) {  // chained conv's weight slab: nothing to transform, but every
@@ -996,7 +1202,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
-        if (!BF) {
+        if (HF) {
+          // thread = tile row r (= TMEM lane): the row's power-of-two scale, pre-activation
+          // folded into the scaling (LeakyReLU(x) 2^s = max(x 2^s, x (a 2^s)) exactly: 2^s is a
+          // power of two), fp16 hi | lo pairs (low half = even k) into this slab's TMEM A slot;
+          // the unscale exponent of (row, slab) goes to the ring the drain reads.  The scale is
+          // taken from max |x| x max(1, a) (>= max |act(x)|; tanh: <= |x|) — the same rule as
+          // the window transform, so both modes produce identical operands.
+          const int quarter = warp & 3;
+          const int r = quarter * 32 + lane;
+          const float4* row = reinterpret_cast<const float4*>(a_hi(s)) + r * 8;
+          const bool pre_tanh = p.pre_act == ACT_TANH;
+          const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+          float x[32];
+          float m = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = row[j ^ (r & 7)];
+            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
+          if (!pre_tanh && pre_s > 1.f) m *= pre_s;
+          const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
+          const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
+          int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+          sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+          const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+          const float scn = sc * pre_s;  // exact
+          uint32_t hv[16], lv[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            float2 t2;
+            if (pre_tanh) {
+              t2 = fmul2s(tanh_ool(x[2 * k]), tanh_ool(x[2 * k + 1]), sc);
+            } else {
+              const float2 p2 = fmul2s(x[2 * k], x[2 * k + 1], sc), n2 = fmul2s(x[2 * k], x[2 * k + 1], scn);
+              t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+            }
+            const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
+            const float2 l = fsub2(t2, __half22float2(h2));
+            const __half2 l2 = __floats2half2_rn(l.x, l.y);
+            hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
+            lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
+          }
+          rsc[(ga % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+          const int a_sl = ga % TS;
+          if (ga >= TS) mbar_wait(&aempty[a_sl], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
+          tc_fence_after();
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 32 * a_sl;
+          tmem_st16(ta, hv);
+          tmem_st16(ta + 16, lv);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          // no proxy fence: nothing was written to shared memory for the async proxy (the A
+          // slot is TMEM; the stage is only read), and the scale byte is read by the drain
+          ++ga;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xform[s]);
+          continue;
+        }
+        if (!BF && !HF) {
           // thread = tile row r (= TMEM lane): SW128 chunk j of row r lives at j ^ (r & 7); hi
           // and lo go to this stage's TMEM A columns (the MMAs read A from TMEM)
           const int quarter = warp & 3;
@@ -1033,11 +1299,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && t == 0) g_tc_trace[2 * 256 + g] = clk();
       }
     }
-  } else if (warp >= EP_WARP0) {
-    // ===================== drain + epilogue (w7..w14) =====================
+  } else if (warp >= EP0) {
+    // ===================== drain + epilogue (w7..w14; X2: w11..w18) =====================
     constexpr int COLS = BN / 2;
     const int quarter = warp & 3;
-    const int half = (warp - EP_WARP0) >> 2;
+    const int half = (warp - EP0) >> 2;
     const int r = quarter * 32 + lane;  // tile row == TMEM lane
     const int col0 = half * COLS;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + col0;
@@ -1045,8 +1311,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
     for (int u = 0; u < COLS; ++u) acc[u] = 0.f;
     int c = 0, tcount = 0;
+    const int taps_w = nk / p.cblocks;  // window mode (HF): chunk kb = (32-channel block, tap)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+      int wq = 0, wu = tcount * p.cblocks;  // HF window: this chunk's tap and window count
       for (int kb = 0; kb < nkt; ++kb) {
         const bool one2 = CH && p.chain_one && kb >= nk;
         const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
@@ -1055,23 +1323,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
         const int b = c % NB;
         mbar_wait(&tfull[b], (c / NB) & 1);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
         tc_fence_after();
+        float f = 1.f;  // HF: this (row, K-slab)'s exact unscale 2^-(s + s_w)
+        if (HF) {
+          uint32_t eb;
+          if (WIN) {
+            eb = rsc[(wu % RS_WIN) * L::WROWS + r + wq * p.a_tap_rows];
+            if (++wq == taps_w) wq = 0, ++wu;
+          } else {
+            eb = rsc[(c % RS_RING) * BM + r];
+          }
+          f = __uint_as_float(eb << 23);
+        }
 #pragma unroll
-        for (int cc = 0; cc < COLS; cc += (COLS >= 32 ? 32 : 16)) {  // main chunk, 32 columns per wait
-          uint32_t v[32];
-          if (COLS >= 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
+        // main chunk, 32 columns per wait (16 for X2: its 96-register budget)
+        constexpr int LDC = (COLS >= 32 && !X2) ? 32 : 16;
+#pragma unroll
+        for (int cc = 0; cc < COLS; cc += LDC) {
+          uint32_t v[LDC];
+          if (LDC == 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
           else tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);
           tmem_wait_ld();
+          // the bias enters with the first chunk (keeps it off the tile-boundary epilogue);
+          // pairs of columns in packed fp32x2 (same round-to-nearest results)
+          if (first) {
 #pragma unroll
-          for (int u = 0; u < (COLS >= 32 ? 32 : 16); ++u)
-            // the bias enters with the first chunk (keeps it off the tile-boundary epilogue)
-            acc[cc + u] = first ? __uint_as_float(v[u]) + sbias[boff + tc.n0 + col0 + cc + u] : acc[cc + u] + __uint_as_float(v[u]);
+            for (int u = 0; u < LDC; ++u) acc[cc + u] = sbias[boff + tc.n0 + col0 + cc + u];
+          }
+#pragma unroll
+          for (int u = 0; u < LDC; u += 2) {
+            if (HF)
+              ffma2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]), f);
+            else
+              fadd2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]));
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP_WARP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
+        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
         ++c;
         if (CH && kb == nk - 1) {
           // the first conv's tile is complete: h = act2(act1(acc)) split hi / lo exactly like
@@ -1125,7 +1416,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
-      const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP_WARP0 && lane == 0;
+      const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP0 && lane == 0;
       if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
       if (p.res) {
         mbar_wait(res_full, tcount & 1);
@@ -1238,10 +1529,10 @@ int num_sms(int dev) {
   return n;
 }
 
-template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0, bool CH = false>
+template <int BN, int STAGES, int CK, bool BF, bool WIN = false, int IOB = 0, bool CH = false, bool HF = false>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& mo, const CUtensorMap& mr,
                const TcParams& p, cudaStream_t st) {
-  using L = TcSmem<BN, STAGES, BF, WIN, IOB>;
+  using L = TcSmem<BN, STAGES, BF, WIN, IOB, HF>;
   static_assert(L::BYTES <= 232448, "shared memory budget");
   // cudaFuncSetAttribute applies to the CURRENT device only: track it per device ordinal.  A
   // concurrent first launch on two threads just sets the (idempotent) attribute twice; a
@@ -1252,14 +1543,14 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
-    if (cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH>,
+    if (cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH, HF>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES) == cudaSuccess)
       attr_mask.fetch_or(bit, std::memory_order_release);
   }
   const int g_sms = num_sms(dev);
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_sms ? n_tiles : g_sms;
-  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH><<<grid, NUM_THREADS, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH, HF><<<grid, Roles<HF && !WIN>::NT, L::BYTES, st>>>(ma, mw, mo, mr, p);
 }
 
 template <int IOB>
@@ -1305,6 +1596,22 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
       case 1: launch_bf16<1>(map_a, map_w, map_out, map_res, p, st); break;
       case 2: launch_bf16<2>(map_a, map_w, map_out, map_res, p, st); break;
       default: launch_bf16<3>(map_a, map_w, map_out, map_res, p, st); break;
+    }
+    return;
+  }
+  if (p.f16) {  // 3xFP16 (HF): fp16 hi / lo planes, per-row power-of-two block scaling
+    if (p.win) {
+      switch (p.BN) {
+        case 32: launch_bn<32, 14, 1, false, true, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+        case 64: launch_bn<64, 7, 1, false, true, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+        default: launch_bn<128, 4, 1, false, true, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+      }
+      return;
+    }
+    switch (p.BN) {
+      case 32: launch_bn<32, 9, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 7, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+      default: launch_bn<128, 4, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;
   }

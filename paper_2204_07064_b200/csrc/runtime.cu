@@ -9,8 +9,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -47,15 +49,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D tensor map (fp32 with 128B swizzle: inner box = 32 floats = 128 bytes; or bf16 with
 // 64B swizzle: inner box = 32 bf16 = 64 bytes).
 CUtensorMap make_map3(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
-                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2, bool bf16 = false) {
+                      uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2, bool bf16 = false,
+                      bool fp16 = false) {
   CUtensorMap m;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {s1_bytes, s2_bytes};
   cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+  CUresult r = encode_fn()(&m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                            const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           (bf16 || fp16) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(SC_ERR_CUDA_BASE, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -95,13 +99,27 @@ bool win_disabled() {
   return e && std::atoi(e) != 0;
 }
 
+// fp32 plans: the fp32-accurate tensor-core split — "f16" (3xFP16, default) or "tf32" (3xTF32,
+// the round-1 form; chained k3 + 1x1 convs always use it).  SC_FP32_SPLIT=tf32 selects it.
+bool split_tf32() {
+  const char* e = std::getenv("SC_FP32_SPLIT");
+  return e && std::string(e) == "tf32";
+}
+
+// 3xFP16 non-window tiles: L2 prefetch distance of the input boxes in 32-channel blocks
+// (SC_PF_DIST, default 2; 0 disables)
+int pf_dist() {
+  const char* e = std::getenv("SC_PF_DIST");
+  return e ? std::max(0, std::atoi(e)) : 2;
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("SC_DISABLE_TC");
   return e && std::atoi(e) != 0;
 }
 
 // Decide whether an op runs on the tensor-core kernel and build its hi/lo weight planes.
-void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<float>& wtc) {
+void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<float>& wtc, bool f16 = false) {
   const ConvOp& op = pg.ops[i];
   if (op.kind == OPK_SUM) {
     d.kernel = KERNEL_SUM;
@@ -136,8 +154,20 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
   d.tap_rows = strided ? 1 : op.tap_step;
   const int64_t Kpad = static_cast<int64_t>(d.taps_view) * d.cin_view_pad;
   const int64_t N = op.nout;
-  // fp32: [2 (hi, lo)][N][Kpad] floats; bf16: [N][Kpad] bf16 (round-to-nearest) packed in floats
-  wtc.assign(d.bf16 ? static_cast<size_t>((N * Kpad + 1) / 2) : static_cast<size_t>(2 * N * Kpad), 0.f);
+  d.f16 = f16 && !d.bf16;
+  // 3xFP16: one power-of-two scale per layer puts max |w| in [2^14, 2^15) (kernels_tc.cu HF)
+  d.f16_sw = 0;
+  if (d.f16) {
+    float wmax = 0.f;
+    for (float w : op.w) wmax = std::max(wmax, std::fabs(w));
+    const int e = wmax > 0.f ? std::ilogb(wmax) : 0;
+    d.f16_sw = std::min(100, std::max(-100, 14 - e));
+  }
+  const float wsc = std::ldexp(1.0f, d.f16_sw);
+  // fp32: [2 (hi, lo)][N][Kpad] floats; bf16: [N][Kpad] bf16 (round-to-nearest) packed in floats;
+  // 3xFP16: [2 (hi, lo)][N][Kpad] fp16 of w x 2^f16_sw (packed two per float slot)
+  wtc.assign(d.bf16 ? static_cast<size_t>((N * Kpad + 1) / 2) : d.f16 ? static_cast<size_t>(N * Kpad)
+                                                                     : static_cast<size_t>(2 * N * Kpad), 0.f);
   uint16_t* wb = reinterpret_cast<uint16_t*>(wtc.data());
   for (int64_t n = 0; n < N; ++n)
     for (int q = 0; q < d.taps_view; ++q)
@@ -154,6 +184,12 @@ void plan_tc(const Program& pg, size_t i, int precision, DevOp& d, std::vector<f
         if (d.bf16) {
           const uint32_t u = __builtin_bit_cast(uint32_t, w);
           wb[o] = static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);  // RN-even
+        } else if (d.f16) {
+          const float ws = w * wsc;  // exact (power of two)
+          const __half h = __float2half_rn(ws);
+          const __half l = __float2half_rn(ws - __half2float(h));
+          wb[o] = __half_as_ushort(h);
+          wb[static_cast<size_t>(N * Kpad) + o] = __half_as_ushort(l);
         } else {
           const float hi = __builtin_bit_cast(float, __builtin_bit_cast(uint32_t, w) & 0xFFFFE000u);
           wtc[o] = hi;
@@ -181,7 +217,11 @@ bool chain_disabled() {
 // intermediate tile never leaves the SM (kernels_tc.cu CH; cfg2's residual blocks: LReLU ->
 // conv K3 -> LReLU -> conv 1x1 + skip).  The 1x1 weights are appended along K of the first
 // conv's packed weights ([2][128][Kpad + 128]), so one weight map serves both GEMMs.
-void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::vector<float>>& wtc) {
+// merge = false: only mark the chain-eligible pairs (DevOp::chain) without touching weights —
+// fp32 plans keep such pairs on the 3xTF32 split even when SC_CHAIN=0, so the two-launch form
+// stays bit-identical to the chained one
+void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::vector<float>>& wtc,
+                 bool merge = true) {
   for (size_t i = 0; i + 1 < pg.ops.size(); ++i) {
     const size_t j = i + 1;
     const ConvOp& a = pg.ops[i];
@@ -203,6 +243,10 @@ void find_chains(const Program& pg, std::vector<DevOp>& dops, std::vector<std::v
       for (const SumIn& si : o.sum_in) other = other || si.buf == a.out_buf;
     }
     if (other) continue;
+    if (!merge) {
+      da.chain = static_cast<int>(j);
+      continue;
+    }
     const size_t N = 128, K1 = static_cast<size_t>(da.taps_view) * da.cin_view_pad, K2 = 128;
     std::vector<float> w;
     if (da.bf16) {  // [N][K] bf16 (packed two per float slot)
@@ -274,6 +318,21 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
   plan->dops.assign(nops, DevOp{});
   std::vector<std::vector<float>> wtc(nops);
   for (size_t i = 0; i < nops; ++i) plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i]);
+  // fp32 plans: every tensor-core op outside a chain-eligible pair takes the 3xFP16 split
+  if (precision == SC_PREC_FP32 && !split_tf32()) {
+    std::vector<uint8_t> chained(nops, 0);
+    {
+      std::vector<DevOp> probe = plan->dops;
+      find_chains(plan->prog, probe, wtc, false);
+      for (size_t i = 0; i < nops; ++i)
+        if (probe[i].chain >= 0) chained[i] = chained[static_cast<size_t>(probe[i].chain)] = 1;
+    }
+    for (size_t i = 0; i < nops; ++i)
+      if (plan->dops[i].kernel == KERNEL_TC && !chained[i]) {
+        plan->dops[i] = DevOp{};
+        plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i], true);
+      }
+  }
   if (!chain_disabled()) find_chains(plan->prog, plan->dops, wtc);
   // PQMF fast form: the factor arrays (S, C, class index as float) follow the op's blob slots
   std::vector<std::vector<float>> pqv(nops);
@@ -343,6 +402,9 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
       if (d.bf16)
         d.map_w = make_map3(d.wtc, Kpad, op.nout, 1, Kpad * 2, static_cast<uint64_t>(op.nout) * Kpad * 2, 32,
                             d.BN, 1, true);
+      else if (d.f16)
+        d.map_w = make_map3(d.wtc, Kpad, op.nout, 2, Kpad * 2, static_cast<uint64_t>(op.nout) * Kpad * 2, 32,
+                            d.BN, 1, false, true);
       else
         d.map_w = make_map3(d.wtc, Kpad, op.nout, 2, Kpad * 4, static_cast<uint64_t>(op.nout) * Kpad * 4, 32,
                             d.BN, 1);
@@ -680,12 +742,16 @@ CallPlan& State::call_plan(int64_t F) {
     p.halo = (d.taps_view - 1) * d.tap_rows;
     // a layer that may run in window mode for some call geometry accumulates in the window
     // order in every mode (bit-identity across partitions); a static property of the layer
-    p.cbmaj = ((d.bf16 || d.BN <= 64) && d.taps_view > 1) ? 1 : 0;
-    p.win = ((d.bf16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
+    p.cbmaj = ((d.bf16 || d.f16 || d.BN <= 64) && d.taps_view > 1) ? 1 : 0;
+    p.win = ((d.bf16 || d.f16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
              !win_disabled() && !(plan->dops[i].chain >= 0 && !d.bf16)) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
-    p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * 4 <= 112 * 1024 &&
+    p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * (d.f16 ? 2 : 4) <=
+                                        (d.f16 ? 56 : 112) * 1024 &&
               op.nout == d.BN) ? 1 : 0;
+    p.f16 = d.f16 ? 1 : 0;
+    p.f16_sw = d.f16_sw;
+    p.pf_dist = pf_dist();
     p.pre_act = c.pre_act;
     p.pre_alpha = c.pre_alpha;
     p.post_act = c.post_act;

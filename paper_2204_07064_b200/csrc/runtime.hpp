@@ -27,6 +27,8 @@ struct DevOp {
   CUtensorMap map_w{};
   int BN = 0;
   bool bf16 = false;
+  bool f16 = false;          // fp32 plan, 3xFP16 split (fp16 hi / lo weight planes)
+  int f16_sw = 0;            // ... weights scaled by 2^f16_sw
   int view_S = 1;            // super-row factor of the input view (conv stride, or 1)
   int cin_view = 0, cin_view_pad = 0, taps_view = 0, tap_rows = 1;
   int chain = -1;            // fp32: index of the K = 1 conv chained into this op's launch

@@ -1,0 +1,5 @@
+export SC_LIB_PATH=exp/libstreamconv_b200.so SC_SKIP_BUILD=1
+SC_TC_TRACE_OP=29 python tools/trace_tc.py 5 fp32 > gpurun_out/trace_hf29.txt 2>&1
+SC_FP32_SPLIT=tf32 SC_TC_TRACE_OP=29 python tools/trace_tc.py 5 fp32 > gpurun_out/trace_tf29.txt 2>&1
+SC_TC_TRACE_OP=2 python tools/trace_tc.py 5 fp32 > gpurun_out/trace_hf2.txt 2>&1
+tail -3 gpurun_out/trace_hf29.txt
