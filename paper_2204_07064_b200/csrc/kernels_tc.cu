@@ -43,7 +43,7 @@ namespace scb {
 
 namespace {
 
-__device__ long long g_tc_trace[12 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
+__device__ long long g_tc_trace[16 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
 
 __device__ __forceinline__ long long clk() { return clock64(); }  // SM cycles (per-SM counter)
 
@@ -65,11 +65,21 @@ constexpr int EP_WARP0 = 7;   // drain/epilogue warps 7..14 (11..18, X2)
 // X2 (3xFP16 non-window tiles): two sets of four transform warps take alternate K-slabs — one
 // set of four (one warp per SM sub-partition) could not split a slab as fast as kind::f16 MMAs
 // consume it (measured ~0.9k cycles per slab vs 384 cycles of MMA)
+// X2 also has its own A-unit producer warp (EP0 + 8), so the input loads run ahead of the W ring.
 template <bool X2> struct Roles {
+  static constexpr int XF0 = X2 ? 4 : XF_WARP0;  // X2: w0 W | w1 MMA | w2 I/O | w3 A units
   static constexpr int NXF = X2 ? 8 : 4;
-  static constexpr int EP0 = XF_WARP0 + NXF;
+  static constexpr int EP0 = XF0 + NXF;
+  static constexpr int AW_WARP = 3;
   static constexpr int NT = (EP0 + 8) * 32;
 };
+
+template <uint32_t N> __device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N> __device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
 
 // packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): same round-to-nearest results as
 // the scalar forms, half the instructions
@@ -96,6 +106,24 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {  // a - b
       "sub.rn.f32x2 R, A, B;\n\tmov.b64 {%0, %1}, R;\n\t}"
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
+}
+
+// 3xFP16 split of a (scaled) pair: hi = t rounded to 11 significant bits in the fp32 domain
+// (integer round-half-away on the magnitude: two ALU ops, no conversion), lo = t - hi (exact),
+// both packed to fp16 pairs.  Two conversions per pair: the conversion pipe bounded the
+// transform when hi was also unpacked back to fp32 (ncu: XU at 126% of peak).  (A Veltkamp
+// split, c t - (c t - t), is folded to t by ptxas.)  hi is exact in fp16 down to 2^-14; below
+// that (< 2^-28 of the row max after scaling) the fp16 rounding of hi adds at most 2^-25
+// absolute — negligible, and a fixed function of the row like the scale.
+__device__ __forceinline__ void split_f16x2(float2 t, uint32_t& h, uint32_t& l) {
+  float2 hi;
+  hi.x = __uint_as_float((__float_as_uint(t.x) + 0x1000u) & 0xFFFFE000u);
+  hi.y = __uint_as_float((__float_as_uint(t.y) + 0x1000u) & 0xFFFFE000u);
+  const float2 lo = fsub2(t, hi);
+  const __half2 h2 = __floats2half2_rn(hi.x, hi.y);
+  const __half2 l2 = __floats2half2_rn(lo.x, lo.y);
+  h = *reinterpret_cast<const uint32_t*>(&h2);
+  l = *reinterpret_cast<const uint32_t*>(&l2);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -266,6 +294,26 @@ __device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, 
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K-slab of the 3xFP16 product (two K = 16 steps, A hi | lo from TMEM): the corrections
+// A_lo W_hi, A_hi W_lo of both steps, then A_hi W_hi — six MMAs under one elected lane.
+__device__ __forceinline__ void mma_f16x3_slab_w(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t bh0, uint64_t bh1,
+                                                 uint64_t bl0, uint64_t bl1, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %9, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%10], %4, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%11], %6, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%11], %4, %8, t;\n\t}" ::"r"(d),
+      "r"(ahi), "r"(alo), "l"(bh0), "l"(bh1), "l"(bl0), "l"(bl1), "r"(0), "r"(idesc), "r"(acc0), "r"(alo + 8),
+      "r"(ahi + 8)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -346,19 +394,24 @@ constexpr uint32_t WREG_H = 56 * 1024;  // 3xFP16 windows: fp16 hi + lo weight p
 // deep enough that the transform never overwrites an entry the drain has not read yet
 // (transform of slab g implies the drain finished slab g - STAGES - NB; see HF below)
 constexpr int RS_RING = 32;
+constexpr int AW_ROWS = 192;  // X2 A units: G x (R + halo) rows of one 32-channel block (24 KB)
 constexpr int RS_WIN = 16;
 template <int BN, int STAGES, bool BF = false, bool WIN = false, int IOB = 0, bool HF = false>
 struct TcSmem {
   static constexpr uint32_t B_TILE = (BF || HF) ? BN * BK * 2 : BN * BK * 4;
-  static constexpr uint32_t STAGE = WIN ? (BF ? B_TILE : 2 * B_TILE) : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
+  // X2 (3xFP16 non-window): the stage ring holds only W hi | lo; the input rows come through a
+  // separate ring of A units (per-slab boxes, or per 32-channel-block windows of every tap)
+  static constexpr bool X2 = HF && !WIN;
+  static constexpr uint32_t STAGE = (WIN || X2) ? (BF ? B_TILE : 2 * B_TILE) : BF ? A_TILE + B_TILE : A_TILE + 2 * B_TILE;
   // window slots: fp32 = A hi + A lo (SW128); bf16 = the raw fp32 rows + their bf16 copy (SW64);
   // 3xFP16 = the raw fp32 rows, converted in place to fp16 hi | lo planes (SW64)
-  static constexpr int AST = WIN ? (BF ? 3 : HF ? 4 : 2) : 0;
+  static constexpr int AST = WIN ? (BF ? 3 : HF ? 4 : 2) : X2 ? 3 : 0;
   // bf16 windows hold 128 + 64 rows when they fit three slots next to the staging tile (narrow
   // tiles, or bf16 input rows: a raw bf16 row is half the size)
   static constexpr bool ABF = BF && (IOB & 1);
   static constexpr int WROWS = (BF && (BN < 128 || ABF)) ? WIN_ROWS_BF : WIN_ROWS;
-  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * ((ABF ? 2 : 4) + 2) : HF ? WROWS * BK * 4 : 2 * WROWS * BK * 4;
+  static constexpr uint32_t WIN_SLOT = BF ? WROWS * BK * ((ABF ? 2 : 4) + 2)
+                                       : X2 ? AW_ROWS * BK * 4 : HF ? WROWS * BK * 4 : 2 * WROWS * BK * 4;
   static constexpr uint32_t STAGING = BM * BN * 4;  // residual-in / output-out tile, 32-col SW128 slabs
   // 3xFP16 BN = 128 windows: a W ring of STAGES K-slab tiles (never resident); BN <= 64: the
   // 56 KB weight region (ring or the whole weight)
@@ -439,7 +492,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
                    const TcParams p) {
   using L = TcSmem<BN, STAGES, BF, WIN, IOB, HF>;
   static_assert(!HF || (!BF && !CH && CK == 1), "3xFP16: fp32 plans, unchained, one K-slab per chunk");
-  constexpr bool X2 = HF && !WIN;
+  constexpr bool X2 = L::X2;
   constexpr int EP0 = Roles<X2>::EP0;
   constexpr int NT = Roles<X2>::NT;
   constexpr bool ABF = BF && (IOB & 1);  // input rows are bf16
@@ -471,8 +524,8 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
   uint8_t* rsc = reinterpret_cast<uint8_t*>(bars) + 1024 + 8192;  // HF: per-row unscale exponents
 
   auto a_hi = [&](int s) { return smem + s * L::STAGE; };
-  auto b_hi = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE); };
-  auto b_lo = [&](int s) { return smem + s * L::STAGE + (WIN ? 0 : A_TILE) + L::B_TILE; };
+  auto b_hi = [&](int s) { return smem + s * L::STAGE + ((WIN || X2) ? 0 : A_TILE); };
+  auto b_lo = [&](int s) { return smem + s * L::STAGE + ((WIN || X2) ? 0 : A_TILE) + L::B_TILE; };
   auto b_bf = [&](int s) { return smem + s * L::STAGE + A_TILE; };
   auto win_hi = [&](int sa) { return wins + sa * L::WIN_SLOT; };
   auto win_lo = [&](int sa) { return wins + sa * L::WIN_SLOT + L::WROWS * BK * 4; };  // fp32: A lo
@@ -535,7 +588,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
     for (int a = 0; a < (L::AST > 0 ? L::AST : 1); ++a) {
       mbar_init(&wa_full[a], 1);
       mbar_init(&wa_ready[a], 4);
-      mbar_init(&wa_empty[a], 1);
+      mbar_init(&wa_empty[a], X2 ? 8 : 1);  // X2: released by all eight transform warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -564,7 +617,532 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (WIN && warp == 0) {
+  // role bodies shared by the X2 and the classic layouts
+  auto role_mma = [&]() {
+      // ===================== MMA issuer (whole warp, one elected lane issues) =====================
+      {
+        const uint32_t tbase = warp_uniform(tmem_base);
+        // c_format F32 | a,b format TF32 (2) or BF16 (1) | N >> 3 | M >> 4
+        const uint32_t fmt = BF ? 1u : HF ? 0u : 2u;  // HF: F16
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                               (static_cast<uint32_t>(BM >> 4) << 24);
+        int g = 0, c = 0, tcount = 0, ga = 0;  // ga: A-ring slab counter (first-conv slabs)
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+          for (int kb = 0; kb < nkt; ++kb, ++g) {
+            const int s = g % STAGES;
+            const int b = c % NB;
+            const bool one2 = CH && p.chain_one && kb >= nk;  // chained GEMM in one accumulator
+            const bool chunk_first = one2 ? kb == nk : (kb % CK) == 0;
+            const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
+            if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+            if (CH && kb >= nk) {
+              // chained GEMM slab: W from the ring, A (h hi / lo of 32 channels) from the slot
+              // the drain wrote; its own chunk accumulator like every first-conv slab
+              const int u = tcount * NK2 + (kb - nk), sl = u % NS2;
+              mbar_wait(&xform[s], (g / STAGES) & 1);
+              mbar_wait(&a2full[sl], (u / NS2) & 1);
+              tc_fence_after();
+              const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+              if (BF) {
+                const uint32_t bb = smem_u32(b_bf(s)), at = tbase + A2_COL + W2 * sl;
+  #pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
+              } else {
+                const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+                const uint32_t ahi = tbase + (SHR ? A_COL + 64 * (ga % TS) : A2_COL + W2 * sl), alo = ahi + 32;
+  #pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                  mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
+                  mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+                }
+  #pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
+              }
+              if (SHR) {
+                mma_commit_w(&aempty[ga % TS]);
+                ++ga;
+              } else {
+                mma_commit_w(&a2empty[sl]);
+              }
+              mma_commit_w(&empty[s]);
+              if (chunk_last) {
+                mma_commit_w(&tfull[b]);
+                ++c;
+              }
+              continue;
+            }
+            mbar_wait(&xform[s], (g / STAGES) & 1);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+            tc_fence_after();
+            const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+            if (BF) {
+              // A (bf16 pairs) from this stage's TMEM columns, W from shared memory
+              const uint32_t bb = smem_u32(b_bf(s));
+              const uint32_t at = tbase + A_COL + 16 * (ga % TS);
+  #pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 8 TMEM columns / 32 bytes of the 64B row
+                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, acc0);
+              }
+              mma_commit_w(&aempty[ga % TS]);
+            } else if (HF) {
+              // fp16 A hi | lo (16 TMEM columns each) from this slab's A slot, W hi / lo planes
+              // (SW64) from shared memory; corrections first, then the main product.  X2: the
+              // transform does not touch the W stage, so wait for its landing here
+              mbar_wait(&full[s], (g / STAGES) & 1);
+              const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+              const uint32_t ahi = tbase + A_COL + 32 * (ga % TS), alo = ahi + 16;
+              mma_f16x3_slab_w(dmain, ahi, alo, sw64_desc(bh), sw64_desc(bh + 32), sw64_desc(bl), sw64_desc(bl + 32), idesc,
+                               chunk_first ? 0u : 1u);
+              mma_commit_w(&aempty[ga % TS]);
+            } else {
+              // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
+              // shared-memory operand traffic is the weight tile (A never re-read from smem).
+              // Corrections first (2^-10 of the signal), then the main product, all into this
+              // chunk's accumulator: the truncating accumulation meets the large terms only in
+              // its last four steps.
+              const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+              const uint32_t ahi = tbase + A_COL + 64 * (ga % TS);
+              const uint32_t alo = ahi + 32;
+              if (!(TC_DBG(p) & 2)) {
+  #pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                  const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                  mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+                  mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
+                }
+              }
+  #pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
+                const uint32_t acc0 = (!chunk_first || kk > 0 || !(TC_DBG(p) & 2)) ? 1u : 0u;
+                mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
+              }
+              mma_commit_w(&aempty[ga % TS]);
+            }
+            ++ga;
+            mma_commit_w(&empty[s]);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
+            if (chunk_last) {
+              mma_commit_w(&tfull[b]);
+              ++c;
+            }
+          }
+        }
+      }
+  };
+  auto role_io = [&]() {
+      // ===================== epilogue I/O (one thread) =====================
+      if (lane == 0) {
+        const int n_tiles_n2 = n_tiles_n;
+        const int out_cols = p.gate ? BN / 2 : BN;
+        int tcount = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+          const TileCoord tc = tile_coord(p, tile, n_tiles_n2, BN);
+          if (p.res) {  // staging is free (previous store read it): bring this tile's residual in
+            const int res_es = OBF ? 2 : 4;  // bytes per residual element (slab = BM x 32 elements)
+            mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * res_es * p.R * p.G);
+            for (int k = 0; k < BN / 32; ++k)
+              tma_load_3d(&tmap_res, res_full, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * res_es),
+                          p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
+            // warm L2 with the next tile's residual: its load is issued only once this tile's
+            // output has left staging, so it must not also pay the DRAM latency
+            if (tile + static_cast<int>(gridDim.x) < n_tiles && !(TC_DBG(p) & 4)) {
+              const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n2, BN);
+              for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
+            }
+          }
+          mbar_wait(stg_written, tcount & 1);
+          const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
+          for (int k = 0; k < (out_cols + 31) / 32; ++k)
+            tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
+                         tc.i0, tc.s0);
+          bulk_commit();
+          bulk_wait_read0();
+          mbar_arrive(stg_free);
+        }
+        bulk_wait0();
+      }
+  };
+  auto role_drain = [&]() {
+      // ===================== drain + epilogue (w7..w14; X2: w11..w18) =====================
+      constexpr int COLS = BN / 2;
+      const int quarter = warp & 3;
+      const int half = (warp - EP0) >> 2;
+      const int r = quarter * 32 + lane;  // tile row == TMEM lane
+      const int col0 = half * COLS;
+      const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + col0;
+      float acc[COLS];
+  #pragma unroll
+      for (int u = 0; u < COLS; ++u) acc[u] = 0.f;
+      int c = 0, tcount = 0;
+      int cb_ = 0, cph = 0;  // HF: chunk buffer c % NB and its phase (c / NB) & 1, kept incrementally
+      const int taps_w = nk / p.cblocks;  // window mode (HF): chunk kb = (32-channel block, tap)
+      const uint8_t* rs_row = rsc + r;     // HF: this row's scale bytes
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+        const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+        int wq = 0, wu = tcount * p.cblocks;  // HF window: this chunk's tap and window count
+        if (HF) {  // the bias is the accumulator's start value (one load per tile, not per chunk)
+  #pragma unroll
+          for (int u = 0; u < COLS; u += 4) {
+            const float4 bv = *reinterpret_cast<const float4*>(sbias + tc.n0 + col0 + u);
+            acc[u] = bv.x, acc[u + 1] = bv.y, acc[u + 2] = bv.z, acc[u + 3] = bv.w;
+          }
+        }
+#pragma unroll 1
+        for (int kb = 0; kb < nkt; ++kb) {
+          const bool one2 = CH && p.chain_one && kb >= nk;
+          const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
+          if (!chunk_last) continue;
+          const bool first = (kb / CK) == 0 || kb == (one2 ? nkt - 1 : nk);  // + the chained conv's first chunk
+          const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
+          const int b = HF ? cb_ : c % NB;
+          mbar_wait(&tfull[b], HF ? cph : (c / NB) & 1);
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
+          tc_fence_after();
+          float f = 1.f;  // HF: this (row, K-slab)'s exact unscale 2^-(s + s_w)
+          if (HF) {
+            uint32_t eb;
+            if (WIN) {
+              eb = rs_row[(wu % RS_WIN) * L::WROWS + wq * p.a_tap_rows];
+              if (++wq == taps_w) wq = 0, ++wu;
+            } else {
+              eb = rs_row[(c % RS_RING) * BM];
+            }
+            f = __uint_as_float(eb << 23);
+            if (++cb_ == NB) cb_ = 0, cph ^= 1;
+          }
+  #pragma unroll
+          // main chunk, 32 columns per wait (16 for X2: its 96-register budget)
+          constexpr int LDC = COLS >= 32 ? 32 : 16;
+  #pragma unroll
+          for (int cc = 0; cc < COLS; cc += LDC) {
+            uint32_t v[LDC];
+            if (LDC == 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
+            else tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);
+            tmem_wait_ld();
+            // the bias enters with the first chunk (keeps it off the tile-boundary epilogue);
+            // pairs of columns in packed fp32x2 (same round-to-nearest results)
+            if (!HF && first) {
+  #pragma unroll
+              for (int u = 0; u < LDC; ++u) acc[cc + u] = sbias[boff + tc.n0 + col0 + cc + u];
+            }
+  #pragma unroll
+            for (int u = 0; u < LDC; u += 2) {
+              if (HF)
+                ffma2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]), f);
+              else
+                fadd2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]));
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
+          ++c;
+          if (CH && kb == nk - 1) {
+            // the first conv's tile is complete: h = act2(act1(acc)) split hi / lo exactly like
+            // the transform would split it after a round trip through HBM (bit-identical to the
+            // two-launch form), into the chained GEMM's A slots — this half's 64 columns are its
+            // K-slabs 2 half and 2 half + 1
+            const float s1 = slope_of(p.mid_act1, p.mid_alpha1), s2 = slope_of(p.mid_act2, p.mid_alpha2);
+  #pragma unroll
+            for (int j = 0; j < COLS / 32; ++j) {
+              const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u % NS2;
+              const int pa = tcount * (nk + NK2) + nk + half * (COLS / 32) + j;  // A-ring position (SHR)
+              if (SHR) mbar_wait(&aempty[pa % TS], ((pa / TS) + 1) & 1);  // MMAs of position pa - TS done
+              else if (u >= NS2) mbar_wait(&a2empty[sl], ((u / NS2) + 1) & 1);  // MMAs of use u - NS2 done
+              tc_fence_after();
+              const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                  (SHR ? A_COL + 64 * (pa % TS) : A2_COL + W2 * sl);
+              if (BF) {
+                // the two-launch form rounds h to bf16 once in the first conv's epilogue when the
+                // intermediate buffer holds bf16 (p.mid_bf), then applies act2 and rounds again
+                uint32_t pk[16];
+  #pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  float v0 = act_lin(acc[32 * j + 2 * e], s1), v1 = act_lin(acc[32 * j + 2 * e + 1], s1);
+                  if (p.mid_bf) {
+                    v0 = __bfloat162float(__float2bfloat16_rn(v0));
+                    v1 = __bfloat162float(__float2bfloat16_rn(v1));
+                  }
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(act_lin(v0, s2), act_lin(v1, s2));
+                  pk[e] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                tmem_st16(ta, pk);
+              }
+  #pragma unroll
+              for (int h16 = 0; h16 < (BF ? 0 : 2); ++h16) {
+                uint32_t hv[16], lv[16];
+  #pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const float a = act_lin(act_lin(acc[32 * j + 16 * h16 + e], s1), s2);
+                  const float hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+                  hv[e] = __float_as_uint(hi);
+                  lv[e] = __float_as_uint(a - hi);
+                }
+                tmem_st16(ta + 16 * h16, hv);
+                tmem_st16(ta + 32 + 16 * h16, lv);
+              }
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&a2full[sl]);
+            }
+          }
+        }
+        // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
+        const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP0 && lane == 0;
+        if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
+        if (p.res) {
+          mbar_wait(res_full, tcount & 1);
+        } else if (tcount > 0) {
+          mbar_wait(stg_free, (tcount - 1) & 1);
+        }
+        if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
+        __nv_bfloat16* stgb = reinterpret_cast<__nv_bfloat16*>(stg);  // bf16 buffers (bf16 plans)
+        if (p.gate) {
+  #pragma unroll
+          for (int u = 0; u < COLS; u += 2) {
+            const float o = gate_ool(acc[u], acc[u + 1]);
+            if (OBF)
+              stgb[stg_off_b(r, (col0 + u) >> 1)] = __float2bfloat16_rn(o);
+            else
+              stg[stg_off(r, (col0 + u) >> 1)] = o;
+          }
+        } else if (OBF && p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
+          // bf16 output (and bf16 residual: a plan never mixes the two on one op), 4 columns per access
+          const float ps = slope_of(p.post_act, p.post_alpha);
+          const float rs = slope_of(p.res_act, p.res_alpha);
+          const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
+          auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
+  #pragma unroll
+          for (int u = 0; u < COLS; u += 4) {
+            uint2* dst = reinterpret_cast<uint2*>(stgb + stg_off_b(r, col0 + u));
+            float o[4] = {lin(acc[u], ps, pmax), lin(acc[u + 1], ps, pmax), lin(acc[u + 2], ps, pmax),
+                          lin(acc[u + 3], ps, pmax)};
+            if (p.res) {
+              const uint2 rv = *dst;
+              const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.x));
+              const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.y));
+              const float rr[4] = {r0.x, r0.y, r1.x, r1.y};
+  #pragma unroll
+              for (int k = 0; k < 4; ++k) o[k] += rid ? rr[k] : lin(rr[k], rs, rmax);
+            }
+            __nv_bfloat162 a2 = __floats2bfloat162_rn(o[0], o[1]), b2 = __floats2bfloat162_rn(o[2], o[3]);
+            uint2 w;
+            w.x = *reinterpret_cast<uint32_t*>(&a2);
+            w.y = *reinterpret_cast<uint32_t*>(&b2);
+            *dst = w;
+          }
+        } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
+          // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
+          const float ps = slope_of(p.post_act, p.post_alpha);
+          const float rs = slope_of(p.res_act, p.res_alpha);
+          const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
+          auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
+  #pragma unroll
+          for (int u = 0; u < COLS; u += 4) {
+            float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
+            float4 o;
+            o.x = lin(acc[u], ps, pmax);
+            o.y = lin(acc[u + 1], ps, pmax);
+            o.z = lin(acc[u + 2], ps, pmax);
+            o.w = lin(acc[u + 3], ps, pmax);
+            if (p.res) {
+              float4 rv = *dst;
+              if (!rid) rv = make_float4(lin(rv.x, rs, rmax), lin(rv.y, rs, rmax), lin(rv.z, rs, rmax), lin(rv.w, rs, rmax));
+              o.x += rv.x;
+              o.y += rv.y;
+              o.z += rv.z;
+              o.w += rv.w;
+            }
+            *dst = o;
+          }
+        } else {  // tanh epilogues (unused by the five configs): out-of-line math
+  #pragma unroll
+          for (int u = 0; u < COLS; ++u) {
+            const int n = tc.n0 + col0 + u;
+            float o = act_apply(acc[u], p.post_act, p.post_alpha);
+            if (OBF) {
+              __nv_bfloat16* dst = stgb + stg_off_b(r, col0 + u);
+              if (p.res) o += act_apply(__bfloat162float(*dst), p.res_act, p.res_alpha);
+              *dst = __float2bfloat16_rn(o);
+            } else {
+              float* dst = stg + stg_off(r, col0 + u);
+              if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
+              *dst = o;
+            }
+          }
+        }
+        if (trace) g_tc_trace[6 * 256 + 4 * tcount + 2] = clk();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stg_written);
+        if (trace) g_tc_trace[6 * 256 + 4 * tcount + 3] = clk();
+      }
+  };
+  if constexpr (X2) {
+    // X2: warpgroup-aligned roles with register reallocation (setmaxnreg): WG0 = W producer,
+    // MMA issuer, epilogue I/O, A-unit producer (48 registers); WG1-2 = the two transform
+    // sets (88); WG3-4 = drain + epilogue (128: a 64-column fp32 accumulator per thread)
+    if (warp < 4) {
+      reg_dealloc<48>();
+      if (warp == 0) {
+        // ===================== W producer, X2: weight hi | lo tiles into the stage ring ==========
+        const int taps = nk / p.cblocks;
+        int g = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+          const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+          int cb = 0, q = 0;
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
+            const int kw = (q * p.cblocks + cb) * BK;
+            mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
+            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
+            tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
+            if (p.cbmaj) {
+              if (++q == taps) q = 0, ++cb;
+            } else if (++cb == p.cblocks) {
+              cb = 0, ++q;
+            }
+          }
+        }
+      } else if (warp == 1) {
+        role_mma();
+      } else if (warp == IO_WARP) {
+        role_io();
+      } else {
+        // ===================== A-unit producer, X2 =====================
+        // A unit = the rows of one K-slab (p.awin = 0), or of one 32-channel block for every tap:
+        // G streams x (R + halo) rows (p.awin = 1: the taps' boxes overlap, so one load serves them).
+        // Limited only by the unit ring (released by the transform), not by the W ring.
+        const int taps = nk / p.cblocks;
+        const uint32_t abytes = static_cast<uint32_t>(BK * 4 * (p.R + (p.awin ? p.halo : 0)) * p.G);
+        int u = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+          const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+          int cb = 0, q = 0;
+          for (int kb = 0; kb < nk; ++kb) {
+            if (!p.awin || q == 0) {
+              const int sa = u % L::AST;
+              if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
+              mbar_expect_tx_w(&wa_full[sa], abytes);
+              tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK,
+                            p.a_row0 + tc.i0 + (p.awin ? 0 : q * p.a_tap_rows), tc.s0);
+              ++u;
+            }
+            if (p.cbmaj) {
+              if (++q == taps) q = 0, ++cb;
+            } else if (++cb == p.cblocks) {
+              cb = 0, ++q;
+            }
+          }
+        }
+      }
+    } else if (warp < Roles<X2>::EP0) {
+      reg_dealloc<88>();
+      // ===================== transform, X2 (w3..w10: two sets of four, alternate K-slabs) =====
+      // thread = tile row r (= TMEM lane): the row's power-of-two scale, pre-activation folded
+      // into the scaling (LeakyReLU(x) 2^s = max(x 2^s, x (a 2^s)) exactly: 2^s is a power of
+      // two), fp16 hi | lo pairs (low half = even k) into this slab's TMEM A slot; the unscale
+      // exponent of (row, slab) goes to the ring the drain reads.  The scale is taken from
+      // max |x| x max(1, a) (>= max |act(x)|; tanh: <= |x|) — the same rule as the window
+      // transform, so both modes produce identical operands.  Tile row r = (stream r / R, frame
+      // r % R); its input row sits at r in a per-slab unit, or at (r / R)(R + halo) + r % R + q
+      // tap_rows in a block window (p.awin).  Every transform warp releases a unit after its last
+      // slab (having seen it land: a release can then never run ahead into the slot's previous use).
+      const int xset = (warp - Roles<X2>::XF0) >> 2;
+      const int quarter = warp & 3;
+      const int r = quarter * 32 + lane;
+      const int taps = nk / p.cblocks;
+      // rows past G x R (a partial tile) are never stored: read any in-slot row for them
+      const int srow = (!p.awin || r >= p.G * p.R) ? (r < p.G * p.R ? r : 0) : (r / p.R) * (p.R + p.halo) + r % p.R;
+      const bool pre_tanh = p.pre_act == ACT_TANH;
+      const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+      const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
+      const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
+      int g = 0, u = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int q = 0;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int sa = u % L::AST;
+          const bool unit_last = !p.awin || q == taps - 1;
+          if ((g & 1) == xset) {
+            const int s = g % STAGES;
+            const int ga = g;
+            mbar_wait(&wa_full[sa], (u / L::AST) & 1);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3) g_tc_trace[1 * 256 + g] = clk();
+            const int wr = srow + (p.awin ? q * p.a_tap_rows : 0);
+            const float4* row = reinterpret_cast<const float4*>(win_hi(sa)) + wr * 8;
+            float x[32];
+            float m = 0.f;
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = row[j ^ (wr & 7)];
+              x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+              m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            }
+            // this warp's reads of the unit are done once m (a function of every loaded value)
+            // exists: release the slot only then — an arrive right after the LDS instructions
+            // could let the next TMA fill overwrite rows still in flight to the registers
+            if (unit_last) {
+              m = __shfl_sync(0xffffffffu, m, lane);  // consume m before the arrive
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&wa_empty[sa]);
+            }
+            if (!pre_tanh && pre_s > 1.f) m *= pre_s;
+            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+            const float scn = sc * pre_s;  // exact
+            uint32_t hv[16], lv[16];
+  #pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              float2 t2;
+              if (pre_tanh) {
+                t2 = fmul2s(tanh_ool(x[2 * k]), tanh_ool(x[2 * k + 1]), sc);
+              } else {
+                const float2 p2 = fmul2s(x[2 * k], x[2 * k + 1], sc), n2 = fmul2s(x[2 * k], x[2 * k + 1], scn);
+                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+              }
+              split_f16x2(t2, hv[k], lv[k]);
+            }
+            rsc[(ga % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+            const bool trc = (TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3;
+            if (trc) g_tc_trace[4 * 256 + g] = clk();
+            const int a_sl = ga % TS;
+            if (ga >= TS) mbar_wait(&aempty[a_sl], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
+            if (trc) g_tc_trace[12 * 256 + g] = clk();
+            tc_fence_after();
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 32 * a_sl;
+            tmem_st16(ta, hv);
+            tmem_st16(ta + 16, lv);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (trc) g_tc_trace[13 * 256 + g] = clk();
+            tc_fence_before();
+            // no proxy fence: nothing was written to shared memory for the async proxy (the A
+            // slot is TMEM; the unit is only read), and the scale byte is read by the drain
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xform[s]);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3) g_tc_trace[2 * 256 + g] = clk();
+          } else if (unit_last) {  // the other set's slab ends the unit: release it once it landed
+            mbar_wait(&wa_full[sa], (u / L::AST) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wa_empty[sa]);
+          }
+          if (unit_last) ++u;
+          if (++q == taps) q = 0;
+        }
+      }
+    } else {
+      reg_alloc<128>();
+      role_drain();
+    }
+  } else if (WIN && warp == 0) {
     // ===================== TMA producer, window mode =====================
     // per 32-channel block: the 128 + halo input rows once (window slot), then per tap the
     // weight hi / lo tiles into the W ring
@@ -832,11 +1410,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
                 t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
                                   : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
               }
-              const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
-              const float2 l = fsub2(t2, __half22float2(h2));
-              const __half2 l2 = __floats2half2_rn(l.x, l.y);
-              hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
-              lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
+              split_f16x2(t2, hv[k], lv[k]);
             }
             uint4* hr = reinterpret_cast<uint4*>(win_hi(sa)) + t * 4;
             uint4* lr = reinterpret_cast<uint4*>(win_lo16(sa)) + t * 4;
@@ -869,11 +1443,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
                 t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
                                   : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
               }
-              const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
-              const float2 l = fsub2(t2, __half22float2(h2));
-              const __half2 l2 = __floats2half2_rn(l.x, l.y);
-              hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
-              lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
+              split_f16x2(t2, hv[k], lv[k]);
             }
             const int po = we * 8 + (((je >> 1) ^ ((we >> 1) & 3)) << 1) + (je & 1);  // uint2 units
             reinterpret_cast<uint2*>(win_hi(sa))[po] = make_uint2(hv[0], hv[1]);
@@ -956,17 +1526,6 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
             tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
             tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
           }
-          // 3xFP16 (cbmaj order): at the first tap of a 32-channel block, warm L2 with the A box
-          // of the block p.pf_dist blocks ahead (the next tile's when past this tile's last):
-          // the ring's few stages cannot cover the input's DRAM latency at the kind::f16 rate
-          if (HF && p.pf_dist > 0 && q == 0 && lane == 0) {
-            int cbn = cb + p.pf_dist, tn = tile;
-            while (cbn >= p.cblocks) cbn -= p.cblocks, tn += gridDim.x;
-            if (tn < n_tiles) {
-              const TileCoord tq = tile_coord(p, tn, n_tiles_n, BN);
-              tma_prefetch_3d(&tmap_a, p.a_c0 + cbn * BK, p.a_row0 + tq.i0, tq.s0);
-            }
-          }
           if (p.cbmaj) {
             if (++q == taps) q = 0, ++cb;
           } else if (++cb == p.cblocks) {
@@ -976,164 +1535,15 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (whole warp, one elected lane issues) =====================
-    {
-      const uint32_t tbase = warp_uniform(tmem_base);
-      // c_format F32 | a,b format TF32 (2) or BF16 (1) | N >> 3 | M >> 4
-      const uint32_t fmt = BF ? 1u : HF ? 0u : 2u;  // HF: F16
-      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                             (static_cast<uint32_t>(BM >> 4) << 24);
-      int g = 0, c = 0, tcount = 0, ga = 0;  // ga: A-ring slab counter (first-conv slabs)
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        for (int kb = 0; kb < nkt; ++kb, ++g) {
-          const int s = g % STAGES;
-          const int b = c % NB;
-          const bool one2 = CH && p.chain_one && kb >= nk;  // chained GEMM in one accumulator
-          const bool chunk_first = one2 ? kb == nk : (kb % CK) == 0;
-          const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
-          if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
-          if (CH && kb >= nk) {
-            // chained GEMM slab: W from the ring, A (h hi / lo of 32 channels) from the slot
-            // the drain wrote; its own chunk accumulator like every first-conv slab
-            const int u = tcount * NK2 + (kb - nk), sl = u % NS2;
-            mbar_wait(&xform[s], (g / STAGES) & 1);
-            mbar_wait(&a2full[sl], (u / NS2) & 1);
-            tc_fence_after();
-            const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-            if (BF) {
-              const uint32_t bb = smem_u32(b_bf(s)), at = tbase + A2_COL + W2 * sl;
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)
-                mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
-            } else {
-              const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-              const uint32_t ahi = tbase + (SHR ? A_COL + 64 * (ga % TS) : A2_COL + W2 * sl), alo = ahi + 32;
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk) {
-                mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, (!chunk_first || kk > 0) ? 1u : 0u);
-                mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
-              }
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, 1u);
-            }
-            if (SHR) {
-              mma_commit_w(&aempty[ga % TS]);
-              ++ga;
-            } else {
-              mma_commit_w(&a2empty[sl]);
-            }
-            mma_commit_w(&empty[s]);
-            if (chunk_last) {
-              mma_commit_w(&tfull[b]);
-              ++c;
-            }
-            continue;
-          }
-          mbar_wait(&xform[s], (g / STAGES) & 1);
-          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
-          tc_fence_after();
-          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-          if (BF) {
-            // A (bf16 pairs) from this stage's TMEM columns, W from shared memory
-            const uint32_t bb = smem_u32(b_bf(s));
-            const uint32_t at = tbase + A_COL + 16 * (ga % TS);
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {  // 16 bf16 = 8 TMEM columns / 32 bytes of the 64B row
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc, acc0);
-            }
-            mma_commit_w(&aempty[ga % TS]);
-          } else if (HF) {
-            // fp16 A hi | lo (16 TMEM columns each) from this slab's A slot, W hi / lo planes
-            // (SW64) from shared memory; corrections first, then the main product
-            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-            const uint32_t ahi = tbase + A_COL + 32 * (ga % TS), alo = ahi + 16;
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16_ts_w(dmain, alo + kk * 8, sw64_desc(bh + kk * 32), idesc, acc0);
-              mma_bf16_ts_w(dmain, ahi + kk * 8, sw64_desc(bl + kk * 32), idesc, 1u);
-            }
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) mma_bf16_ts_w(dmain, ahi + kk * 8, sw64_desc(bh + kk * 32), idesc, 1u);
-            mma_commit_w(&aempty[ga % TS]);
-          } else {
-            // A hi / lo from this stage's TMEM columns, W hi / lo from shared memory: the only
-            // shared-memory operand traffic is the weight tile (A never re-read from smem).
-            // Corrections first (2^-10 of the signal), then the main product, all into this
-            // chunk's accumulator: the truncating accumulation meets the large terms only in
-            // its last four steps.
-            const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
-            const uint32_t ahi = tbase + A_COL + 64 * (ga % TS);
-            const uint32_t alo = ahi + 32;
-            if (!(TC_DBG(p) & 2)) {
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk) {
-                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-                mma_tf32_ts_w(dmain, alo + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
-                mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bl + kk * 32), idesc, 1u);
-              }
-            }
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {  // 8 tf32 = 8 TMEM columns / 32 B of the row
-              const uint32_t acc0 = (!chunk_first || kk > 0 || !(TC_DBG(p) & 2)) ? 1u : 0u;
-              mma_tf32_ts_w(dmain, ahi + kk * 8, sw128_desc(bh + kk * 32), idesc, acc0);
-            }
-            mma_commit_w(&aempty[ga % TS]);
-          }
-          ++ga;
-          mma_commit_w(&empty[s]);
-          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
-          if (chunk_last) {
-            mma_commit_w(&tfull[b]);
-            ++c;
-          }
-        }
-      }
-    }
+    role_mma();
   } else if (warp == IO_WARP) {
-    // ===================== epilogue I/O (one thread) =====================
-    if (lane == 0) {
-      const int n_tiles_n2 = n_tiles_n;
-      const int out_cols = p.gate ? BN / 2 : BN;
-      int tcount = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        const TileCoord tc = tile_coord(p, tile, n_tiles_n2, BN);
-        if (p.res) {  // staging is free (previous store read it): bring this tile's residual in
-          const int res_es = OBF ? 2 : 4;  // bytes per residual element (slab = BM x 32 elements)
-          mbar_expect_tx(res_full, static_cast<uint32_t>(BN / 32) * 32u * res_es * p.R * p.G);
-          for (int k = 0; k < BN / 32; ++k)
-            tma_load_3d(&tmap_res, res_full, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * res_es),
-                        p.res_off + tc.n0 + 32 * k, tc.i0, tc.s0);
-          // warm L2 with the next tile's residual: its load is issued only once this tile's
-          // output has left staging, so it must not also pay the DRAM latency
-          if (tile + static_cast<int>(gridDim.x) < n_tiles && !(TC_DBG(p) & 4)) {
-            const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n2, BN);
-            for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
-          }
-        }
-        mbar_wait(stg_written, tcount & 1);
-        const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
-        for (int k = 0; k < (out_cols + 31) / 32; ++k)
-          tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
-                       tc.i0, tc.s0);
-        bulk_commit();
-        bulk_wait_read0();
-        mbar_arrive(stg_free);
-      }
-      bulk_wait0();
-    }
+    role_io();
   } else if (warp >= XF_WARP0 && warp < EP0) {
-    // ===================== transform (w3..w6; X2: w3..w10, set = alternate K-slabs) ==========
-    const int xset = X2 ? (warp - XF_WARP0) >> 2 : 0;
-    const int t = threadIdx.x - XF_WARP0 * 32 - xset * 128;  // 0..127
+    // ===================== transform (w3..w6) =====================
+    const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
     int g = 0, ga = 0;  // ga: A-ring slab counter (the chained conv's slabs skip the transform)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int kb = 0; kb < nkt; ++kb, ++g) {
-        if (X2 && (g & 1) != xset) {  // the other set's slab (HF: ga == g, no chained slabs)
-          ++ga;
-          continue;
-        }
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
         if (CH && kb >= nk) {  // chained conv's weight slab: nothing to transform, but every
@@ -1202,67 +1612,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
-        if (HF) {
-          // thread = tile row r (= TMEM lane): the row's power-of-two scale, pre-activation
-          // folded into the scaling (LeakyReLU(x) 2^s = max(x 2^s, x (a 2^s)) exactly: 2^s is a
-          // power of two), fp16 hi | lo pairs (low half = even k) into this slab's TMEM A slot;
-          // the unscale exponent of (row, slab) goes to the ring the drain reads.  The scale is
-          // taken from max |x| x max(1, a) (>= max |act(x)|; tanh: <= |x|) — the same rule as
-          // the window transform, so both modes produce identical operands.
-          const int quarter = warp & 3;
-          const int r = quarter * 32 + lane;
-          const float4* row = reinterpret_cast<const float4*>(a_hi(s)) + r * 8;
-          const bool pre_tanh = p.pre_act == ACT_TANH;
-          const float pre_s = slope_of(p.pre_act, p.pre_alpha);
-          float x[32];
-          float m = 0.f;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 v = row[j ^ (r & 7)];
-            x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-          }
-          if (!pre_tanh && pre_s > 1.f) m *= pre_s;
-          const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
-          const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
-          int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
-          sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
-          const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
-          const float scn = sc * pre_s;  // exact
-          uint32_t hv[16], lv[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            float2 t2;
-            if (pre_tanh) {
-              t2 = fmul2s(tanh_ool(x[2 * k]), tanh_ool(x[2 * k + 1]), sc);
-            } else {
-              const float2 p2 = fmul2s(x[2 * k], x[2 * k + 1], sc), n2 = fmul2s(x[2 * k], x[2 * k + 1], scn);
-              t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
-            }
-            const __half2 h2 = __floats2half2_rn(t2.x, t2.y);
-            const float2 l = fsub2(t2, __half22float2(h2));
-            const __half2 l2 = __floats2half2_rn(l.x, l.y);
-            hv[k] = *reinterpret_cast<const uint32_t*>(&h2);
-            lv[k] = *reinterpret_cast<const uint32_t*>(&l2);
-          }
-          rsc[(ga % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);
-          const int a_sl = ga % TS;
-          if (ga >= TS) mbar_wait(&aempty[a_sl], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
-          tc_fence_after();
-          const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 32 * a_sl;
-          tmem_st16(ta, hv);
-          tmem_st16(ta + 16, lv);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-          // no proxy fence: nothing was written to shared memory for the async proxy (the A
-          // slot is TMEM; the stage is only read), and the scale byte is read by the drain
-          ++ga;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&xform[s]);
-          continue;
-        }
-        if (!BF && !HF) {
+        if (!BF) {
           // thread = tile row r (= TMEM lane): SW128 chunk j of row r lives at j ^ (r & 7); hi
           // and lo go to this stage's TMEM A columns (the MMAs read A from TMEM)
           const int quarter = warp & 3;
@@ -1300,211 +1650,7 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
       }
     }
   } else if (warp >= EP0) {
-    // ===================== drain + epilogue (w7..w14; X2: w11..w18) =====================
-    constexpr int COLS = BN / 2;
-    const int quarter = warp & 3;
-    const int half = (warp - EP0) >> 2;
-    const int r = quarter * 32 + lane;  // tile row == TMEM lane
-    const int col0 = half * COLS;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + col0;
-    float acc[COLS];
-#pragma unroll
-    for (int u = 0; u < COLS; ++u) acc[u] = 0.f;
-    int c = 0, tcount = 0;
-    const int taps_w = nk / p.cblocks;  // window mode (HF): chunk kb = (32-channel block, tap)
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-      const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
-      int wq = 0, wu = tcount * p.cblocks;  // HF window: this chunk's tap and window count
-      for (int kb = 0; kb < nkt; ++kb) {
-        const bool one2 = CH && p.chain_one && kb >= nk;
-        const bool chunk_last = one2 ? kb == nkt - 1 : ((kb % CK) == CK - 1) || (kb == nk - 1) || kb >= nk;
-        if (!chunk_last) continue;
-        const bool first = (kb / CK) == 0 || kb == (one2 ? nkt - 1 : nk);  // + the chained conv's first chunk
-        const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
-        const int b = c % NB;
-        mbar_wait(&tfull[b], (c / NB) & 1);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
-        tc_fence_after();
-        float f = 1.f;  // HF: this (row, K-slab)'s exact unscale 2^-(s + s_w)
-        if (HF) {
-          uint32_t eb;
-          if (WIN) {
-            eb = rsc[(wu % RS_WIN) * L::WROWS + r + wq * p.a_tap_rows];
-            if (++wq == taps_w) wq = 0, ++wu;
-          } else {
-            eb = rsc[(c % RS_RING) * BM + r];
-          }
-          f = __uint_as_float(eb << 23);
-        }
-#pragma unroll
-        // main chunk, 32 columns per wait (16 for X2: its 96-register budget)
-        constexpr int LDC = (COLS >= 32 && !X2) ? 32 : 16;
-#pragma unroll
-        for (int cc = 0; cc < COLS; cc += LDC) {
-          uint32_t v[LDC];
-          if (LDC == 32) tmem_ld32(lane_base + static_cast<uint32_t>(b * BN + cc), v);
-          else tmem_ld16(lane_base + static_cast<uint32_t>(b * BN + cc), v);
-          tmem_wait_ld();
-          // the bias enters with the first chunk (keeps it off the tile-boundary epilogue);
-          // pairs of columns in packed fp32x2 (same round-to-nearest results)
-          if (first) {
-#pragma unroll
-            for (int u = 0; u < LDC; ++u) acc[cc + u] = sbias[boff + tc.n0 + col0 + cc + u];
-          }
-#pragma unroll
-          for (int u = 0; u < LDC; u += 2) {
-            if (HF)
-              ffma2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]), f);
-            else
-              fadd2_acc(acc[cc + u], acc[cc + u + 1], __uint_as_float(v[u]), __uint_as_float(v[u + 1]));
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[b]);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[10 * 256 + c] = clk();
-        ++c;
-        if (CH && kb == nk - 1) {
-          // the first conv's tile is complete: h = act2(act1(acc)) split hi / lo exactly like
-          // the transform would split it after a round trip through HBM (bit-identical to the
-          // two-launch form), into the chained GEMM's A slots — this half's 64 columns are its
-          // K-slabs 2 half and 2 half + 1
-          const float s1 = slope_of(p.mid_act1, p.mid_alpha1), s2 = slope_of(p.mid_act2, p.mid_alpha2);
-#pragma unroll
-          for (int j = 0; j < COLS / 32; ++j) {
-            const int u = tcount * NK2 + half * (COLS / 32) + j, sl = u % NS2;
-            const int pa = tcount * (nk + NK2) + nk + half * (COLS / 32) + j;  // A-ring position (SHR)
-            if (SHR) mbar_wait(&aempty[pa % TS], ((pa / TS) + 1) & 1);  // MMAs of position pa - TS done
-            else if (u >= NS2) mbar_wait(&a2empty[sl], ((u / NS2) + 1) & 1);  // MMAs of use u - NS2 done
-            tc_fence_after();
-            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                (SHR ? A_COL + 64 * (pa % TS) : A2_COL + W2 * sl);
-            if (BF) {
-              // the two-launch form rounds h to bf16 once in the first conv's epilogue when the
-              // intermediate buffer holds bf16 (p.mid_bf), then applies act2 and rounds again
-              uint32_t pk[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                float v0 = act_lin(acc[32 * j + 2 * e], s1), v1 = act_lin(acc[32 * j + 2 * e + 1], s1);
-                if (p.mid_bf) {
-                  v0 = __bfloat162float(__float2bfloat16_rn(v0));
-                  v1 = __bfloat162float(__float2bfloat16_rn(v1));
-                }
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(act_lin(v0, s2), act_lin(v1, s2));
-                pk[e] = *reinterpret_cast<uint32_t*>(&b2);
-              }
-              tmem_st16(ta, pk);
-            }
-#pragma unroll
-            for (int h16 = 0; h16 < (BF ? 0 : 2); ++h16) {
-              uint32_t hv[16], lv[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const float a = act_lin(act_lin(acc[32 * j + 16 * h16 + e], s1), s2);
-                const float hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-                hv[e] = __float_as_uint(hi);
-                lv[e] = __float_as_uint(a - hi);
-              }
-              tmem_st16(ta + 16 * h16, hv);
-              tmem_st16(ta + 32 + 16 * h16, lv);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&a2full[sl]);
-          }
-        }
-      }
-      // ---- epilogue: bias/act/gate (+ residual from staging) -> staging (TMA-stored by w14)
-      const bool trace = (TC_DBG(p) & 32) && blockIdx.x == 0 && tcount < 64 && warp == EP0 && lane == 0;
-      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 0] = clk();
-      if (p.res) {
-        mbar_wait(res_full, tcount & 1);
-      } else if (tcount > 0) {
-        mbar_wait(stg_free, (tcount - 1) & 1);
-      }
-      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 1] = clk();
-      __nv_bfloat16* stgb = reinterpret_cast<__nv_bfloat16*>(stg);  // bf16 buffers (bf16 plans)
-      if (p.gate) {
-#pragma unroll
-        for (int u = 0; u < COLS; u += 2) {
-          const float o = gate_ool(acc[u], acc[u + 1]);
-          if (OBF)
-            stgb[stg_off_b(r, (col0 + u) >> 1)] = __float2bfloat16_rn(o);
-          else
-            stg[stg_off(r, (col0 + u) >> 1)] = o;
-        }
-      } else if (OBF && p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
-        // bf16 output (and bf16 residual: a plan never mixes the two on one op), 4 columns per access
-        const float ps = slope_of(p.post_act, p.post_alpha);
-        const float rs = slope_of(p.res_act, p.res_alpha);
-        const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
-        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
-#pragma unroll
-        for (int u = 0; u < COLS; u += 4) {
-          uint2* dst = reinterpret_cast<uint2*>(stgb + stg_off_b(r, col0 + u));
-          float o[4] = {lin(acc[u], ps, pmax), lin(acc[u + 1], ps, pmax), lin(acc[u + 2], ps, pmax),
-                        lin(acc[u + 3], ps, pmax)};
-          if (p.res) {
-            const uint2 rv = *dst;
-            const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.x));
-            const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.y));
-            const float rr[4] = {r0.x, r0.y, r1.x, r1.y};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) o[k] += rid ? rr[k] : lin(rr[k], rs, rmax);
-          }
-          __nv_bfloat162 a2 = __floats2bfloat162_rn(o[0], o[1]), b2 = __floats2bfloat162_rn(o[2], o[3]);
-          uint2 w;
-          w.x = *reinterpret_cast<uint32_t*>(&a2);
-          w.y = *reinterpret_cast<uint32_t*>(&b2);
-          *dst = w;
-        }
-      } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
-        // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
-        const float ps = slope_of(p.post_act, p.post_alpha);
-        const float rs = slope_of(p.res_act, p.res_alpha);
-        const bool pmax = ps <= 1.f, rmax = rs <= 1.f, rid = rs == 1.f;
-        auto lin = [](float v, float sl, bool mx) { return mx ? fmaxf(v, v * sl) : fminf(v, v * sl); };
-#pragma unroll
-        for (int u = 0; u < COLS; u += 4) {
-          float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
-          float4 o;
-          o.x = lin(acc[u], ps, pmax);
-          o.y = lin(acc[u + 1], ps, pmax);
-          o.z = lin(acc[u + 2], ps, pmax);
-          o.w = lin(acc[u + 3], ps, pmax);
-          if (p.res) {
-            float4 rv = *dst;
-            if (!rid) rv = make_float4(lin(rv.x, rs, rmax), lin(rv.y, rs, rmax), lin(rv.z, rs, rmax), lin(rv.w, rs, rmax));
-            o.x += rv.x;
-            o.y += rv.y;
-            o.z += rv.z;
-            o.w += rv.w;
-          }
-          *dst = o;
-        }
-      } else {  // tanh epilogues (unused by the five configs): out-of-line math
-#pragma unroll
-        for (int u = 0; u < COLS; ++u) {
-          const int n = tc.n0 + col0 + u;
-          float o = act_apply(acc[u], p.post_act, p.post_alpha);
-          if (OBF) {
-            __nv_bfloat16* dst = stgb + stg_off_b(r, col0 + u);
-            if (p.res) o += act_apply(__bfloat162float(*dst), p.res_act, p.res_alpha);
-            *dst = __float2bfloat16_rn(o);
-          } else {
-            float* dst = stg + stg_off(r, col0 + u);
-            if (p.res) o += act_apply(*dst, p.res_act, p.res_alpha);
-            *dst = o;
-          }
-        }
-      }
-      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 2] = clk();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(stg_written);
-      if (trace) g_tc_trace[6 * 256 + 4 * tcount + 3] = clk();
-    }
+    role_drain();
   }
 
   tc_fence_before();
@@ -1583,7 +1729,7 @@ void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUten
 
 }  // namespace
 
-void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 12 * 256); }
+void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 16 * 256); }
 
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {
@@ -1609,8 +1755,8 @@ void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CU
       return;
     }
     switch (p.BN) {
-      case 32: launch_bn<32, 9, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
-      case 64: launch_bn<64, 7, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 32: launch_bn<32, 16, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
+      case 64: launch_bn<64, 12, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
       default: launch_bn<128, 4, 1, false, false, 0, false, true>(map_a, map_w, map_out, map_res, p, st); break;
     }
     return;

@@ -47,7 +47,8 @@ struct TcParams {
   int bf16;   // 1: bf16 operands (kind::f16), fp32 accumulate; 0: fp32-accurate (3xTF32 or 3xFP16)
   int f16;    // fp32 plans: 1 = 3xFP16 (fp16 hi / lo, per-row power-of-two scaling), 0 = 3xTF32
   int f16_sw; // 3xFP16: the layer's weight scale exponent (weights were multiplied by 2^f16_sw)
-  int pf_dist; // 3xFP16 non-window tiles: L2 prefetch distance of the A boxes, in 32-channel blocks (0: off)
+  int awin;    // 3xFP16 non-window tiles: one A load per 32-channel block serves every tap (box
+               // of G streams x (R + halo) rows <= 192), else one A box per K-slab
   int a_bf, r_bf, o_bf;  // bf16 plans: input / residual / output buffer holds bf16 (else fp32)
   int cbmaj;  // 1: K-slabs channel-block major (layers that may run in window mode), else tap major
   // chained 1x1 conv (fp32, BN = 128, one N tile): the drain turns the first conv's tile

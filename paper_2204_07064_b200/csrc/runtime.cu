@@ -106,11 +106,10 @@ bool split_tf32() {
   return e && std::string(e) == "tf32";
 }
 
-// 3xFP16 non-window tiles: L2 prefetch distance of the input boxes in 32-channel blocks
-// (SC_PF_DIST, default 2; 0 disables)
-int pf_dist() {
-  const char* e = std::getenv("SC_PF_DIST");
-  return e ? std::max(0, std::atoi(e)) : 2;
+// 3xFP16 non-window tiles: per-block input windows (TcParams::awin); SC_AWIN=0 disables
+bool awin_disabled() {
+  const char* e = std::getenv("SC_AWIN");
+  return e && e[0] == '0';
 }
 
 bool tc_disabled() {
@@ -751,7 +750,7 @@ CallPlan& State::call_plan(int64_t F) {
               op.nout == d.BN) ? 1 : 0;
     p.f16 = d.f16 ? 1 : 0;
     p.f16_sw = d.f16_sw;
-    p.pf_dist = pf_dist();
+    p.awin = (d.f16 && !p.win && p.cbmaj && d.taps_view > 1 && (p.R + p.halo) * p.G <= 192 && !awin_disabled()) ? 1 : 0;
     p.pre_act = c.pre_act;
     p.pre_alpha = c.pre_alpha;
     p.post_act = c.post_act;
@@ -784,7 +783,7 @@ CallPlan& State::call_plan(int64_t F) {
     // word (4-byte) offsets into the buffers: a bf16 buffer packs two elements per word
     cp->tc[i].map_a = make_map3(cp->base[op.in_buf] + base_off * plan->fw(op.in_buf), bufC_view, rows_view, streams,
                                 bufC_view * aes, static_cast<uint64_t>(buf_sstride[op.in_buf]) * 4, 32,
-                                static_cast<uint32_t>(p.R + (p.win ? p.halo : 0)), static_cast<uint32_t>(p.G), a_bf);
+                                static_cast<uint32_t>(p.R + ((p.win || p.awin) ? p.halo : 0)), static_cast<uint32_t>(p.G), a_bf);
     // output rows start at the cache end; rows >= t_out and streams >= n_streams are clipped by TMA
     cp->tc[i].map_out = make_map3(c.out + cache[op.out_buf] * plan->fw(op.out_buf), static_cast<uint64_t>(c.out_rstride),
                                   static_cast<uint64_t>(t_out), streams, static_cast<uint64_t>(c.out_rstride) * oes,
