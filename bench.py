@@ -81,11 +81,21 @@ def peaks():
         d = json.loads(t.read_text())
         pk["tf32"] = d.get("tf32_tflops")
         pk["tf32_sus"] = d.get("tf32_tflops_sustained", pk["tf32"])
+        pk["f16"] = d.get("f16_tflops")
+        pk["f16_sus"] = d.get("f16_tflops_sustained", pk["f16"])
     return pk
 
 
-def fp32_path_ceiling(pk, sustained=False):
-    """(TFLOP/s, source) of the 3xTF32 path's tensor ceiling in algorithmic FLOPs."""
+def fp32_path_ceiling(pk, sustained=False, split="tf32"):
+    """(TFLOP/s, source) of the fp32-accurate path's tensor ceiling in algorithmic FLOPs: three
+    MMAs per fp32 product — kind::tf32 (3xTF32, "[tc]" launches) or kind::f16 (3xFP16,
+    "[tc-3xf16]" launches, the default split)."""
+    if split == "f16":
+        f = pk.get("f16_sus") if sustained else pk.get("f16")
+        if f:
+            return f / 3.0, "measured f16 (profiles/tf32_peak.json: kind::f16 TS N128) / 3"
+        bf = pk["bf16_sus"] if sustained else pk["bf16"]
+        return bf / 3.0, "bf16 dense / 3 (f16 unmeasured)"
     tf = pk["tf32_sus"] if sustained else pk["tf32"]
     if tf:
         return tf / 3.0, "measured tf32 (profiles/tf32_peak.json) / 3"
@@ -410,8 +420,8 @@ def main():
         ois = [int(k) for k in dom_name.split()[0][2:].split("+")]
         flops = 2.0 * sum(op_macs[oi] for oi in ois) * frames * streams
         achieved = flops / (dom_ms / 1e3) / 1e12
-        if args.precision == "fp32" and "[tc]" in dom_name:
-            ceil, csrc = fp32_path_ceiling(pk)
+        if args.precision == "fp32" and ("[tc]" in dom_name or "[tc-3xf16]" in dom_name):
+            ceil, csrc = fp32_path_ceiling(pk, split="f16" if "[tc-3xf16]" in dom_name else "tf32")
         else:
             ceil, csrc = pk["bf16"], "bf16 dense (burst; MEASURED_PEAKS.json)"
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
@@ -420,7 +430,8 @@ def main():
                 "peak_source": f"{pk['src']} bf16 dense (burst; MEASURED_PEAKS.json)",
                 "path_ceiling": ceil, "frac_of_path_ceiling": achieved / ceil,
                 "path_ceiling_source": csrc,
-                "path_ceiling_note": "3xTF32 = 3 kind::tf32 MMAs per fp32 product"
+                "path_ceiling_note": ("3xFP16 = 3 kind::f16 MMAs per fp32 product (per-row power-of-two block scaling)"
+                                      if "[tc-3xf16]" in dom_name else "3xTF32 = 3 kind::tf32 MMAs per fp32 product")
                 if args.precision == "fp32" else "bf16 kind::f16 MMA",
                 "flops_per_launch": flops}
         tfile = ROOT / "profiles" / "traffic.json"
@@ -434,7 +445,8 @@ def main():
     step_roof_ms = max(total_flops / (pk["bf16_sus"] * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
     # the same bound with this precision's tensor ceiling (3xTF32: P_TF32 / 3, sustained)
     if args.precision == "fp32":
-        path_tf, path_src = fp32_path_ceiling(pk, sustained=True)
+        path_tf, path_src = fp32_path_ceiling(pk, sustained=True,
+                                              split="tf32" if os.environ.get("SC_FP32_SPLIT") == "tf32" else "f16")
     else:
         path_tf, path_src = pk["bf16_sus"], "bf16 dense sustained (MEASURED_PEAKS.json)"
     step_path_ms = max(total_flops / (path_tf * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3

@@ -616,6 +616,12 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: everything above (barriers, TMEM, bias, tensor-map prefetch)
+  // touches only this launch's constants, so it overlaps the previous kernel's tail; the
+  // activations it wrote are read only after its grid has completed.  The next launch may start
+  // its own prologue as this grid's CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // role bodies shared by the X2 and the classic layouts
   auto role_mma = [&]() {
@@ -1663,6 +1669,15 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
   }
 }
 
+// programmatic dependent launch of the tensor-core convs (SC_PDL=0 disables)
+bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("SC_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
+
 // SM count per device ordinal (plans may live on different GPUs of one process)
 std::atomic<int> g_num_sms[64];
 
@@ -1696,7 +1711,17 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   const int g_sms = num_sms(dev);
   const int n_tiles = p.m_tiles * ((p.nout + BN - 1) / BN);
   const int grid = n_tiles < g_sms ? n_tiles : g_sms;
-  conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH, HF><<<grid, Roles<HF && !WIN>::NT, L::BYTES, st>>>(ma, mw, mo, mr, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Roles<HF && !WIN>::NT);
+  cfg.dynamicSmemBytes = L::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, STAGES, CK, BF, WIN, IOB, CH, HF>, ma, mw, mo, mr, p);
 }
 
 template <int IOB>

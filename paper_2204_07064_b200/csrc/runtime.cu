@@ -112,6 +112,11 @@ bool awin_disabled() {
   return e && e[0] == '0';
 }
 
+bool small_bn_disabled() {
+  const char* e = std::getenv("SC_SMALL_BN");
+  return e && e[0] == '0';
+}
+
 bool tc_disabled() {
   const char* e = std::getenv("SC_DISABLE_TC");
   return e && std::atoi(e) != 0;
@@ -731,6 +736,23 @@ CallPlan& State::call_plan(int64_t F) {
       p.tiles_per_stream = 1;
       p.m_tiles = (streams + p.G - 1) / p.G;
     }
+    // few output tiles (deep layers at small stream counts, e.g. 1 frame x 2048 streams): halve
+    // the N tile until the grid covers the SMs.  The K order does not depend on BN, so results
+    // are bit-identical to the full-width tile (buffer-partition / stream-count invariance).
+    if (!c.gate && plan->dops[i].chain < 0 && !small_bn_disabled()) {
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+      while (p.BN > 32 && static_cast<int64_t>(p.m_tiles) * ((c.nout + p.BN - 1) / p.BN) < sms &&
+             c.nout % (p.BN / 2) == 0)
+        p.BN /= 2;
+    }
+    if (p.BN != d.BN) {  // this call's weight boxes: BN rows
+      const uint64_t Kpad = static_cast<uint64_t>(d.taps_view) * d.cin_view_pad + d.k_chain;
+      const int es = (d.bf16 || d.f16) ? 2 : 4;
+      cp->tc[i].map_w = make_map3(d.wtc, Kpad, op.nout, d.bf16 ? 1 : 2, Kpad * es,
+                                  static_cast<uint64_t>(op.nout) * Kpad * es, 32, p.BN, 1, d.bf16, d.f16);
+      cp->tc[i].own_w = true;
+    }
     p.cblocks = d.cin_view_pad / 32;
     p.n_kblocks = d.taps_view * p.cblocks;
     p.a_c0 = S > 1 ? 0 : op.in_off;
@@ -745,9 +767,9 @@ CallPlan& State::call_plan(int64_t F) {
     p.win = ((d.bf16 || d.f16 || d.BN <= 64) && p.G == 1 && d.taps_view > 1 && p.R + p.halo <= ((d.bf16 && (d.BN < 128 || plan->buf_bf16[op.in_buf])) ? 192 : 144) &&
              !win_disabled() && !(plan->dops[i].chain >= 0 && !d.bf16)) ? 1 : 0;
     // ... and the whole weight (hi + lo, every K-slab) resident when it fits 112 KB
-    p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * d.BN * 32 * (d.f16 ? 2 : 4) <=
+    p.wres = (p.win && !d.bf16 && static_cast<int64_t>(d.taps_view) * (d.cin_view_pad / 32) * 2 * p.BN * 32 * (d.f16 ? 2 : 4) <=
                                         (d.f16 ? 56 : 112) * 1024 &&
-              op.nout == d.BN) ? 1 : 0;
+              op.nout == p.BN) ? 1 : 0;
     p.f16 = d.f16 ? 1 : 0;
     p.f16_sw = d.f16_sw;
     p.awin = (d.f16 && !p.win && p.cbmaj && d.taps_view > 1 && (p.R + p.halo) * p.G <= 192 && !awin_disabled()) ? 1 : 0;
@@ -1009,7 +1031,7 @@ std::string State::launch_name(int64_t F, int i) {
         return "op" + std::to_string(j) + "+" + std::to_string(jc) + " " + op.name + " + " +
                plan->prog.ops[jc].name + (plan->dops[j].bf16 ? " [tc-bf16]" : " [tc]");
       return "op" + std::to_string(j) + " " + op.name + " [" +
-             (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : "tc")
+             (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : d.f16 ? "tc-3xf16" : "tc")
               : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";
     }
   }
@@ -1030,7 +1052,7 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     if (cp.t_out[i] == 0) continue;
     if (plan->dops[i].kernel == KERNEL_TC) {
       const TcLaunch& t = cp.tc[i];
-      launch_conv_tc(t.map_a, plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
+      launch_conv_tc(t.map_a, t.own_w ? t.map_w : plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
     } else if (plan->dops[i].kernel == KERNEL_SUM) {
       launch_sum(sum_params(i, cp), s);
     } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {

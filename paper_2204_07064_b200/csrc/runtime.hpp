@@ -65,6 +65,8 @@ struct GraphEntry {
 
 struct TcLaunch {
   CUtensorMap map_a{};
+  CUtensorMap map_w{};   // this call's weight map when its N tile differs from the plan's (own_w)
+  bool own_w = false;
   CUtensorMap map_out{};
   CUtensorMap map_res{};
   TcParams p{};

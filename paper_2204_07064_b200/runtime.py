@@ -228,7 +228,7 @@ class StreamState:
         return n.value
 
     def launch_names(self, frames: int):
-        """Names of the launches one call of `frames` enqueues ("op<i> <op> [tc|tc-bf16|simt|pqmf]")."""
+        """Names of the launches one call of `frames` enqueues ("op<i> <op> [tc|tc-3xf16|tc-bf16|simt|pqmf]"; tc = 3xTF32, tc-3xf16 = 3xFP16)."""
         return [lib().sc_launch_name(self._h, frames, i).decode() for i in range(self.launches(frames))]
 
     def profile(self, x, y, frames: int, steps: int = 3, stream=None):
