@@ -33,9 +33,16 @@ struct PqmfParams {
   float post_alpha;
 };
 
+// The bank's coefficients, passed by value (kernel-parameter / constant bank):
+//   analysis : S[A][B] | Cm[M][B] | bias[M]        (256 + 512 + 16 floats)
+//   synthesis: R[classes][M] | s[Q][M] | bias[1]   (<= 512 + 256 + 1 floats)
+struct PqmfCoef {
+  float c[800];  // with PqmfParams under the classic 4 KB parameter bank (larger params go through LDC)
+};
+
 // kind 1 = analysis (A = 8, B = 32), 2 = synthesis (Q = 16, canonical classes, P in {1, 2});
 // 16 bands.
 bool pqmf_fast_shape(int kind, int bands, int A_or_Q, int B_or_classes, int period = 0, int mirror = 0);
-void launch_pqmf(int kind, const PqmfParams& p, cudaStream_t st);
+void launch_pqmf(int kind, const PqmfParams& p, const PqmfCoef& k, cudaStream_t st);
 
 }  // namespace scb

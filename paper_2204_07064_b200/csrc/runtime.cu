@@ -357,6 +357,22 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
       d.kernel = KERNEL_PQMF_SYN;
       d.pq_classes = op.pq_B;
     }
+    // coefficients by value for the kernels' parameter bank: analysis S | Cm | bias[M],
+    // synthesis R | s | bias[0] (kernels_pqmf.hpp PqmfCoef)
+    d.pq_k.assign(sizeof(PqmfCoef) / sizeof(float), 0.f);
+    if (op.pq_S.size() + op.pq_C.size() + op.bias.size() > d.pq_k.size()) {
+      d.kernel = KERNEL_SIMT;
+      continue;
+    }
+    if (op.pqmf == 1) {
+      std::copy(op.pq_S.begin(), op.pq_S.end(), d.pq_k.begin());
+      std::copy(op.pq_C.begin(), op.pq_C.end(), d.pq_k.begin() + op.pq_S.size());
+      std::copy(op.bias.begin(), op.bias.end(), d.pq_k.begin() + op.pq_S.size() + op.pq_C.size());
+    } else {
+      std::copy(op.pq_C.begin(), op.pq_C.end(), d.pq_k.begin());
+      std::copy(op.pq_S.begin(), op.pq_S.end(), d.pq_k.begin() + op.pq_C.size());
+      if (!op.bias.empty()) d.pq_k[op.pq_C.size() + op.pq_S.size()] = op.bias[0];
+    }
     auto& v = pqv[i];
     const size_t nS = round_up(static_cast<int64_t>(op.pq_S.size()), 64);
     const size_t nC = round_up(static_cast<int64_t>(op.pq_C.size()), 64);
@@ -1056,7 +1072,8 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     } else if (plan->dops[i].kernel == KERNEL_SUM) {
       launch_sum(sum_params(i, cp), s);
     } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {
-      launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_params(i, cp), s);
+      launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_params(i, cp),
+                  *reinterpret_cast<const PqmfCoef*>(plan->dops[i].pq_k.data()), s);
     } else {
       launch_conv_simt(conv_params(i, cp), s);
     }

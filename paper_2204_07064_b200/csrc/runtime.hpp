@@ -39,6 +39,7 @@ struct DevOp {
   float* pq_C = nullptr;
   float* pq_idx = nullptr;
   int pq_classes = 0;
+  std::vector<float> pq_k;   // the bank's coefficients for the kernel-parameter bank (PqmfCoef)
 };
 
 struct Plan {
