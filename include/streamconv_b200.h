@@ -160,6 +160,12 @@ SC_API int sc_state_reset(sc_state* state, const int32_t* stream_ids, int32_t n_
 SC_API int sc_state_device_bytes(const sc_state* state, int64_t* bytes);
 /* Resident cache bytes per stream (<= sc_plan_state_bytes: skip delays share conv caches). */
 SC_API int sc_state_cache_bytes(const sc_state* state, int64_t* bytes_per_stream);
+/* Debug: with SC_REDZONE=1 in the environment at sc_state_create, every stream's strip and
+ * every buffer is followed by guard bytes holding a fill pattern; this counts the guard bytes
+ * that were overwritten since (out-of-bounds device writes).  *violations = -1 when the state
+ * has no red zones.  Synchronous (waits for the device).  No reference counterpart: a memcheck
+ * substitute (compute-sanitizer is unavailable on the GPU pool). */
+SC_API int sc_state_redzone_check(sc_state* state, int64_t* violations);
 
 /* Replaces: process_buffer for every stream of `state` at once.
  * d_in  : [n_streams][in_channels][frames]  fp32 device

@@ -138,6 +138,7 @@ _SIGS = {
     "sc_state_reset": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
     "sc_state_device_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_state_cache_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "sc_state_redzone_check": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "sc_process": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sc_process_host_wait": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -375,6 +375,13 @@ int sc_state_device_bytes(const sc_state* state, int64_t* bytes) {
   });
 }
 
+int sc_state_redzone_check(sc_state* state, int64_t* violations) {
+  return guard([&] {
+    need(state && violations, "null argument");
+    *violations = state->s->redzone_check();
+  });
+}
+
 int sc_state_cache_bytes(const sc_state* state, int64_t* bytes) {
   return guard([&] {
     need(state && bytes, "null argument");
@@ -442,6 +449,15 @@ const char* sc_launch_name(const sc_state* state, int64_t frames, int32_t i) {
   });
   (void)st;
   return name.c_str();
+}
+
+// tests only: the state's device allocation (red-zone checker self-test)
+SC_API int sc_debug_state_mem(sc_state* state, void** ptr, int64_t* bytes) {
+  return guard([&] {
+    need(state && ptr && bytes, "null argument");
+    *ptr = state->s->mem;
+    *bytes = state->s->mem_bytes;
+  });
 }
 
 // experiments only: timestamps written by the TC kernel when SC_TC_DEBUG has bit 32

@@ -574,22 +574,34 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
     const char* e = std::getenv("SC_STRIP_K");
     st->strip_k = st->phase_mode ? 1 : std::max(1, e ? std::atoi(e) : (big ? 4 : 1));
   }
+  {
+    const char* e = std::getenv("SC_REDZONE");
+    if (e && e[0] != '0') {
+      st->rz_stream = 64;
+      st->rz_gap = 4096;
+    }
+  }
   std::vector<int64_t> off;
   for (;;) {
     int64_t total = 0;
     off.clear();
     st->buf_sstride.clear();
+    st->rz_used.clear();
     st->cache_bytes_per_stream = 0;
     for (size_t i = 0; i < pg.bufs.size(); ++i) {
       const BufferSpec& b = pg.bufs[i];
       // a call may deliver up to (F + ratio) input samples' worth of frames (phase bursts)
       const int64_t T = ((max_frames + pg.ratio) * b.rate.num + b.rate.den - 1) / b.rate.den;
-      const int64_t sstride = round_up((st->cache[i] + st->strip_k * T + b.tail) * plan->fw(i), 32);
+      const int64_t used = (st->cache[i] + st->strip_k * T + b.tail) * plan->fw(i);
+      const int64_t sstride = round_up(used + st->rz_stream, 32);
       st->buf_sstride.push_back(sstride);
+      st->rz_used.push_back(used);
+      total += st->rz_gap;
       off.push_back(total);
       total += round_up(sstride * streams, 64);
       st->cache_bytes_per_stream += st->cache[i] * plan->fw(i) * 4;
     }
+    total += st->rz_gap;
     st->mem_bytes = total * 4;
     const cudaError_t e = cudaMalloc(&st->mem, std::max<int64_t>(st->mem_bytes, 256));
     if (e == cudaSuccess) break;
@@ -599,6 +611,10 @@ std::unique_ptr<State> make_state(const Plan* plan, int streams, int64_t max_fra
   }
   ck(cudaMemset(st->mem, 0, std::max<int64_t>(st->mem_bytes, 256)), "cudaMemset(state)");
   for (size_t i = 0; i < pg.bufs.size(); ++i) st->buf_base.push_back(st->mem + off[i]);
+  if (st->rz_stream > 0) {
+    st->redzone_fill(nullptr);
+    ck(cudaDeviceSynchronize(), "redzone fill");
+  }
   // reset table: buffers with a cache
   std::vector<BufDesc> desc;
   int64_t ritems = 0;
@@ -1333,12 +1349,50 @@ void State::advance(int64_t F, const CallPlan& cp) {
   E += cp.egress_T;
 }
 
+constexpr unsigned char kRedzoneByte = 0xA5;
+
+void State::redzone_fill(cudaStream_t s) {
+  for (size_t i = 0; i < buf_base.size(); ++i) {
+    ck(cudaMemsetAsync(buf_base[i] - rz_gap, kRedzoneByte, rz_gap * 4, s), "redzone gap");
+    ck(cudaMemset2DAsync(buf_base[i] + rz_used[i], buf_sstride[i] * 4, kRedzoneByte,
+                         (buf_sstride[i] - rz_used[i]) * 4, streams, s), "redzone stream");
+  }
+  ck(cudaMemsetAsync(mem + mem_bytes / 4 - rz_gap, kRedzoneByte, rz_gap * 4, s), "redzone tail");
+}
+
+// guard bytes that no longer hold the fill pattern (-1: red zones disabled); synchronous
+int64_t State::redzone_check() {
+  if (rz_stream == 0) return -1;
+  DeviceScope g(plan->device);
+  ck(cudaDeviceSynchronize(), "redzone check");
+  int64_t bad = 0;
+  auto count = [&](const std::vector<unsigned char>& v) {
+    for (unsigned char c : v) bad += c != kRedzoneByte;
+  };
+  std::vector<unsigned char> h;
+  for (size_t i = 0; i < buf_base.size(); ++i) {
+    h.assign(rz_gap * 4, 0);
+    ck(cudaMemcpy(h.data(), buf_base[i] - rz_gap, h.size(), cudaMemcpyDeviceToHost), "redzone read");
+    count(h);
+    const int64_t w = (buf_sstride[i] - rz_used[i]) * 4;
+    h.assign(w * streams, 0);
+    ck(cudaMemcpy2D(h.data(), w, buf_base[i] + rz_used[i], buf_sstride[i] * 4, w, streams,
+                    cudaMemcpyDeviceToHost), "redzone read");
+    count(h);
+  }
+  h.assign(rz_gap * 4, 0);
+  ck(cudaMemcpy(h.data(), mem + mem_bytes / 4 - rz_gap, h.size(), cudaMemcpyDeviceToHost), "redzone read");
+  count(h);
+  return bad;
+}
+
 void State::reset(const int* ids, int n_ids, cudaStream_t s) {
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
   if (!ids) {
     ck(cudaMemsetAsync(mem, 0, mem_bytes, s), "cudaMemsetAsync");
+    if (rz_stream > 0) redzone_fill(s);
     std::fill(N.begin(), N.end(), 0);
     std::fill(pos.begin(), pos.end(), 0);
     E = 0;

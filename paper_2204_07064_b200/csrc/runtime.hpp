@@ -102,6 +102,14 @@ struct State {
   int64_t max_frames = 0;
   float* mem = nullptr;
   int64_t mem_bytes = 0;
+  // red zones (SC_REDZONE=1; compute-sanitizer is unavailable on the GPU pool): guard floats
+  // after each stream's strip and between buffers, filled with a byte pattern at creation and
+  // after a full reset; redzone_check() counts the guard bytes a kernel overwrote.
+  int64_t rz_stream = 0;                 // guard floats at the end of every stream's region
+  int64_t rz_gap = 0;                    // guard floats before each buffer and after the last
+  std::vector<int64_t> rz_used;          // per buffer: used floats per stream (before the guard)
+  void redzone_fill(cudaStream_t s);
+  int64_t redzone_check();
   int64_t cache_bytes_per_stream = 0;
   std::vector<float*> buf_base;
   std::vector<int64_t> buf_sstride;

@@ -249,6 +249,12 @@ class StreamState:
         check(lib().sc_state_device_bytes(self._h, C.byref(r)))
         return r.value
 
+    def redzone_violations(self) -> int:
+        """Guard bytes overwritten since creation / full reset (-1: created without SC_REDZONE=1)."""
+        r = C.c_int64()
+        check(lib().sc_state_redzone_check(self._h, C.byref(r)))
+        return r.value
+
     @property
     def cache_bytes(self) -> int:
         r = C.c_int64()
