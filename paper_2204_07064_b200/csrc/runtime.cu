@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -993,6 +994,26 @@ SumParams State::sum_params(size_t i, const CallPlan& cp) const {
   return p;
 }
 
+// NVTX ranges (SC_NVTX=1): one per process call, and one per launch in eager mode (graph
+// replays have no host-side launches to mark) — layer names as in sc_launch_name
+bool nvtx_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SC_NVTX");
+    return e && e[0] != '0';
+  }();
+  return on;
+}
+
+struct NvtxRange {
+  bool on;
+  NvtxRange(bool enabled, const std::string& name) : on(enabled) {
+    if (on) nvtxRangePushA(name.c_str());
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+
 IngestArgs State::ingest_args(const float* in, const CallPlan& cp) const {
   const Program& pg = plan->prog;
   IngestArgs a{};
@@ -1082,6 +1103,7 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
   if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
     if (cp.t_out[i] == 0) continue;
+    NvtxRange op_range(ev == nullptr && nvtx_enabled() && !capturing, "op" + std::to_string(i) + " " + plan->prog.ops[i].name);
     if (plan->dops[i].kernel == KERNEL_TC) {
       const TcLaunch& t = cp.tc[i];
       launch_conv_tc(t.map_a, t.own_w ? t.map_w : plan->dops[i].map_w, t.map_out, t.map_res, t.p, s);
@@ -1151,6 +1173,7 @@ void State::profile(const float* in, float* out, int64_t F, int steps, float* ms
 void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
   check_frames(F);
   if (!in || !out) fail(SC_ERR_INVALID_ARGUMENT, "null I/O pointer");
+  NvtxRange call_range(nvtx_enabled(), "sc_process F=" + std::to_string(F) + " streams=" + std::to_string(streams));
   int prev = 0;
   ck(cudaGetDevice(&prev), "cudaGetDevice");
   ck(cudaSetDevice(plan->device), "cudaSetDevice");
@@ -1202,7 +1225,9 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         ck(cudaGraphExecKernelNodeSetParams(g.exec, g.egress_node, &kp), "ExecKernelNodeSetParams");
       } else {
         ck(cudaStreamBeginCapture(capture_stream, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+        capturing = true;
         enqueue(in, out, cp, capture_stream, nullptr);
+        capturing = false;
         cudaError_t le = cudaGetLastError();
         cudaGraph_t graph = nullptr;
         cudaError_t ee = cudaStreamEndCapture(capture_stream, &graph);

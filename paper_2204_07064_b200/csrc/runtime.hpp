@@ -105,6 +105,7 @@ struct State {
   // red zones (SC_REDZONE=1; compute-sanitizer is unavailable on the GPU pool): guard floats
   // after each stream's strip and between buffers, filled with a byte pattern at creation and
   // after a full reset; redzone_check() counts the guard bytes a kernel overwrote.
+  bool capturing = false;                // enqueue() is recording a CUDA graph
   int64_t rz_stream = 0;                 // guard floats at the end of every stream's region
   int64_t rz_gap = 0;                    // guard floats before each buffer and after the last
   std::vector<int64_t> rz_used;          // per buffer: used floats per stream (before the guard)
