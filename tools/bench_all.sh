@@ -16,3 +16,5 @@ run --config 5 --steps 10 --warmup 4
 run --config 5 --steps 10 --warmup 4 --precision bf16
 run --config 5 --steps 16 --warmup 8 --frames 512
 run --config 5 --steps 6 --warmup 3 --frames 8192
+run --config 5 --steps 10 --warmup 4 --streams 2048
+SC_FP32_SPLIT=tf32 run --config 5 --steps 10 --warmup 4  # 3xTF32 A/B
