@@ -450,6 +450,30 @@ def main():
     else:
         path_tf, path_src = pk["bf16_sus"], "bf16 dense sustained (MEASURED_PEAKS.json)"
     step_path_ms = max(total_flops / (path_tf * 1e12), step_bytes_min / (pk["hbm"] * 1e9)) * 1e3
+    # layer-wise bound: sum over the step's launches of max(FLOPs / tensor ceiling, DRAM bytes /
+    # HBM), with each launch's DRAM bytes from the committed ncu launch list of this config
+    # (profiles/traffic.json, tools/ncu_traffic.py) — activations between layers count here
+    layerwise = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists() and not args.frames and not args.streams:
+        try:
+            tr = json.loads(tfile.read_text())
+            lw_ms, covered = 0.0, 0
+            for name, _ in prof:
+                b = tr.get(f"cfg{args.config}:{name}")
+                if b is None:
+                    continue
+                covered += 1
+                fl = 0.0
+                if name.startswith("op") and "[tc" in name:
+                    ois = [int(k) for k in name.split()[0][2:].split("+")]
+                    fl = 2.0 * sum(op_macs[oi] for oi in ois) * frames * streams
+                lw_ms += max(fl / (path_tf * 1e12), b / (pk["hbm"] * 1e9)) * 1e3
+            if covered >= len(prof) - 1:
+                layerwise = {"ms": lw_ms, "frac": lw_ms / (ms / args.steps), "launches_covered": covered,
+                             "bytes_source": "profiles/traffic.json (ncu dram__bytes read+write per launch)"}
+        except Exception:
+            layerwise = None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -478,6 +502,7 @@ def main():
                               "path_ms": step_path_ms,
                               "frac_of_path_ceiling": step_path_ms / (ms / args.steps),
                               "path_ceiling_tflops": path_tf, "path_ceiling_source": path_src,
+                              "layerwise": layerwise,
                               "note": "whole-step bound max(F/P, bytes/HBM) (SURVEY §8d); `ms` uses "
                                       "P = bf16 sustained, `path_ms` this precision's tensor ceiling"},
             "cpu_baseline": cpu,

@@ -26,6 +26,13 @@ def launches(path):
 
 def main():
     seq = launches(sys.argv[1])
+    # a capture window that starts mid-step: rotate so it starts at an ingest (the launches of
+    # one step are the same every step, so the tail + head form one complete step)
+    names0 = [n for n in json.loads(open(sys.argv[2]).read())["profile_ms"] if n != "carry"]
+    first = next((i for i, k in enumerate(seq) if "ingest" in k["name"]), 0)
+    if first > 0 and len(seq) - first < len(names0):
+        need = len(names0) - (len(seq) - first)
+        seq = seq[first:] + seq[first - need:first]
     names = [n for n in json.loads(open(sys.argv[2]).read())["profile_ms"] if n != "carry"]
     cfg = sys.argv[3]
     out = sys.argv[4] if len(sys.argv) > 4 else "profiles/traffic.json"
