@@ -486,15 +486,16 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int tile, int
 // scale depends only on the row's own 32 values: identical in window and non-window mode, for
 // any tile geometry (bit-identity across buffer partitions).
 template <int BN, int STAGES, int CK, bool BF, bool WIN, int IOB, bool CH, bool HF>
-__global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
+__global__ void __launch_bounds__(Roles<HF>::NT, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out, const __grid_constant__ CUtensorMap tmap_res,
                    const TcParams p) {
   using L = TcSmem<BN, STAGES, BF, WIN, IOB, HF>;
   static_assert(!HF || (!BF && !CH && CK == 1), "3xFP16: fp32 plans, unchained, one K-slab per chunk");
-  constexpr bool X2 = L::X2;
-  constexpr int EP0 = Roles<X2>::EP0;
-  constexpr int NT = Roles<X2>::NT;
+  constexpr bool X2 = L::X2;  // 3xFP16 non-window layout (A units + W ring)
+  constexpr bool RX = HF;     // 3xFP16 (window or not): warpgroup roles, two transform sets
+  constexpr int EP0 = Roles<RX>::EP0;
+  constexpr int NT = Roles<RX>::NT;
   constexpr bool ABF = BF && (IOB & 1);  // input rows are bf16
   constexpr bool OBF = BF && (IOB & 2);  // output / residual rows are bf16
   extern __shared__ uint8_t smem_raw[];
@@ -988,13 +989,372 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
         if (trace) g_tc_trace[6 * 256 + 4 * tcount + 3] = clk();
       }
   };
-  if constexpr (X2) {
-    // X2: warpgroup-aligned roles with register reallocation (setmaxnreg): WG0 = W producer,
-    // MMA issuer, epilogue I/O, A-unit producer (48 registers); WG1-2 = the two transform
-    // sets (88); WG3-4 = drain + epilogue (128: a 64-column fp32 accumulator per thread)
+  auto role_win_prod = [&]() {
+      // ===================== TMA producer, window mode =====================
+      // per 32-channel block: the 128 + halo input rows once (window slot), then per tap the
+      // weight hi / lo tiles into the W ring
+      const int taps = nk / p.cblocks;
+      const uint32_t a_bytes = static_cast<uint32_t>(BK * (ABF ? 2 : 4) * (p.R + p.halo));
+      if (p.wres) {  // whole weight resident: slab kb = cb * taps + q at slot kb
+        mbar_expect_tx_w(wres_full, static_cast<uint32_t>(nk) * 2 * L::B_TILE);
+        for (int cb = 0; cb < p.cblocks; ++cb)
+          for (int q = 0; q < taps; ++q) {
+            const int kb = cb * taps + q, kw = (q * p.cblocks + cb) * BK;
+            tma_load_3d_w(&tmap_w, wres_full, b_hi(kb), kw, 0, 0);
+            tma_load_3d_w(&tmap_w, wres_full, b_lo(kb), kw, 0, 1);
+          }
+      }
+      int g = 0, u = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
+        for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+          const int sa = u % L::AST;
+          if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
+          mbar_expect_tx_w(&wa_full[sa], a_bytes);
+          tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
+          // warm L2 with the next tile's window of this channel block: two fp32 window slots
+          // cannot cover the DRAM latency of the next load on their own (bf16 tiles hold three
+          // slots; there the prefetch cost 15-25% on cfg3's strided / ConvT layers)
+          if (!BF && tile + static_cast<int>(gridDim.x) < n_tiles && lane == 0) {
+            const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n, BN);
+            tma_prefetch_3d(&tmap_a, p.a_c0 + cb * BK, p.a_row0 + tn.i0, tn.s0);
+          }
+          if (p.wres) continue;
+          for (int q = 0; q < taps; ++q, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+            const int kw = (q * p.cblocks + cb) * BK;
+            mbar_expect_tx_w(&full[s], (BF ? 1 : 2) * L::B_TILE);
+            tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
+            if (!BF) tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
+          }
+        }
+        for (int k2 = 0; k2 < NK2; ++k2, ++g) {  // chained conv's weight slabs (bf16)
+          const int s = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          mbar_expect_tx_w(&full[s], L::B_TILE);
+          tma_load_3d_w(&tmap_w, &full[s], b_hi(s), (nk + k2) * BK, tc.n0, 0);
+        }
+      }
+  };
+  auto role_win_mma = [&]() {
+      // ===================== MMA issuer, window mode (SS-MMAs at a per-tap row offset) ========
+      const uint32_t tbase = warp_uniform(tmem_base);
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                             (static_cast<uint32_t>(BM >> 4) << 24);
+      const int taps = nk / p.cblocks;
+      int g = 0, c = 0, tcount = 0, u = 0;
+      if (p.wres) mbar_wait(wres_full, 0);
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+        for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+          const int sa = u % L::AST;
+          mbar_wait(&wa_ready[sa], (u / L::AST) & 1);
+          tc_fence_after();
+          const uint32_t wh = smem_u32(win_hi(sa)), wl = smem_u32(win_lo(sa));
+          for (int q = 0; q < taps; ++q, ++g) {
+            const int kb = cb * taps + q;
+            const int s = g % STAGES;
+            const int b = c % NB;
+            const bool chunk_first = (kb % CK) == 0;
+            const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
+            if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+            if (!p.wres) mbar_wait(&full[s], (g / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+            if (BF) {  // one bf16 window copy, SW64 rows of 64 B: tap q starts q * tap_rows rows in
+              const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                        (static_cast<uint32_t>(BM >> 4) << 24);
+              const uint32_t offb = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
+              const uint32_t wb = smem_u32(win_bf(sa)), bb = smem_u32(b_hi(s));
+  #pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                mma_bf16_w(dmain, sw64_desc(wb + offb + kk * 32), sw64_desc(bb + kk * 32), idesc_bf, acc0);
+              }
+            } else if (HF) {  // fp16 hi / lo window planes (SW64 rows of 64 B), tap q at a row offset
+              const uint32_t idesc_h = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                       (static_cast<uint32_t>(BM >> 4) << 24);  // F32 += F16 x F16
+              const uint32_t offh = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
+              const int ws = p.wres ? kb : s;
+              const uint32_t ah = smem_u32(win_hi(sa)) + offh, al = smem_u32(win_lo16(sa)) + offh;
+              const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+  #pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                mma_bf16_w(dmain, sw64_desc(al + kk * 32), sw64_desc(bh + kk * 32), idesc_h, acc0);
+                mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bl + kk * 32), idesc_h, 1u);
+              }
+  #pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bh + kk * 32), idesc_h, 1u);
+            } else {
+              const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
+              const int ws = p.wres ? kb : s;
+              if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
+              const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
+              // corrections first (2^-10 of the signal), then the main product, all into this
+              // chunk's accumulator: the truncating accumulation meets the large terms only in
+              // its last four steps (same error as a separate correction accumulator)
+  #pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
+                mma_tf32_w(dmain, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
+                mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
+              }
+  #pragma unroll
+              for (int kk = 0; kk < BK / 8; ++kk)
+                mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
+            }
+            if (!p.wres) mma_commit_w(&empty[s]);
+            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
+            if (chunk_last) {
+              mma_commit_w(&tfull[b]);
+              ++c;
+            }
+          }
+          mma_commit_w(&wa_empty[sa]);
+        }
+        if (CH) {  // chained 1x1 GEMM (bf16): A from the drain's TMEM slots, one chunk accumulator
+          const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>(BM >> 4) << 24);
+          for (int k2 = 0; k2 < NK2; ++k2, ++g) {
+            const int s = g % STAGES;
+            const int b = c % NB;
+            const int u2 = tcount * NK2 + k2, sl = u2 % NS2;
+            if (k2 == 0 && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
+            mbar_wait(&full[s], (g / STAGES) & 1);
+            mbar_wait(&a2full[sl], (u2 / NS2) & 1);
+            tc_fence_after();
+            const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
+            const uint32_t bb = smem_u32(b_hi(s)), at = tbase + A2_COL + W2 * sl;
+  #pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc_bf, (k2 > 0 || kk > 0) ? 1u : 0u);
+            mma_commit_w(&a2empty[sl]);
+            mma_commit_w(&empty[s]);
+            if (k2 == NK2 - 1) {
+              mma_commit_w(&tfull[b]);
+              ++c;
+            }
+          }
+        }
+      }
+  };
+  auto role_win_xf = [&]() {
+      // ===================== transform, window mode: hi in place, lo to the lo window ==========
+      // (3xFP16: two sets of four warps take alternate windows, each with its own named barrier)
+      const int xset = RX ? (warp - Roles<RX>::XF0) >> 2 : 0;
+      const int t = threadIdx.x - (Roles<RX>::XF0 + 4 * xset) * 32;  // 0..127
+      const bool pre_tanh = p.pre_act == ACT_TANH;
+      const float pre_s = slope_of(p.pre_act, p.pre_alpha);
+      const int rows = p.R + p.halo;
+      int u = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
+          if (RX && (u & 1) != xset) continue;
+          const int sa = u % L::AST;
+          mbar_wait(&wa_full[sa], (u / L::AST) & 1);
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
+          if (BF) {
+            // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
+            // (SW64 rows of 64 B, 16B chunk jo at jo ^ ((w >> 1) & 3)); item = (row, output chunk)
+            uint4* bfr = reinterpret_cast<uint4*>(win_bf(sa));
+            if (ABF) {  // the window rows are bf16 already (SW64): pre-activation into the copy
+              const uint4* rawb = reinterpret_cast<const uint4*>(win_hi(sa));
+              for (int e = t; e < rows * 4; e += 128) {
+                const int w = e >> 2, jp = (e & 3) ^ ((w >> 1) & 3);
+                uint4 u = rawb[w * 4 + jp];
+                if (pre_tanh || pre_s != 1.f) {
+                  uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+  #pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    if (!pre_tanh && pre_s < 1.f) {  // exact LeakyReLU on the packed pair
+                      const float lo = __uint_as_float(wv[k] << 16), hi = __uint_as_float(wv[k] & 0xFFFF0000u);
+                      __nv_bfloat162 b2 = __floats2bfloat162_rn(fmaxf(lo, lo * pre_s), fmaxf(hi, hi * pre_s));
+                      wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                    } else {
+                      float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[k]));
+                      f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
+                      f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
+                      __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
+                      wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                  }
+                  u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                bfr[w * 4 + jp] = u;
+              }
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&wa_ready[sa]);
+              continue;
+            }
+            const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
+            constexpr int IPB = (L::WROWS * 4 + 127) / 128;
+            float4 v[IPB][2];
+  #pragma unroll
+            for (int i = 0; i < IPB; ++i) {
+              const int e = t + 128 * i, w = e >> 2, jo = e & 3;
+              if (w < rows) {
+                v[i][0] = raw[w * 8 + ((2 * jo) ^ (w & 7))];
+                v[i][1] = raw[w * 8 + ((2 * jo + 1) ^ (w & 7))];
+              }
+            }
+  #pragma unroll
+            for (int i = 0; i < IPB; ++i) {
+              const int e = t + 128 * i, w = e >> 2, jo = e & 3;
+              if (w >= rows) continue;
+              float x[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
+              uint32_t pk[4];
+  #pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float y0 = pre_tanh ? tanh_ool(x[2 * k]) : act_lin(x[2 * k], pre_s);
+                const float y1 = pre_tanh ? tanh_ool(x[2 * k + 1]) : act_lin(x[2 * k + 1], pre_s);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(y0, y1);
+                pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              bfr[w * 4 + (jo ^ ((w >> 1) & 3))] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wa_ready[sa]);
+            continue;
+          }
+          if (HF) {
+            // raw fp32 rows (SW128, 16B chunk j of row w at j ^ (w & 7)) -> pre-activation ->
+            // per-row power-of-two scale -> fp16 hi | lo planes written IN PLACE over the raw rows
+            // (SW64 rows of 64 B: 16B chunk jb of row w at jb ^ ((w >> 1) & 3)), once every
+            // thread of the four warps has read its rows (named barrier 1).  Thread t owns row t
+            // whole (no shuffles) plus one 16-byte item of the halo rows 128 .. 143 (8 lanes per
+            // row, max by three shuffles).  Rows past the window are converted too (stale data,
+            // never read by an MMA): no branches, so the two rows' math interleaves.
+            const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
+            float4 v[8];
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = raw[t * 8 + (j ^ (t & 7))];
+            const int we = BM + (t >> 3), je = t & 7;
+            const float4 ve = raw[we * 8 + (je ^ (we & 7))];
+            named_bar(1 + xset, 128);
+            uint8_t* rsw = rsc + (u % RS_WIN) * L::WROWS;
+            const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
+            const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
+            const float scf = (!pre_tanh && pre_s > 1.f) ? pre_s : 1.f;  // scale rule: see the non-window HF
+            {
+              float m = 0.f;
+  #pragma unroll
+              for (int j = 0; j < 8; ++j)
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+              m *= scf;
+              int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+              sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+              const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+              const float scn = sc * pre_s;
+              uint32_t hv[16], lv[16];
+  #pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
+                float2 t2;
+                if (pre_tanh) {
+                  t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
+                } else {
+                  const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                  t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                    : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+                }
+                split_f16x2(t2, hv[k], lv[k]);
+              }
+              uint4* hr = reinterpret_cast<uint4*>(win_hi(sa)) + t * 4;
+              uint4* lr = reinterpret_cast<uint4*>(win_lo16(sa)) + t * 4;
+  #pragma unroll
+              for (int jb = 0; jb < 4; ++jb) {
+                hr[jb ^ ((t >> 1) & 3)] = make_uint4(hv[4 * jb], hv[4 * jb + 1], hv[4 * jb + 2], hv[4 * jb + 3]);
+                lr[jb ^ ((t >> 1) & 3)] = make_uint4(lv[4 * jb], lv[4 * jb + 1], lv[4 * jb + 2], lv[4 * jb + 3]);
+              }
+              rsw[t] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+            }
+            {
+              float m = fmaxf(fmaxf(fabsf(ve.x), fabsf(ve.y)), fmaxf(fabsf(ve.z), fabsf(ve.w)));
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+              m *= scf;
+              int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+              sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+              const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+              const float scn = sc * pre_s;
+              uint32_t hv[2], lv[2];
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const float x0 = k ? ve.z : ve.x, x1 = k ? ve.w : ve.y;
+                float2 t2;
+                if (pre_tanh) {
+                  t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
+                } else {
+                  const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                  t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
+                                    : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+                }
+                split_f16x2(t2, hv[k], lv[k]);
+              }
+              const int po = we * 8 + (((je >> 1) ^ ((we >> 1) & 3)) << 1) + (je & 1);  // uint2 units
+              reinterpret_cast<uint2*>(win_hi(sa))[po] = make_uint2(hv[0], hv[1]);
+              reinterpret_cast<uint2*>(win_lo16(sa))[po] = make_uint2(lv[0], lv[1]);
+              if (je == 0) rsw[we] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wa_ready[sa]);
+            continue;
+          }
+          float4* hrow = reinterpret_cast<float4*>(win_hi(sa));
+          float4* lrow = reinterpret_cast<float4*>(win_lo(sa));
+          // (row, 16B chunk) items spread evenly over the 128 threads, all loads issued first;
+          // 8 consecutive items = the 8 chunks of one row: conflict-free 128-bit accesses
+          constexpr int IPT = (WIN_ROWS * 8 + 127) / 128;  // items per thread (9)
+          float4 v[IPT];
+  #pragma unroll
+          for (int i = 0; i < IPT; ++i) {
+            const int e = t + 128 * i, w = e >> 3;
+            if (w < rows) v[i] = hrow[w * 8 + ((e & 7) ^ (w & 7))];
+          }
+  #pragma unroll
+          for (int i = 0; i < IPT; ++i) {
+            const int e = t + 128 * i, w = e >> 3;
+            if (w >= rows) continue;
+            const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            float h[4], l[4];
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float y = pre_tanh ? tanh_ool(x[k]) : act_lin(x[k], pre_s);
+              h[k] = __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
+              l[k] = y - h[k];
+            }
+            const int pj = w * 8 + ((e & 7) ^ (w & 7));
+            hrow[pj] = make_float4(h[0], h[1], h[2], h[3]);
+            lrow[pj] = make_float4(l[0], l[1], l[2], l[3]);
+          }
+          fence_proxy_async();  // generic smem writes -> read by the tensor core (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wa_ready[sa]);
+          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[2 * 256 + u] = clk();
+        }
+      }
+  };
+  if constexpr (RX) {
+    // 3xFP16: warpgroup-aligned roles with register reallocation (setmaxnreg): WG0 = W / window
+    // producer, MMA issuer, epilogue I/O, A-unit producer (X2) (48 registers); WG1-2 = the two
+    // transform sets, alternate K-slabs (X2) or windows (88); WG3-4 = drain + epilogue (128: a
+    // 64-column fp32 accumulator per thread)
     if (warp < 4) {
       reg_dealloc<48>();
-      if (warp == 0) {
+      if (WIN && warp == 0) {
+        role_win_prod();
+      } else if (WIN && warp == 1) {
+        role_win_mma();
+      } else if (WIN && warp == 3) {
+        // (no A-unit producer in window mode)
+      } else if (warp == 0) {
         // ===================== W producer, X2: weight hi | lo tiles into the stage ring ==========
         const int taps = nk / p.cblocks;
         int g = 0;
@@ -1048,8 +1408,11 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
           }
         }
       }
-    } else if (warp < Roles<X2>::EP0) {
+    } else if (warp < Roles<RX>::EP0) {
       reg_dealloc<88>();
+      if (WIN) {
+        role_win_xf();
+      } else {
       // ===================== transform, X2 (w3..w10: two sets of four, alternate K-slabs) =====
       // thread = tile row r (= TMEM lane): the row's power-of-two scale, pre-activation folded
       // into the scaling (LeakyReLU(x) 2^s = max(x 2^s, x (a 2^s)) exactly: 2^s is a power of
@@ -1144,356 +1507,17 @@ __global__ void __launch_bounds__(Roles<HF && !WIN>::NT, 1)
           if (++q == taps) q = 0;
         }
       }
+      }
     } else {
       reg_alloc<128>();
       role_drain();
     }
   } else if (WIN && warp == 0) {
-    // ===================== TMA producer, window mode =====================
-    // per 32-channel block: the 128 + halo input rows once (window slot), then per tap the
-    // weight hi / lo tiles into the W ring
-    const int taps = nk / p.cblocks;
-    const uint32_t a_bytes = static_cast<uint32_t>(BK * (ABF ? 2 : 4) * (p.R + p.halo));
-    if (p.wres) {  // whole weight resident: slab kb = cb * taps + q at slot kb
-      mbar_expect_tx_w(wres_full, static_cast<uint32_t>(nk) * 2 * L::B_TILE);
-      for (int cb = 0; cb < p.cblocks; ++cb)
-        for (int q = 0; q < taps; ++q) {
-          const int kb = cb * taps + q, kw = (q * p.cblocks + cb) * BK;
-          tma_load_3d_w(&tmap_w, wres_full, b_hi(kb), kw, 0, 0);
-          tma_load_3d_w(&tmap_w, wres_full, b_lo(kb), kw, 0, 1);
-        }
-    }
-    int g = 0, u = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
-      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u % L::AST;
-        if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
-        mbar_expect_tx_w(&wa_full[sa], a_bytes);
-        tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
-        // warm L2 with the next tile's window of this channel block: two fp32 window slots
-        // cannot cover the DRAM latency of the next load on their own (bf16 tiles hold three
-        // slots; there the prefetch cost 15-25% on cfg3's strided / ConvT layers)
-        if (!BF && tile + static_cast<int>(gridDim.x) < n_tiles && lane == 0) {
-          const TileCoord tn = tile_coord(p, tile + gridDim.x, n_tiles_n, BN);
-          tma_prefetch_3d(&tmap_a, p.a_c0 + cb * BK, p.a_row0 + tn.i0, tn.s0);
-        }
-        if (p.wres) continue;
-        for (int q = 0; q < taps; ++q, ++g) {
-          const int s = g % STAGES;
-          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
-          const int kw = (q * p.cblocks + cb) * BK;
-          mbar_expect_tx_w(&full[s], (BF ? 1 : 2) * L::B_TILE);
-          tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
-          if (!BF) tma_load_3d_w(&tmap_w, &full[s], b_lo(s), kw, tc.n0, 1);
-        }
-      }
-      for (int k2 = 0; k2 < NK2; ++k2, ++g) {  // chained conv's weight slabs (bf16)
-        const int s = g % STAGES;
-        if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
-        mbar_expect_tx_w(&full[s], L::B_TILE);
-        tma_load_3d_w(&tmap_w, &full[s], b_hi(s), (nk + k2) * BK, tc.n0, 0);
-      }
-    }
+    role_win_prod();
   } else if (WIN && warp == 1) {
-    // ===================== MMA issuer, window mode (SS-MMAs at a per-tap row offset) ========
-    const uint32_t tbase = warp_uniform(tmem_base);
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                           (static_cast<uint32_t>(BM >> 4) << 24);
-    const int taps = nk / p.cblocks;
-    int g = 0, c = 0, tcount = 0, u = 0;
-    if (p.wres) mbar_wait(wres_full, 0);
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u % L::AST;
-        mbar_wait(&wa_ready[sa], (u / L::AST) & 1);
-        tc_fence_after();
-        const uint32_t wh = smem_u32(win_hi(sa)), wl = smem_u32(win_lo(sa));
-        for (int q = 0; q < taps; ++q, ++g) {
-          const int kb = cb * taps + q;
-          const int s = g % STAGES;
-          const int b = c % NB;
-          const bool chunk_first = (kb % CK) == 0;
-          const bool chunk_last = ((kb % CK) == CK - 1) || (kb == nk - 1);
-          if (chunk_first && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
-          if (!p.wres) mbar_wait(&full[s], (g / STAGES) & 1);
-          tc_fence_after();
-          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-          if (BF) {  // one bf16 window copy, SW64 rows of 64 B: tap q starts q * tap_rows rows in
-            const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                                      (static_cast<uint32_t>(BM >> 4) << 24);
-            const uint32_t offb = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
-            const uint32_t wb = smem_u32(win_bf(sa)), bb = smem_u32(b_hi(s));
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16_w(dmain, sw64_desc(wb + offb + kk * 32), sw64_desc(bb + kk * 32), idesc_bf, acc0);
-            }
-          } else if (HF) {  // fp16 hi / lo window planes (SW64 rows of 64 B), tap q at a row offset
-            const uint32_t idesc_h = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                                     (static_cast<uint32_t>(BM >> 4) << 24);  // F32 += F16 x F16
-            const uint32_t offh = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
-            const int ws = p.wres ? kb : s;
-            const uint32_t ah = smem_u32(win_hi(sa)) + offh, al = smem_u32(win_lo16(sa)) + offh;
-            const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_bf16_w(dmain, sw64_desc(al + kk * 32), sw64_desc(bh + kk * 32), idesc_h, acc0);
-              mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bl + kk * 32), idesc_h, 1u);
-            }
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bh + kk * 32), idesc_h, 1u);
-          } else {
-            const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
-            const int ws = p.wres ? kb : s;
-            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[3 * 256 + g] = clk();
-            const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
-            // corrections first (2^-10 of the signal), then the main product, all into this
-            // chunk's accumulator: the truncating accumulation meets the large terms only in
-            // its last four steps (same error as a separate correction accumulator)
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-              mma_tf32_w(dmain, sw128_desc(wl + off + kk * 32), sw128_desc(bh + kk * 32), idesc, acc0);
-              mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bl + kk * 32), idesc, 1u);
-            }
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk)
-              mma_tf32_w(dmain, sw128_desc(wh + off + kk * 32), sw128_desc(bh + kk * 32), idesc, 1u);
-          }
-          if (!p.wres) mma_commit_w(&empty[s]);
-          if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[11 * 256 + g] = clk();
-          if (chunk_last) {
-            mma_commit_w(&tfull[b]);
-            ++c;
-          }
-        }
-        mma_commit_w(&wa_empty[sa]);
-      }
-      if (CH) {  // chained 1x1 GEMM (bf16): A from the drain's TMEM slots, one chunk accumulator
-        const uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                                  (static_cast<uint32_t>(BM >> 4) << 24);
-        for (int k2 = 0; k2 < NK2; ++k2, ++g) {
-          const int s = g % STAGES;
-          const int b = c % NB;
-          const int u2 = tcount * NK2 + k2, sl = u2 % NS2;
-          if (k2 == 0 && c >= NB) mbar_wait(&tempty[b], ((c / NB) + 1) & 1);
-          mbar_wait(&full[s], (g / STAGES) & 1);
-          mbar_wait(&a2full[sl], (u2 / NS2) & 1);
-          tc_fence_after();
-          const uint32_t dmain = tbase + static_cast<uint32_t>(b * BN);
-          const uint32_t bb = smem_u32(b_hi(s)), at = tbase + A2_COL + W2 * sl;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            mma_bf16_ts_w(dmain, at + kk * 8, sw64_desc(bb + kk * 32), idesc_bf, (k2 > 0 || kk > 0) ? 1u : 0u);
-          mma_commit_w(&a2empty[sl]);
-          mma_commit_w(&empty[s]);
-          if (k2 == NK2 - 1) {
-            mma_commit_w(&tfull[b]);
-            ++c;
-          }
-        }
-      }
-    }
+    role_win_mma();
   } else if (WIN && warp >= XF_WARP0 && warp < EP0) {
-    // ===================== transform, window mode: hi in place, lo to the lo window ==========
-    const int t = threadIdx.x - XF_WARP0 * 32;  // 0..127
-    const bool pre_tanh = p.pre_act == ACT_TANH;
-    const float pre_s = slope_of(p.pre_act, p.pre_alpha);
-    const int rows = p.R + p.halo;
-    int u = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
-        const int sa = u % L::AST;
-        mbar_wait(&wa_full[sa], (u / L::AST) & 1);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
-        if (BF) {
-          // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
-          // (SW64 rows of 64 B, 16B chunk jo at jo ^ ((w >> 1) & 3)); item = (row, output chunk)
-          uint4* bfr = reinterpret_cast<uint4*>(win_bf(sa));
-          if (ABF) {  // the window rows are bf16 already (SW64): pre-activation into the copy
-            const uint4* rawb = reinterpret_cast<const uint4*>(win_hi(sa));
-            for (int e = t; e < rows * 4; e += 128) {
-              const int w = e >> 2, jp = (e & 3) ^ ((w >> 1) & 3);
-              uint4 u = rawb[w * 4 + jp];
-              if (pre_tanh || pre_s != 1.f) {
-                uint32_t wv[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  if (!pre_tanh && pre_s < 1.f) {  // exact LeakyReLU on the packed pair
-                    const float lo = __uint_as_float(wv[k] << 16), hi = __uint_as_float(wv[k] & 0xFFFF0000u);
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(fmaxf(lo, lo * pre_s), fmaxf(hi, hi * pre_s));
-                    wv[k] = *reinterpret_cast<uint32_t*>(&b2);
-                  } else {
-                    float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[k]));
-                    f.x = pre_tanh ? tanh_ool(f.x) : act_lin(f.x, pre_s);
-                    f.y = pre_tanh ? tanh_ool(f.y) : act_lin(f.y, pre_s);
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(f.x, f.y);
-                    wv[k] = *reinterpret_cast<uint32_t*>(&b2);
-                  }
-                }
-                u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-              }
-              bfr[w * 4 + jp] = u;
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wa_ready[sa]);
-            continue;
-          }
-          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
-          constexpr int IPB = (L::WROWS * 4 + 127) / 128;
-          float4 v[IPB][2];
-#pragma unroll
-          for (int i = 0; i < IPB; ++i) {
-            const int e = t + 128 * i, w = e >> 2, jo = e & 3;
-            if (w < rows) {
-              v[i][0] = raw[w * 8 + ((2 * jo) ^ (w & 7))];
-              v[i][1] = raw[w * 8 + ((2 * jo + 1) ^ (w & 7))];
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < IPB; ++i) {
-            const int e = t + 128 * i, w = e >> 2, jo = e & 3;
-            if (w >= rows) continue;
-            float x[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
-            uint32_t pk[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float y0 = pre_tanh ? tanh_ool(x[2 * k]) : act_lin(x[2 * k], pre_s);
-              const float y1 = pre_tanh ? tanh_ool(x[2 * k + 1]) : act_lin(x[2 * k + 1], pre_s);
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(y0, y1);
-              pk[k] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            bfr[w * 4 + (jo ^ ((w >> 1) & 3))] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&wa_ready[sa]);
-          continue;
-        }
-        if (HF) {
-          // raw fp32 rows (SW128, 16B chunk j of row w at j ^ (w & 7)) -> pre-activation ->
-          // per-row power-of-two scale -> fp16 hi | lo planes written IN PLACE over the raw rows
-          // (SW64 rows of 64 B: 16B chunk jb of row w at jb ^ ((w >> 1) & 3)), once every
-          // thread of the four warps has read its rows (named barrier 1).  Thread t owns row t
-          // whole (no shuffles) plus one 16-byte item of the halo rows 128 .. 143 (8 lanes per
-          // row, max by three shuffles).  Rows past the window are converted too (stale data,
-          // never read by an MMA): no branches, so the two rows' math interleaves.
-          const float4* raw = reinterpret_cast<const float4*>(win_hi(sa));
-          float4 v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = raw[t * 8 + (j ^ (t & 7))];
-          const int we = BM + (t >> 3), je = t & 7;
-          const float4 ve = raw[we * 8 + (je ^ (we & 7))];
-          named_bar(1, 128);
-          uint8_t* rsw = rsc + (u % RS_WIN) * L::WROWS;
-          const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
-          const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
-          const float scf = (!pre_tanh && pre_s > 1.f) ? pre_s : 1.f;  // scale rule: see the non-window HF
-          {
-            float m = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
-            m *= scf;
-            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
-            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
-            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
-            const float scn = sc * pre_s;
-            uint32_t hv[16], lv[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
-              float2 t2;
-              if (pre_tanh) {
-                t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
-              } else {
-                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
-              }
-              split_f16x2(t2, hv[k], lv[k]);
-            }
-            uint4* hr = reinterpret_cast<uint4*>(win_hi(sa)) + t * 4;
-            uint4* lr = reinterpret_cast<uint4*>(win_lo16(sa)) + t * 4;
-#pragma unroll
-            for (int jb = 0; jb < 4; ++jb) {
-              hr[jb ^ ((t >> 1) & 3)] = make_uint4(hv[4 * jb], hv[4 * jb + 1], hv[4 * jb + 2], hv[4 * jb + 3]);
-              lr[jb ^ ((t >> 1) & 3)] = make_uint4(lv[4 * jb], lv[4 * jb + 1], lv[4 * jb + 2], lv[4 * jb + 3]);
-            }
-            rsw[t] = static_cast<uint8_t>(127 - sx - p.f16_sw);
-          }
-          {
-            float m = fmaxf(fmaxf(fabsf(ve.x), fabsf(ve.y)), fmaxf(fabsf(ve.z), fabsf(ve.w)));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-            m *= scf;
-            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
-            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
-            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
-            const float scn = sc * pre_s;
-            uint32_t hv[2], lv[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const float x0 = k ? ve.z : ve.x, x1 = k ? ve.w : ve.y;
-              float2 t2;
-              if (pre_tanh) {
-                t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
-              } else {
-                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
-              }
-              split_f16x2(t2, hv[k], lv[k]);
-            }
-            const int po = we * 8 + (((je >> 1) ^ ((we >> 1) & 3)) << 1) + (je & 1);  // uint2 units
-            reinterpret_cast<uint2*>(win_hi(sa))[po] = make_uint2(hv[0], hv[1]);
-            reinterpret_cast<uint2*>(win_lo16(sa))[po] = make_uint2(lv[0], lv[1]);
-            if (je == 0) rsw[we] = static_cast<uint8_t>(127 - sx - p.f16_sw);
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&wa_ready[sa]);
-          continue;
-        }
-        float4* hrow = reinterpret_cast<float4*>(win_hi(sa));
-        float4* lrow = reinterpret_cast<float4*>(win_lo(sa));
-        // (row, 16B chunk) items spread evenly over the 128 threads, all loads issued first;
-        // 8 consecutive items = the 8 chunks of one row: conflict-free 128-bit accesses
-        constexpr int IPT = (WIN_ROWS * 8 + 127) / 128;  // items per thread (9)
-        float4 v[IPT];
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-          const int e = t + 128 * i, w = e >> 3;
-          if (w < rows) v[i] = hrow[w * 8 + ((e & 7) ^ (w & 7))];
-        }
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-          const int e = t + 128 * i, w = e >> 3;
-          if (w >= rows) continue;
-          const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-          float h[4], l[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float y = pre_tanh ? tanh_ool(x[k]) : act_lin(x[k], pre_s);
-            h[k] = __uint_as_float(__float_as_uint(y) & 0xFFFFE000u);
-            l[k] = y - h[k];
-          }
-          const int pj = w * 8 + ((e & 7) ^ (w & 7));
-          hrow[pj] = make_float4(h[0], h[1], h[2], h[3]);
-          lrow[pj] = make_float4(l[0], l[1], l[2], l[3]);
-        }
-        fence_proxy_async();  // generic smem writes -> read by the tensor core (async proxy)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&wa_ready[sa]);
-        if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[2 * 256 + u] = clk();
-      }
-    }
+    role_win_xf();
   } else if (warp == 0) {
     // ===================== TMA producer (whole warp, one elected lane issues) =====================
     {
@@ -1713,7 +1737,7 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mw, const CUtensorMap& 
   const int grid = n_tiles < g_sms ? n_tiles : g_sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(Roles<HF && !WIN>::NT);
+  cfg.blockDim = dim3(Roles<HF>::NT);
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
