@@ -15,6 +15,8 @@
 // conflict-free and vectorise the broadcast coefficient reads.
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "kernels_pqmf.hpp"
 
 namespace scb {
@@ -38,7 +40,7 @@ __device__ __forceinline__ float act_apply(float v, int kind, float alpha) {
 // One output row = M contiguous floats (M bands of a frame, or M samples of a mono buffer).
 __device__ __forceinline__ void store_row(const PqmfParams& p, int s, int row, const float (&y)[M]) {
   float* dst = p.out + static_cast<int64_t>(s) * p.out_sstride + p.out_base + static_cast<int64_t>(row) * M;
-  if (((p.out_sstride | p.out_base) & 3) == 0) {
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // (a fused output may be any caller pointer)
     float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
     for (int q = 0; q < M / 4; ++q) d4[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
@@ -75,10 +77,22 @@ __global__ void __launch_bounds__(FB) pqmf_analysis_kernel(const PqmfParams p, c
   {  // all loads in flight before the first store (the block's only HBM read)
     constexpr int IT = (WMAX + FB - 1) / FB;
     float v[IT];
+    if (p.xin) {  // fused mono input: cached rows from the strip, new rows from the caller
+      const int a0 = p.in_f0 + M * i0;  // strip row of window element 0
+      const float* xs = p.xin + static_cast<int64_t>(s) * p.xin_T - p.cache0;
+      float* tail = p.strip + static_cast<int64_t>(s) * p.in_sstride;
 #pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int e = t + it * FB;
-      v[it] = e < W ? __ldg(src + e) : 0.f;
+      for (int it = 0; it < IT; ++it) {
+        const int e = t + it * FB, a = a0 + e;
+        v[it] = e < W ? __ldg(a < p.cache0 ? src + e : xs + a) : 0.f;
+        if (e < W && a >= p.xin_T) tail[a] = v[it];  // the next call's cache rows
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int e = t + it * FB;
+        v[it] = e < W ? __ldg(src + e) : 0.f;
+      }
     }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -224,6 +238,15 @@ bool pqmf_fast_shape(int kind, int bands, int A_or_Q, int B_or_classes, int peri
   if (bands != M) return false;
   if (kind == 1) return A_or_Q == A && B_or_classes == B;
   return A_or_Q == Q && (period == 1 || period == 2) && B_or_classes == period * (mirror ? M / 2 : M);
+}
+
+const void* pqmf_kernel_ptr(int kind, int period, int mirror) {
+  if (kind == 1) return reinterpret_cast<const void*>(&pqmf_analysis_kernel);
+  if (period == 2)
+    return mirror ? reinterpret_cast<const void*>(&pqmf_synthesis_kernel<2, true>)
+                  : reinterpret_cast<const void*>(&pqmf_synthesis_kernel<2, false>);
+  return mirror ? reinterpret_cast<const void*>(&pqmf_synthesis_kernel<1, true>)
+                : reinterpret_cast<const void*>(&pqmf_synthesis_kernel<1, false>);
 }
 
 void launch_pqmf(int kind, const PqmfParams& p, const PqmfCoef& k, cudaStream_t st) {

@@ -31,6 +31,14 @@ struct PqmfParams {
   float pre_alpha;
   int post_act;
   float post_alpha;
+  // fused mono input (analysis, xin != nullptr): window rows >= cache0 (relative to `in`'s
+  // frame 0) come from the caller's input xin[stream * xin_T + row - cache0] instead of the
+  // state's strip, and rows >= xin_T (the last cache0 rows of the call) are also written to the
+  // strip (`strip`, same geometry as `in`): they are the next call's cache.  No ingest launch.
+  const float* xin;
+  float* strip;
+  int xin_T;
+  int cache0;
 };
 
 // The bank's coefficients, passed by value (kernel-parameter / constant bank):
@@ -44,5 +52,8 @@ struct PqmfCoef {
 // 16 bands.
 bool pqmf_fast_shape(int kind, int bands, int A_or_Q, int B_or_classes, int period = 0, int mirror = 0);
 void launch_pqmf(int kind, const PqmfParams& p, const PqmfCoef& k, cudaStream_t st);
+// the kernel functions (graph nodes re-targeted per call when they carry the caller's I/O)
+const void* pqmf_kernel_ptr(int kind, int period, int mirror);
+constexpr int kPqmfLook = 240;  // analysis window look-back (K - M) of the 16-band, 256-tap bank
 
 }  // namespace scb

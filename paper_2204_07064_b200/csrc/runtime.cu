@@ -113,6 +113,11 @@ bool awin_disabled() {
   return e && e[0] == '0';
 }
 
+bool io_fuse_disabled() {  // SC_IO_FUSE=0: keep the ingest / egress launches
+  const char* e = std::getenv("SC_IO_FUSE");
+  return e && e[0] == '0';
+}
+
 bool small_bn_disabled() {
   const char* e = std::getenv("SC_SMALL_BN");
   return e && e[0] == '0';
@@ -894,6 +899,36 @@ CallPlan& State::call_plan(int64_t F) {
     cp->chained[i] = j;
     cp->n_launch -= 1;
   }
+  // fused mono I/O: the PQMF analysis reads the caller's input itself (its window's cached rows
+  // from the strip, the new rows from the caller, and it writes the last cache rows back as the
+  // next call's cache), the PQMF synthesis writes the caller's output — no ingest / egress
+  // launch and no strip round trip for the mono signal (C = 1: [stream][1][T] is the frame-major
+  // layout already).  Only when the geometry is the plain one; else the separate kernels run.
+  if (!io_fuse_disabled()) {
+    int reader = -1, readers = 0, writer = -1, writers = 0;
+    for (size_t i = 0; i < pg.ops.size(); ++i) {
+      const ConvOp& op = pg.ops[i];
+      if (op.in_buf == 0) reader = static_cast<int>(i), ++readers;
+      if (op.res_buf == 0) readers += 2;
+      for (const SumIn& si : op.sum_in) readers += si.buf == 0 ? 2 : 0;
+      if (op.out_buf == pg.sink_buf) writer = static_cast<int>(i), ++writers;
+      if (op.res_buf == pg.sink_buf || op.in_buf == pg.sink_buf) writers += 2;
+      for (const SumIn& si : op.sum_in) writers += si.buf == pg.sink_buf ? 2 : 0;
+    }
+    if (readers == 1 && plan->dops[reader].kernel == KERNEL_PQMF_ANA && pg.in_C == 1 && !plan->buf_bf16[0] &&
+        cp->t_out[reader] > 0) {
+      const ConvParams c = conv_params(reader, *cp);
+      const int64_t last_i0 = ((c.t_out - 1) / 128) * 128;
+      if (F >= cache[0] && c.in_f0 + 16 * static_cast<int64_t>(c.t_out) + kPqmfLook == cache[0] + F &&
+          c.in_f0 + 16 * last_i0 <= F && c.in_f0 >= 0)
+        cp->fuse_in = reader;
+    }
+    if (writers == 1 && plan->dops[writer].kernel == KERNEL_PQMF_SYN && pg.sink_C == 1 && pg.sink_off == 0 &&
+        pg.sink_act == ACT_ID && cache[sb] == 0 && !plan->buf_bf16[sb] && cp->t_out[writer] > 0 &&
+        cp->egress_row == 0 && cp->egress_T == 16 * cp->t_out[writer] && pg.bufs[sb].C == 1)
+      cp->fuse_out = writer;
+    cp->n_launch -= (cp->fuse_in >= 0 ? 1 : 0) + (cp->fuse_out >= 0 ? 1 : 0);
+  }
   cp->last_use = ++plan_clock;
   return *plans.emplace(key, std::move(cp)).first->second;
 }
@@ -965,6 +1000,22 @@ PqmfParams State::pqmf_params(size_t i, const CallPlan& cp) const {
   p.pre_alpha = c.pre_alpha;
   p.post_act = c.post_act;
   p.post_alpha = c.post_alpha;
+  return p;
+}
+
+PqmfParams State::pqmf_io_params(size_t i, const CallPlan& cp, const float* in, float* out) const {
+  PqmfParams p = pqmf_params(i, cp);
+  if (static_cast<int>(i) == cp.fuse_in) {
+    p.xin = in;
+    p.strip = cp.base[0];
+    p.xin_T = static_cast<int>(cp.F);
+    p.cache0 = static_cast<int>(cache[0]);
+  }
+  if (static_cast<int>(i) == cp.fuse_out) {
+    p.out = out;
+    p.out_sstride = cp.egress_T;
+    p.out_base = 0;
+  }
   return p;
 }
 
@@ -1062,7 +1113,7 @@ int State::launches(int64_t F) {
   check_frames(F);
   DeviceScope dev(plan->device);
   CallPlan& cp = call_plan(F);
-  int n = 2 + (carry_slot ? 1 : 0);
+  int n = (cp.fuse_in < 0 ? 1 : 0) + (cp.fuse_out < 0 ? 1 : 0) + (carry_slot ? 1 : 0);
   for (int64_t t : cp.t_out) n += t > 0 ? 1 : 0;
   return n;
 }
@@ -1073,7 +1124,7 @@ std::string State::launch_name(int64_t F, int i) {
   CallPlan& cp = call_plan(F);
   int k = 0;
   if (carry_slot && i == k++) return "carry";
-  if (i == k++) return "ingest";
+  if (cp.fuse_in < 0 && i == k++) return "ingest";
   for (size_t j = 0; j < plan->prog.ops.size(); ++j) {
     if (cp.t_out[j] == 0) continue;
     if (i == k++) {
@@ -1085,10 +1136,11 @@ std::string State::launch_name(int64_t F, int i) {
                plan->prog.ops[jc].name + (plan->dops[j].bf16 ? " [tc-bf16]" : " [tc]");
       return "op" + std::to_string(j) + " " + op.name + " [" +
              (d.kernel == KERNEL_TC ? (d.bf16 ? "tc-bf16" : d.f16 ? "tc-3xf16" : "tc")
-              : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum" : "pqmf") + "]";
+              : d.kernel == KERNEL_SIMT ? "simt" : d.kernel == KERNEL_SUM ? "simt-sum"
+              : static_cast<int>(j) == cp.fuse_in ? "pqmf+input" : static_cast<int>(j) == cp.fuse_out ? "pqmf+output" : "pqmf") + "]";
     }
   }
-  if (i == k++) return "egress";
+  if (cp.fuse_out < 0 && i == k++) return "egress";
   return "";
 }
 
@@ -1099,8 +1151,10 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     if (cp.n_desc > 0) launch_carry(cp.d_desc, cp.n_desc, streams, cp.carry_items, s);
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
-  launch_ingest(ingest_args(in, cp), s);
-  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  if (cp.fuse_in < 0) {
+    launch_ingest(ingest_args(in, cp), s);
+    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  }
   for (size_t i = 0; i < plan->prog.ops.size(); ++i) {
     if (cp.t_out[i] == 0) continue;
     NvtxRange op_range(ev == nullptr && nvtx_enabled() && !capturing, "op" + std::to_string(i) + " " + plan->prog.ops[i].name);
@@ -1110,15 +1164,17 @@ void State::enqueue(const float* in, float* out, CallPlan& cp, cudaStream_t s, c
     } else if (plan->dops[i].kernel == KERNEL_SUM) {
       launch_sum(sum_params(i, cp), s);
     } else if (plan->dops[i].kernel == KERNEL_PQMF_ANA || plan->dops[i].kernel == KERNEL_PQMF_SYN) {
-      launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_params(i, cp),
+      launch_pqmf(plan->dops[i].kernel == KERNEL_PQMF_ANA ? 1 : 2, pqmf_io_params(i, cp, in, out),
                   *reinterpret_cast<const PqmfCoef*>(plan->dops[i].pq_k.data()), s);
     } else {
       launch_conv_simt(conv_params(i, cp), s);
     }
     if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
   }
-  launch_egress(egress_args(out, cp), s);
-  if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  if (cp.fuse_out < 0) {
+    launch_egress(egress_args(out, cp), s);
+    if (ev) ck(cudaEventRecord(ev[e++], s), "EventRecord");
+  }
 }
 
 void State::check_frames(int64_t F) const {
@@ -1196,8 +1252,8 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
           if (jt->second.last_use < lru->second.last_use) lru = jt;
         // the ingest / egress kernels (wide or general) are picked per I/O pointer at launch: a
         // graph captured with the other one cannot be re-targeted — drop it and capture anew
-        const bool wide = egress_wide(egress_args(out, cp));
-        const bool iwide = ingest_wide(ingest_args(in, cp));
+        const bool wide = cp.fuse_out < 0 && egress_wide(egress_args(out, cp));
+        const bool iwide = cp.fuse_in < 0 && ingest_wide(ingest_args(in, cp));
         if (is_egress_wide_kernel(lru->second.egress_params.func) != wide ||
             is_ingest_wide_kernel(lru->second.ingest_params.func) != iwide) {
           cudaGraphExecDestroy(lru->second.exec);
@@ -1213,12 +1269,22 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
         cp.graphs.erase(lru);
         g.ia = ingest_args(in, cp);
         g.ea = egress_args(out, cp);
-        void* a1[] = {&g.ia};
+        void* a1[] = {&g.ia, nullptr};
+        if (cp.fuse_in >= 0) {  // the fused PQMF analysis carries the input pointer
+          g.pin = pqmf_io_params(cp.fuse_in, cp, in, out);
+          a1[0] = &g.pin;
+          a1[1] = const_cast<float*>(plan->dops[cp.fuse_in].pq_k.data());
+        }
         cudaKernelNodeParams kp = g.ingest_params;
         kp.kernelParams = a1;
         kp.extra = nullptr;
         ck(cudaGraphExecKernelNodeSetParams(g.exec, g.ingest_node, &kp), "ExecKernelNodeSetParams");
-        void* a2[] = {&g.ea};
+        void* a2[] = {&g.ea, nullptr};
+        if (cp.fuse_out >= 0) {  // the fused PQMF synthesis carries the output pointer
+          g.pout = pqmf_io_params(cp.fuse_out, cp, in, out);
+          a2[0] = &g.pout;
+          a2[1] = const_cast<float*>(plan->dops[cp.fuse_out].pq_k.data());
+        }
         kp = g.egress_params;
         kp.kernelParams = a2;
         kp.extra = nullptr;
@@ -1244,10 +1310,17 @@ void State::process(const float* in, float* out, int64_t F, cudaStream_t s) {
           if (ty != cudaGraphNodeTypeKernel) continue;
           cudaKernelNodeParams kp;
           ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
-          if (kp.func == ingest_kernel_ptr() || is_ingest_wide_kernel(kp.func)) {
+          const void* fin = cp.fuse_in >= 0 ? pqmf_kernel_ptr(1, 0, 0) : nullptr;
+          const void* fout = nullptr;
+          if (cp.fuse_out >= 0) {
+            const ConvOp& so = plan->prog.ops[cp.fuse_out];
+            fout = pqmf_kernel_ptr(2, so.pq_period, so.pq_mirror);
+          }
+          if (cp.fuse_in >= 0 ? kp.func == fin : (kp.func == ingest_kernel_ptr() || is_ingest_wide_kernel(kp.func))) {
             g.ingest_node = nd;
             g.ingest_params = kp;
-          } else if (kp.func == egress_kernel_ptr() || is_egress_wide_kernel(kp.func)) {
+          } else if (cp.fuse_out >= 0 ? kp.func == fout
+                                      : (kp.func == egress_kernel_ptr() || is_egress_wide_kernel(kp.func))) {
             g.egress_node = nd;
             g.egress_params = kp;
           }

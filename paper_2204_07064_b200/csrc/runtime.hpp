@@ -57,10 +57,13 @@ struct Plan {
 struct GraphEntry {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // the nodes carrying the caller's I/O pointers (re-targeted per call): the ingest / egress
+  // kernels, or the PQMF analysis / synthesis when the mono I/O is fused into them
   cudaGraphNode_t ingest_node = nullptr, egress_node = nullptr;
   cudaKernelNodeParams ingest_params{}, egress_params{};
   IngestArgs ia{};
   EgressArgs ea{};
+  PqmfParams pin{}, pout{};
   uint64_t last_use = 0;
 };
 
@@ -89,6 +92,8 @@ struct CallPlan {
   int n_desc = 0;
   int64_t carry_items = 0;
   int n_launch = 0;           // kernels one call of this plan launches
+  int fuse_in = -1;           // the PQMF analysis op that reads the caller's input (no ingest)
+  int fuse_out = -1;          // the PQMF synthesis op that writes the caller's output (no egress)
   std::vector<int> chained;   // per op: the op chained into its launch this call (-1: none)
   std::vector<TcLaunch> tc;
   std::map<std::pair<const float*, float*>, GraphEntry> graphs;
@@ -149,6 +154,8 @@ struct State {
   CallPlan& call_plan(int64_t F);
   ConvParams conv_params(size_t op, const CallPlan& cp) const;
   PqmfParams pqmf_params(size_t op, const CallPlan& cp) const;
+  // pqmf_params plus the caller's I/O when this op carries the fused mono input / output
+  PqmfParams pqmf_io_params(size_t op, const CallPlan& cp, const float* in, float* out) const;
   SumParams sum_params(size_t op, const CallPlan& cp) const;
   IngestArgs ingest_args(const float* in, const CallPlan& cp) const;
   EgressArgs egress_args(float* out, const CallPlan& cp) const;

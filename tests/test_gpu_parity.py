@@ -370,11 +370,31 @@ def test_pqmf_fast_form_vs_oracle(parts):
     x = rng.standard_normal((3, 1, sum(parts))).astype(np.float32)
     y, plan, st = run_gpu(m, x, parts)
     names = st.launch_names(parts[0])
-    assert any("pqmf-analysis" in n and n.endswith("[pqmf]") for n in names), names
-    assert any("pqmf-synthesis" in n and n.endswith("[pqmf]") for n in names), names
+    assert any("pqmf-analysis" in n and "[pqmf" in n for n in names), names
+    assert any("pqmf-synthesis" in n and "[pqmf" in n for n in names), names
     ref = po.run(oracle_twin(m), x, parts=parts)
     err, rms = rel_err(y, ref)
     assert err <= FP32_TOL, (err, rms)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,parts", [(5, [2048, 2048, 4096]), (5, [512] * 8), (4, [1] * 6)])
+def test_fused_mono_io_bit_identical(cfg, parts, monkeypatch):
+    """The PQMF analysis reading the caller's input (and writing the next cache itself) and the
+    synthesis writing the caller's output (no ingest / egress launches) give exactly the
+    outputs of the separate ingest / egress kernels (SC_IO_FUSE=0), graphs and eager."""
+    m = configs.build(cfg, seed=cfg)
+    x = configs.batch_input(cfg, range(3), m.in_channels, sum(parts), seed=4)
+    ya, _, st = run_gpu(m, x, parts)
+    names = st.launch_names(parts[-1])
+    if cfg == 5 and parts[0] >= 2048:
+        assert "ingest" not in names and "egress" not in names, names
+    yb, _, _ = run_gpu(m, x, parts, graphs=False)
+    monkeypatch.setenv("SC_IO_FUSE", "0")
+    yc, _, st2 = run_gpu(m, x, parts)
+    assert "ingest" in st2.launch_names(parts[-1])
+    assert np.array_equal(ya, yb)
+    assert np.array_equal(ya, yc)
 
 
 @pytest.mark.gpu
@@ -385,11 +405,11 @@ def test_pqmf_fast_form_selected_in_rave_configs(monkeypatch):
         model = configs.build(cfg, seed=cfg)
         x = configs.batch_input(cfg, range(2), model.in_channels, sum(parts), seed=3)
         y_fast, _, st = run_gpu(model, x, parts)
-        assert any(n.endswith("[pqmf]") for n in st.launch_names(parts[0]))
+        assert any("[pqmf" in n for n in st.launch_names(parts[0]))
         monkeypatch.setenv("SC_DISABLE_PQMF", "1")
         y_gen, _, st2 = run_gpu(model, x, parts)
         monkeypatch.delenv("SC_DISABLE_PQMF")
-        assert not any(n.endswith("[pqmf]") for n in st2.launch_names(parts[0]))
+        assert not any("[pqmf" in n for n in st2.launch_names(parts[0]))
         err, rms = rel_err(y_fast, y_gen)
         assert err <= 2 * FP32_TOL, (cfg, err, rms)
 
