@@ -24,12 +24,26 @@ def launches(path):
     return list(by.values())
 
 
+def kernel_token(launch_name):
+    """The ncu kernel-name substring of a launch name's kernel (step boundaries)."""
+    if launch_name == "ingest":
+        return "ingest"
+    if launch_name == "egress":
+        return "egress"
+    if "pqmf-analysis" in launch_name:
+        return "pqmf_analysis"
+    if "pqmf-synthesis" in launch_name:
+        return "pqmf_synthesis"
+    return "conv"
+
+
 def main():
     seq = launches(sys.argv[1])
     # a capture window that starts mid-step: rotate so it starts at an ingest (the launches of
     # one step are the same every step, so the tail + head form one complete step)
     names0 = [n for n in json.loads(open(sys.argv[2]).read())["profile_ms"] if n != "carry"]
-    first = next((i for i, k in enumerate(seq) if "ingest" in k["name"]), 0)
+    t0, t1 = kernel_token(names0[0]), kernel_token(names0[-1])
+    first = next((i for i, k in enumerate(seq) if t0 in k["name"]), 0)
     if first > 0 and len(seq) - first < len(names0):
         need = len(names0) - (len(seq) - first)
         seq = seq[first:] + seq[first - need:first]
@@ -39,11 +53,11 @@ def main():
     acc = collections.defaultdict(list)
     i = 0
     while i < len(seq):
-        if "ingest" not in seq[i]["name"]:
+        if t0 not in seq[i]["name"]:
             i += 1
             continue
         step = seq[i:i + len(names)]
-        if len(step) < len(names) or "egress" not in step[-1]["name"]:
+        if len(step) < len(names) or t1 not in step[-1]["name"]:
             break
         for n, k in zip(names, step):
             acc[n].append(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"])
