@@ -1,0 +1,3 @@
+export SC_LIB_PATH=exp/libstreamconv_b200.so SC_SKIP_BUILD=1
+SC_TC_DEBUG=128 SC_TC_TRACE_OP=29 python tools/trace_tc.py 5 fp32 > gpurun_out/trace_d.txt 2>&1
+SC_TC_DEBUG=192 SC_TC_TRACE_OP=29 python tools/trace_tc.py 5 fp32 > gpurun_out/trace_e.txt 2>&1

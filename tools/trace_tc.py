@@ -29,7 +29,7 @@ lib().sc_debug_tc_trace(buf)
 a = np.array(buf, dtype=np.int64).reshape(16, 256)
 t0 = a[0, 0]
 print("(units: kilo-cycles of CTA 0 SM clock)")
-names = ["tma_issue", "full(xf start)", "xform done", "mma start", "empty/xf comp", "tfull(drain)", "drain end", "mma issued", "xf aempty ok", "xf st done"]
+names = ["tma_issue", "full(xf start)", "xform done", "mma start", "empty/xf comp", "tfull(drain)", "drain end", "mma issued", "q3 ready", "q0 ready", "q1 ready", "q2 ready"]
 print("g   " + " ".join(f"{n:>14s}" for n in names))
 st_, en_, sm_ = a[7, :148], a[8, :148], a[9, :148]
 t00 = st_.min()
@@ -42,4 +42,4 @@ for k in range(6):
     e = a[6, 4 * k:4 * k + 4]
     print(k, [round((v - t0) / 1000, 2) for v in e])
 for g in range(0, 40):
-    print(f"{g:3d} " + " ".join(f"{(a[k, g] - t0) / 1000:14.2f}" if a[k, g] else f"{'-':>14s}" for k in (0, 1, 2, 3, 4, 5, 10, 11, 12, 13)))
+    print(f"{g:3d} " + " ".join(f"{(a[k, g] - t0) / 1000:14.2f}" if a[k, g] else f"{'-':>14s}" for k in (0, 1, 2, 3, 4, 5, 10, 11, 12, 13, 14, 15)))
