@@ -43,7 +43,7 @@ namespace scb {
 
 namespace {
 
-__device__ long long g_tc_trace[16 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
+__device__ long long g_tc_trace[32 * 256];  // SC_TC_DEBUG & 32: per-K-block timestamps of CTA 0
 
 __device__ __forceinline__ long long clk() { return clock64(); }  // SM cycles (per-SM counter)
 
@@ -108,17 +108,19 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {  // a - b
   return r;
 }
 
-// 3xFP16 split of a (scaled) pair: hi = t rounded to 11 significant bits in the fp32 domain
-// (integer round-half-away on the magnitude: two ALU ops, no conversion), lo = t - hi (exact),
-// both packed to fp16 pairs.  Two conversions per pair: the conversion pipe bounded the
-// transform when hi was also unpacked back to fp32 (ncu: XU at 126% of peak).  (A Veltkamp
-// split, c t - (c t - t), is folded to t by ptxas.)  hi is exact in fp16 down to 2^-14; below
-// that (< 2^-28 of the row max after scaling) the fp16 rounding of hi adds at most 2^-25
+// 3xFP16 split of a (scaled) pair: hi = t truncated to 11 significant bits in the fp32 domain
+// (one mask per element, no conversion), lo = t - hi (exact, same sign as t, < one unit of
+// hi's last place), both packed to fp16 pairs: hi exact, lo rounded to 11 bits — hi + lo carries
+// >= 22 significant bits of t, as tf32 hi + lo does.  Two conversions per pair: the conversion
+// pipe bounded the transform when hi was also unpacked back to fp32 (ncu: XU at 126% of peak).
+// (A Veltkamp split, c t - (c t - t), is folded to t by ptxas; rounding hi to nearest costs one
+// more integer add per element and buys one bit in lo.)  hi is exact in fp16 down to 2^-14;
+// below that (< 2^-28 of the row max after scaling) the fp16 rounding of hi adds at most 2^-25
 // absolute — negligible, and a fixed function of the row like the scale.
 __device__ __forceinline__ void split_f16x2(float2 t, uint32_t& h, uint32_t& l) {
   float2 hi;
-  hi.x = __uint_as_float((__float_as_uint(t.x) + 0x1000u) & 0xFFFFE000u);
-  hi.y = __uint_as_float((__float_as_uint(t.y) + 0x1000u) & 0xFFFFE000u);
+  hi.x = __uint_as_float(__float_as_uint(t.x) & 0xFFFFE000u);
+  hi.y = __uint_as_float(__float_as_uint(t.y) & 0xFFFFE000u);
   const float2 lo = fsub2(t, hi);
   const __half2 h2 = __floats2half2_rn(hi.x, hi.y);
   const __half2 l2 = __floats2half2_rn(lo.x, lo.y);
@@ -148,6 +150,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Waits off the critical path back off with nanosleep between polls: a failed try_wait returns
+// within ~20 cycles, so a spinning warp takes one issue slot in ten from the transform / drain
+// warps of its SM sub-partition (ncu source counters: 17% of all executed instructions were
+// wait loops).  ns = 0 keeps the plain spin.
+#ifndef SC_SLEEP_IO
+#define SC_SLEEP_IO 128    // epilogue I/O lane: once per tile
+#endif
+#ifndef SC_SLEEP_PROD
+#define SC_SLEEP_PROD 64   // TMA producers waiting for a free ring slot
+#endif
+#ifndef SC_SLEEP_DRAIN
+#define SC_SLEEP_DRAIN 32  // drain warps waiting for a chunk (two more chunk buffers of slack)
+#endif
+#ifndef SC_SLEEP_XF
+#define SC_SLEEP_XF 32     // transform warps waiting for input rows to land
+#endif
+template <uint32_t NS> __device__ __forceinline__ void mbar_wait_bo(uint64_t* bar, uint32_t parity) {
+  if constexpr (NS == 0) {
+    mbar_wait(bar, parity);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE_%=;\n\t"
+        "nanosleep.u32 %2;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(NS)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
@@ -550,6 +585,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
   static_assert(4 * STAGES + 46 <= 128, "barrier area");
   static_assert(!CH || (BN == 128 && CK == (BF ? 4 : 1) && (BF || !WIN)), "chained conv: BN = 128 (windows: bf16)");
   static_assert(TS >= 2, "TMEM A ring needs two slots");
+  static_assert(!X2 || 4 * A_TILE <= L::AST * L::WIN_SLOT, "four per-slab A units fit the unit ring");
   constexpr int OTHER = WIN ? 0 : BF ? 16 * TS : HF ? 32 * TS : 64 * TS;
   // CH: two chunk accumulators + the A ring + the chained GEMM's A slots — fp32: two slots of
   // 64 columns (32 channels hi | lo); bf16: four of 16 (32 channels as bf16 pairs, one per slab)
@@ -586,10 +622,10 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
     mbar_init(stg_written, 8);
     mbar_init(stg_free, 1);
     for (int a = 0; a < STAGES; ++a) mbar_init(&aempty[a], 1);
-    for (int a = 0; a < (L::AST > 0 ? L::AST : 1); ++a) {
+    for (int a = 0; a < (X2 ? 4 : L::AST > 0 ? L::AST : 1); ++a) {
       mbar_init(&wa_full[a], 1);
       mbar_init(&wa_ready[a], 4);
-      mbar_init(&wa_empty[a], X2 ? 8 : 1);  // X2: released by all eight transform warps
+      mbar_init(&wa_empty[a], X2 ? (p.awin ? 8 : 4) : 1);  // X2: released by the transform warps that read the unit
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -759,7 +795,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
               for (int k = 0; k < BN / 32; ++k) tma_prefetch_3d(&tmap_res, p.res_off + tn.n0 + 32 * k, tn.i0, tn.s0);
             }
           }
-          mbar_wait(stg_written, tcount & 1);
+          mbar_wait_bo<SC_SLEEP_IO>(stg_written, tcount & 1);
           const int oc0 = p.gate ? tc.n0 / 2 : tc.n0;
           for (int k = 0; k < (out_cols + 31) / 32; ++k)
             tma_store_3d(&tmap_out, reinterpret_cast<uint8_t*>(stg) + k * (BM * 32 * (OBF ? 2 : 4)), oc0 + 32 * k,
@@ -804,7 +840,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
           const bool first = (kb / CK) == 0 || kb == (one2 ? nkt - 1 : nk);  // + the chained conv's first chunk
           const int boff = (CH && kb >= nk) ? BN : 0;     // its bias sits at sbias[BN, 2 BN)
           const int b = HF ? cb_ : c % NB;
-          mbar_wait(&tfull[b], HF ? cph : (c / NB) & 1);
+          mbar_wait_bo<SC_SLEEP_DRAIN>(&tfull[b], HF ? cph : (c / NB) & 1);
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && c < 256 && warp == EP0 && lane == 0) g_tc_trace[5 * 256 + c] = clk();
           tc_fence_after();
           float f = 1.f;  // HF: this (row, K-slab)'s exact unscale 2^-(s + s_w)
@@ -942,6 +978,20 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
             w.y = *reinterpret_cast<uint32_t*>(&b2);
             *dst = w;
           }
+        } else if (!OBF && p.post_act == ACT_ID && (!p.res || p.res_act == ACT_ID)) {
+          // no activation on either operand (the residual units' convs): out = acc (+ skip),
+          // packed fp32x2 adds
+          const bool has_res = p.res != nullptr;
+  #pragma unroll
+          for (int u = 0; u < COLS; u += 4) {
+            float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
+            if (has_res) {
+              const float4 rv = *dst;
+              fadd2_acc(acc[u], acc[u + 1], rv.x, rv.y);
+              fadd2_acc(acc[u + 2], acc[u + 3], rv.z, rv.w);
+            }
+            *dst = make_float4(acc[u], acc[u + 1], acc[u + 2], acc[u + 3]);
+          }
         } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
           // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
           const float ps = slope_of(p.post_act, p.post_alpha);
@@ -1009,7 +1059,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
         const TileCoord tc = tile_coord(p, tile, n_tiles_n, BN);
         for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
           const int sa = u % L::AST;
-          if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
+          if (u >= L::AST) mbar_wait_bo<SC_SLEEP_PROD>(&wa_empty[sa], ((u / L::AST) + 1) & 1);
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && lane == 0) g_tc_trace[0 * 256 + u] = clk();
           mbar_expect_tx_w(&wa_full[sa], a_bytes);
           tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK, p.a_row0 + tc.i0, tc.s0);
@@ -1023,7 +1073,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
           if (p.wres) continue;
           for (int q = 0; q < taps; ++q, ++g) {
             const int s = g % STAGES;
-            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+            if (g >= STAGES) mbar_wait_bo<SC_SLEEP_PROD>(&empty[s], ((g / STAGES) + 1) & 1);
             const int kw = (q * p.cblocks + cb) * BK;
             mbar_expect_tx_w(&full[s], (BF ? 1 : 2) * L::B_TILE);
             tma_load_3d_w(&tmap_w, &full[s], b_hi(s), kw, tc.n0, 0);
@@ -1032,7 +1082,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
         }
         for (int k2 = 0; k2 < NK2; ++k2, ++g) {  // chained conv's weight slabs (bf16)
           const int s = g % STAGES;
-          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          if (g >= STAGES) mbar_wait_bo<SC_SLEEP_PROD>(&empty[s], ((g / STAGES) + 1) & 1);
           mbar_expect_tx_w(&full[s], L::B_TILE);
           tma_load_3d_w(&tmap_w, &full[s], b_hi(s), (nk + k2) * BK, tc.n0, 0);
         }
@@ -1154,7 +1204,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
         for (int cb = 0; cb < p.cblocks; ++cb, ++u) {
           if (RX && (u & 1) != xset) continue;
           const int sa = u % L::AST;
-          mbar_wait(&wa_full[sa], (u / L::AST) & 1);
+          mbar_wait_bo<SC_SLEEP_XF>(&wa_full[sa], (u / L::AST) & 1);
           if ((TC_DBG(p) & 32) && blockIdx.x == 0 && u < 256 && t == 0) g_tc_trace[1 * 256 + u] = clk();
           if (BF) {
             // raw fp32 rows (SW128, 16B chunk j at j ^ (w & 7)) -> pre-activation -> bf16 copy
@@ -1239,13 +1289,11 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
             uint8_t* rsw = rsc + (u % RS_WIN) * L::WROWS;
             const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
             const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
-            const float scf = (!pre_tanh && pre_s > 1.f) ? pre_s : 1.f;  // scale rule: see the non-window HF
             {
               float m = 0.f;
   #pragma unroll
               for (int j = 0; j < 8; ++j)
                 m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
-              m *= scf;
               int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
               sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
               const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
@@ -1259,8 +1307,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
                   t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
                 } else {
                   const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                  t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                    : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+                  t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
                 }
                 split_f16x2(t2, hv[k], lv[k]);
               }
@@ -1278,7 +1325,6 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
               m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
               m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
               m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-              m *= scf;
               int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
               sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
               const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
@@ -1292,8 +1338,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
                   t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
                 } else {
                   const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                  t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                    : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
+                  t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
                 }
                 split_f16x2(t2, hv[k], lv[k]);
               }
@@ -1363,7 +1408,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
           int cb = 0, q = 0;
           for (int kb = 0; kb < nk; ++kb, ++g) {
             const int s = g % STAGES;
-            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+            if (g >= STAGES) mbar_wait_bo<SC_SLEEP_PROD>(&empty[s], ((g / STAGES) + 1) & 1);
             if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0) g_tc_trace[0 * 256 + g] = clk();
             const int kw = (q * p.cblocks + cb) * BK;
             mbar_expect_tx_w(&full[s], 2 * L::B_TILE);
@@ -1393,10 +1438,14 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
           int cb = 0, q = 0;
           for (int kb = 0; kb < nk; ++kb) {
             if (!p.awin || q == 0) {
-              const int sa = u % L::AST;
-              if (u >= L::AST) mbar_wait(&wa_empty[sa], ((u / L::AST) + 1) & 1);
+              // awin: three window slots in turn (every transform warp reads every unit);
+              // per-slab units: four 16 KB slots, two private to each transform set (slabs
+              // alternate between the sets, and a set only watches its own units' barriers)
+              const int sa = p.awin ? u % L::AST : ((u & 1) << 1) | ((u >> 1) & 1);
+              const int use = p.awin ? u / L::AST : u >> 2;
+              if (use > 0) mbar_wait_bo<SC_SLEEP_PROD>(&wa_empty[sa], (use + 1) & 1);
               mbar_expect_tx_w(&wa_full[sa], abytes);
-              tma_load_3d_w(&tmap_a, &wa_full[sa], win_hi(sa), p.a_c0 + cb * BK,
+              tma_load_3d_w(&tmap_a, &wa_full[sa], p.awin ? win_hi(sa) : wins + sa * A_TILE, p.a_c0 + cb * BK,
                             p.a_row0 + tc.i0 + (p.awin ? 0 : q * p.a_tap_rows), tc.s0);
               ++u;
             }
@@ -1418,11 +1467,11 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
       // into the scaling (LeakyReLU(x) 2^s = max(x 2^s, x (a 2^s)) exactly: 2^s is a power of
       // two), fp16 hi | lo pairs (low half = even k) into this slab's TMEM A slot; the unscale
       // exponent of (row, slab) goes to the ring the drain reads.  The scale is taken from
-      // max |x| x max(1, a) (>= max |act(x)|; tanh: <= |x|) — the same rule as the window
+      // max |x| (>= max |act(x)|: LeakyReLU slopes are <= 1 here, plan time; tanh: <= |x|) — the same rule as the window
       // transform, so both modes produce identical operands.  Tile row r = (stream r / R, frame
       // r % R); its input row sits at r in a per-slab unit, or at (r / R)(R + halo) + r % R + q
-      // tap_rows in a block window (p.awin).  Every transform warp releases a unit after its last
-      // slab (having seen it land: a release can then never run ahead into the slot's previous use).
+      // tap_rows in a block window (p.awin).  A transform warp releases a unit after its own last
+      // read of it (having seen it land: a release can never run ahead into the slot's previous use).
       const int xset = (warp - Roles<X2>::XF0) >> 2;
       const int quarter = warp & 3;
       const int r = quarter * 32 + lane;
@@ -1433,79 +1482,93 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
       const float pre_s = slope_of(p.pre_act, p.pre_alpha);
       const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
       const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
-      int g = 0, u = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        int q = 0;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int sa = u % L::AST;
-          const bool unit_last = !p.awin || q == taps - 1;
-          if ((g & 1) == xset) {
-            const int s = g % STAGES;
-            const int ga = g;
-            mbar_wait(&wa_full[sa], (u / L::AST) & 1);
-            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3) g_tc_trace[1 * 256 + g] = clk();
-            const int wr = srow + (p.awin ? q * p.a_tap_rows : 0);
-            const float4* row = reinterpret_cast<const float4*>(win_hi(sa)) + wr * 8;
-            float x[32];
-            float m = 0.f;
+      // Each set walks only its own slabs (g = xset, xset + 2, ...; g counts across tiles).  The
+      // tail of a slab — TMEM store completion, fence, arrive — is deferred into the next own
+      // slab, after that slab's loads have been issued, and the A-slot wait is taken there too
+      // (it has long completed): both latencies overlap the shared-memory loads instead of
+      // idling the warp (per-quarter traces: ~300 of ~1950 cycles per slab pair).  A warp
+      // releases a unit right after its own last read of it (awin: both sets read every unit, 8
+      // arrivals; per-slab units: the handling set's 4).
+      int g = xset, kb = xset, tile = blockIdx.x, tcount = 0;
+      while (tile < n_tiles && kb >= nk) kb -= nk, tile += gridDim.x, ++tcount;
+      int cb = p.awin ? kb / taps : 0, q = p.awin ? kb % taps : 0;
+      int prev_s = -1;
+      const uint32_t tq = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL;
+      while (tile < n_tiles) {
+        const int u = p.awin ? tcount * p.cblocks + cb : g;
+        const bool last_read = !p.awin || q + 2 >= taps;
+        const int sa = p.awin ? u % L::AST : ((u & 1) << 1) | ((u >> 1) & 1);  // see the A-unit producer
+        mbar_wait_bo<SC_SLEEP_XF>(&wa_full[sa], (p.awin ? u / L::AST : u >> 2) & 1);
+        const bool trq = (TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0;  // rows 16 + 4 quarter ..
+        if (trq) g_tc_trace[(16 + 4 * quarter) * 256 + g] = clk();
+        const int wr = srow + (p.awin ? q * p.a_tap_rows : 0);
+        const float4* row = reinterpret_cast<const float4*>(p.awin ? win_hi(sa) : wins + sa * A_TILE) + wr * 8;
+        float4 v[8];
   #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 v = row[j ^ (wr & 7)];
-              x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-              m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-            }
-            // this warp's reads of the unit are done once m (a function of every loaded value)
-            // exists: release the slot only then — an arrive right after the LDS instructions
-            // could let the next TMA fill overwrite rows still in flight to the registers
-            if (unit_last) {
-              m = __shfl_sync(0xffffffffu, m, lane);  // consume m before the arrive
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&wa_empty[sa]);
-            }
-            if (!pre_tanh && pre_s > 1.f) m *= pre_s;
-            int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
-            sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
-            const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
-            const float scn = sc * pre_s;  // exact
-            uint32_t hv[16], lv[16];
-  #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              float2 t2;
-              if (pre_tanh) {
-                t2 = fmul2s(tanh_ool(x[2 * k]), tanh_ool(x[2 * k + 1]), sc);
-              } else {
-                const float2 p2 = fmul2s(x[2 * k], x[2 * k + 1], sc), n2 = fmul2s(x[2 * k], x[2 * k + 1], scn);
-                t2 = pre_s <= 1.f ? make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y))
-                                  : make_float2(fminf(p2.x, n2.x), fminf(p2.y, n2.y));
-              }
-              split_f16x2(t2, hv[k], lv[k]);
-            }
-            rsc[(ga % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);
-            const bool trc = (TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3;
-            if (trc) g_tc_trace[4 * 256 + g] = clk();
-            const int a_sl = ga % TS;
-            if (ga >= TS) mbar_wait(&aempty[a_sl], ((ga / TS) + 1) & 1);  // MMAs of ga - TS done
-            if (trc) g_tc_trace[12 * 256 + g] = clk();
-            tc_fence_after();
-            const uint32_t ta = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + A_COL + 32 * a_sl;
-            tmem_st16(ta, hv);
-            tmem_st16(ta + 16, lv);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            if (trc) g_tc_trace[13 * 256 + g] = clk();
-            tc_fence_before();
-            // no proxy fence: nothing was written to shared memory for the async proxy (the A
-            // slot is TMEM; the unit is only read), and the scale byte is read by the drain
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&xform[s]);
-            if ((TC_DBG(p) & 32) && blockIdx.x == 0 && g < 256 && lane == 0 && quarter == 3) g_tc_trace[2 * 256 + g] = clk();
-          } else if (unit_last) {  // the other set's slab ends the unit: release it once it landed
-            mbar_wait(&wa_full[sa], (u / L::AST) & 1);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wa_empty[sa]);
-          }
-          if (unit_last) ++u;
-          if (++q == taps) q = 0;
+        for (int j = 0; j < 8; ++j) v[j] = row[j ^ (wr & 7)];
+        // while the loads are in flight: this slab's A slot (MMAs of g - TS done), then the
+        // previous own slab's deferred tail
+        if (g >= TS) mbar_wait(&aempty[g % TS], ((g / TS) + 1) & 1);
+        if (prev_s >= 0) {
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xform[prev_s]);
         }
+        tc_fence_after();
+        float m = 0.f;
+  #pragma unroll
+        for (int j = 0; j < 8; ++j)
+          m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+        // this warp's reads of the unit are done once m (a function of every loaded value)
+        // exists: release the slot only then — an arrive right after the LDS instructions
+        // could let the next TMA fill overwrite rows still in flight to the registers
+        if (last_read) {
+          m = __shfl_sync(0xffffffffu, m, lane);  // consume m before the arrive
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wa_empty[sa]);
+        }
+        int sx = 14 - (static_cast<int>(__float_as_uint(m) >> 23) - 127);
+        sx = sx < s_lo ? s_lo : sx > s_hi ? s_hi : sx;
+        const float sc = __uint_as_float(static_cast<uint32_t>(127 + sx) << 23);
+        const float scn = sc * pre_s;  // exact
+        uint32_t hv[16], lv[16];
+  #pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
+          float2 t2;
+          if (pre_tanh) {
+            t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
+          } else {
+            const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+            t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
+          }
+          split_f16x2(t2, hv[k], lv[k]);
+        }
+        rsc[(g % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);
+        if (trq) g_tc_trace[(17 + 4 * quarter) * 256 + g] = clk();
+        const uint32_t ta = tq + 32 * (g % TS);
+        tmem_st16(ta, hv);
+        tmem_st16(ta + 16, lv);
+        // no proxy fence: nothing was written to shared memory for the async proxy (the A
+        // slot is TMEM; the unit is only read), and the scale byte is read by the drain
+        prev_s = g % STAGES;
+        if (trq) g_tc_trace[(18 + 4 * quarter) * 256 + g] = clk();
+        g += 2, kb += 2;
+        if (p.awin) {
+          q += 2;
+          if (q >= taps) q -= taps, ++cb;
+        }
+        if (kb >= nk) {
+          do kb -= nk, tile += gridDim.x, ++tcount; while (kb >= nk);
+          if (p.awin) cb = kb / taps, q = kb - cb * taps;
+        }
+      }
+      if (prev_s >= 0) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xform[prev_s]);
       }
       }
     } else {
@@ -1529,7 +1592,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
         int cb = 0, q = 0;  // this slab's 32-channel block and tap (advanced below, no divisions)
         for (int kb = 0; kb < nkt; ++kb, ++g) {
           const int s = g % STAGES;
-          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) + 1) & 1);
+          if (g >= STAGES) mbar_wait_bo<SC_SLEEP_PROD>(&empty[s], ((g / STAGES) + 1) & 1);
           if (CH && kb >= nk) {  // chained conv's weight slab only (its A comes from the drain)
             if (BF) {
               mbar_expect_tx_w(&full[s], L::B_TILE);
@@ -1778,7 +1841,7 @@ void launch_bf16(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUten
 
 }  // namespace
 
-void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 16 * 256); }
+void tc_trace_dump(long long* host) { cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(long long) * 32 * 256); }
 
 void launch_conv_tc(const CUtensorMap& map_a, const CUtensorMap& map_w, const CUtensorMap& map_out,
                     const CUtensorMap& map_res, const TcParams& p, cudaStream_t st) {

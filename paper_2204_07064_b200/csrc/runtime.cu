@@ -338,7 +338,11 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
         if (probe[i].chain >= 0) chained[i] = chained[static_cast<size_t>(probe[i].chain)] = 1;
     }
     for (size_t i = 0; i < nops; ++i)
-      if (plan->dops[i].kernel == KERNEL_TC && !chained[i]) {
+      // (a LeakyReLU slope > 1 on the input stays on 3xTF32: the 3xFP16 transform applies the
+      // pre-activation as max(x, a x), which is LeakyReLU only for a <= 1,
+      // and scales rows by max |x| >= max |act(x)|)
+      if (plan->dops[i].kernel == KERNEL_TC && !chained[i] &&
+          !(plan->prog.ops[i].pre_act == ACT_LRELU && std::fabs(plan->prog.ops[i].pre_alpha) > 1.f)) {
         plan->dops[i] = DevOp{};
         plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i], true);
       }

@@ -23,10 +23,10 @@ y = torch.empty(S, cout, F * num // den, device="cuda")
 # run ops up to `op` only: run full step; trace holds the last TC launch -> use op index via env
 st.process_buffer(x, y, F)
 torch.cuda.synchronize()
-buf = (C.c_longlong * (16 * 256))()
+buf = (C.c_longlong * (32 * 256))()
 lib().sc_debug_tc_trace.argtypes = [C.POINTER(C.c_longlong)]
 lib().sc_debug_tc_trace(buf)
-a = np.array(buf, dtype=np.int64).reshape(16, 256)
+a = np.array(buf, dtype=np.int64).reshape(32, 256)
 t0 = a[0, 0]
 print("(units: kilo-cycles of CTA 0 SM clock)")
 names = ["tma_issue", "full(xf start)", "xform done", "mma start", "empty/xf comp", "tfull(drain)", "drain end", "mma issued", "q3 ready", "q0 ready", "q1 ready", "q2 ready"]
@@ -43,3 +43,8 @@ for k in range(6):
     print(k, [round((v - t0) / 1000, 2) for v in e])
 for g in range(0, 40):
     print(f"{g:3d} " + " ".join(f"{(a[k, g] - t0) / 1000:14.2f}" if a[k, g] else f"{'-':>14s}" for k in (0, 1, 2, 3, 4, 5, 10, 11, 12, 13, 14, 15)))
+
+print("X2 transform per lane quarter: [landed, math done, A slot free, arrived] (kilo-cycles)")
+for g in range(16, 40):
+    print(f"{g:3d} " + "  ".join("[" + " ".join(f"{(a[16 + 4 * qq + k, g] - t0) / 1000:6.2f}" if a[16 + 4 * qq + k, g] else "   -  " for k in range(4)) + "]" for qq in range(4)),
+          f" mma {(a[3, g] - t0) / 1000:6.2f}")
