@@ -981,16 +981,28 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
         } else if (!OBF && p.post_act == ACT_ID && (!p.res || p.res_act == ACT_ID)) {
           // no activation on either operand (the residual units' convs): out = acc (+ skip),
           // packed fp32x2 adds
+          // (skip rows read four vectors at a time ahead of their adds: one exposed
+          // shared-memory latency per batch instead of one per vector)
           const bool has_res = p.res != nullptr;
+          constexpr int EB = COLS >= 16 ? 16 : COLS;
   #pragma unroll
-          for (int u = 0; u < COLS; u += 4) {
-            float4* dst = reinterpret_cast<float4*>(stg + stg_off(r, col0 + u));
+          for (int u0 = 0; u0 < COLS; u0 += EB) {
+            float4 rv[EB / 4];
             if (has_res) {
-              const float4 rv = *dst;
-              fadd2_acc(acc[u], acc[u + 1], rv.x, rv.y);
-              fadd2_acc(acc[u + 2], acc[u + 3], rv.z, rv.w);
+  #pragma unroll
+              for (int k = 0; k < EB / 4; ++k) rv[k] = *reinterpret_cast<const float4*>(stg + stg_off(r, col0 + u0 + 4 * k));
+  #pragma unroll
+              for (int k = 0; k < EB / 4; ++k) {
+                const int u = u0 + 4 * k;
+                fadd2_acc(acc[u], acc[u + 1], rv[k].x, rv[k].y);
+                fadd2_acc(acc[u + 2], acc[u + 3], rv[k].z, rv[k].w);
+              }
             }
-            *dst = make_float4(acc[u], acc[u + 1], acc[u + 2], acc[u + 3]);
+  #pragma unroll
+            for (int k = 0; k < EB / 4; ++k) {
+              const int u = u0 + 4 * k;
+              *reinterpret_cast<float4*>(stg + stg_off(r, col0 + u)) = make_float4(acc[u], acc[u + 1], acc[u + 2], acc[u + 3]);
+            }
           }
         } else if (p.post_act != ACT_TANH && p.res_act != ACT_TANH) {
           // LeakyReLU(v) = max(v, a v) for a <= 1 (min for a > 1): 2 instructions
