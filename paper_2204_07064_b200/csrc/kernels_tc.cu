@@ -108,21 +108,30 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {  // a - b
   return r;
 }
 
-// 3xFP16 split of a (scaled) pair: hi = t truncated to 11 significant bits in the fp32 domain
-// (one mask per element, no conversion), lo = t - hi (exact, same sign as t, < one unit of
-// hi's last place), both packed to fp16 pairs: hi exact, lo rounded to 11 bits — hi + lo carries
-// >= 22 significant bits of t, as tf32 hi + lo does.  Two conversions per pair: the conversion
-// pipe bounded the transform when hi was also unpacked back to fp32 (ncu: XU at 126% of peak).
-// (A Veltkamp split, c t - (c t - t), is folded to t by ptxas; rounding hi to nearest costs one
-// more integer add per element and buys one bit in lo.)  hi is exact in fp16 down to 2^-14;
-// below that (< 2^-28 of the row max after scaling) the fp16 rounding of hi adds at most 2^-25
-// absolute — negligible, and a fixed function of the row like the scale.
+// 3xFP16 split of a (scaled) pair: hi = fp16_rn(t) (one packed conversion), lo = fp16_rn(t -
+// float(hi)) — t - hi is exact in fp32, so hi + lo carries >= 22 significant bits of t, as tf32
+// hi + lo does.  The unpack of hi runs as HADD2.F32 on the FMA-class pipe: per pair two ALU-pipe
+// conversions and three FMA-pipe operations.  (Forms tried before: an integer round or mask of
+// the fp32 bits for hi — two more ALU-pipe operations per pair, and the ALU pipe, which issues a
+// warp instruction every other cycle, is the transform's busiest unit (ncu: "math pipe throttle"
+// on a quarter of its samples); cvt.f32.f16 for the unpack — the conversion unit at 126% of peak;
+// a Veltkamp split, c t - (c t - t) — folded to t by ptxas.)  SC_SPLIT_MASK=1 builds the mask form.
+// hi is exact in fp16 down to 2^-14; below that (< 2^-28 of the row max after scaling) it rounds
+// to fp16 subnormals and lo picks up the remainder — a fixed function of the row like the scale.
+#ifndef SC_SPLIT_MASK
+#define SC_SPLIT_MASK 0
+#endif
 __device__ __forceinline__ void split_f16x2(float2 t, uint32_t& h, uint32_t& l) {
+#if SC_SPLIT_MASK
   float2 hi;
   hi.x = __uint_as_float(__float_as_uint(t.x) & 0xFFFFE000u);
   hi.y = __uint_as_float(__float_as_uint(t.y) & 0xFFFFE000u);
-  const float2 lo = fsub2(t, hi);
   const __half2 h2 = __floats2half2_rn(hi.x, hi.y);
+#else
+  const __half2 h2 = __floats2half2_rn(t.x, t.y);
+  const float2 hi = __half22float2(h2);
+#endif
+  const float2 lo = fsub2(t, hi);
   const __half2 l2 = __floats2half2_rn(lo.x, lo.y);
   h = *reinterpret_cast<const uint32_t*>(&h2);
   l = *reinterpret_cast<const uint32_t*>(&l2);
