@@ -358,6 +358,32 @@ __device__ __forceinline__ void mma_f16x3_slab_w(uint32_t d, uint32_t ahi, uint3
       : "memory");
 }
 
+// The same six MMAs with both operands in shared memory (window tiles: A = fp16 hi / lo window
+// planes at a tap's row offset): descriptors of the first K = 16 step; the second step's start 32
+// bytes (2 descriptor address units) further.  One elected lane, one asm block: issuing the six
+// MMAs one call at a time cost ~120 uniform-datapath instructions per K-slab in the issuing warp
+// (descriptor rebuilds, an elect per MMA) — more than the 192 cycles the N = 64 MMAs take.
+__device__ __forceinline__ void mma_f16x3_slab_ss_w(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                    uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t.reg .b64 ah1, al1, bh1, bl1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.u64 ah1, %1, 2;\n\t"
+      "add.u64 al1, %2, 2;\n\t"
+      "add.u64 bh1, %3, 2;\n\t"
+      "add.u64 bl1, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], al1, bh1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah1, bl1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah1, bh1, %5, t;\n\t}" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -1123,6 +1149,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
           mbar_wait(&wa_ready[sa], (u / L::AST) & 1);
           tc_fence_after();
           const uint32_t wh = smem_u32(win_hi(sa)), wl = smem_u32(win_lo(sa));
+          const uint64_t wdesc_h = sw64_desc(wh);  // 3xFP16: this window's fp16 hi plane
           for (int q = 0; q < taps; ++q, ++g) {
             const int kb = cb * taps + q;
             const int s = g % STAGES;
@@ -1146,19 +1173,13 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
             } else if (HF) {  // fp16 hi / lo window planes (SW64 rows of 64 B), tap q at a row offset
               const uint32_t idesc_h = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
                                        (static_cast<uint32_t>(BM >> 4) << 24);  // F32 += F16 x F16
-              const uint32_t offh = static_cast<uint32_t>(q * p.a_tap_rows * BK * 2);
+              // descriptors by addition: the window's hi plane + the tap's row offset (64 B rows:
+              // 4 address units per row); lo plane / W lo tile at fixed distances
               const int ws = p.wres ? kb : s;
-              const uint32_t ah = smem_u32(win_hi(sa)) + offh, al = smem_u32(win_lo16(sa)) + offh;
-              const uint32_t bh = smem_u32(b_hi(ws)), bl = smem_u32(b_lo(ws));
-  #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t acc0 = (!chunk_first || kk > 0) ? 1u : 0u;
-                mma_bf16_w(dmain, sw64_desc(al + kk * 32), sw64_desc(bh + kk * 32), idesc_h, acc0);
-                mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bl + kk * 32), idesc_h, 1u);
-              }
-  #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)
-                mma_bf16_w(dmain, sw64_desc(ah + kk * 32), sw64_desc(bh + kk * 32), idesc_h, 1u);
+              const uint64_t ah = wdesc_h + static_cast<uint64_t>(q * p.a_tap_rows * 4);
+              const uint64_t bh = sw64_desc(smem_u32(b_hi(ws)));
+              mma_f16x3_slab_ss_w(dmain, ah, ah + (L::WROWS * BK * 2) / 16, bh, bh + L::B_TILE / 16, idesc_h,
+                                  chunk_first ? 0u : 1u);
             } else {
               const uint32_t off = static_cast<uint32_t>(q * p.a_tap_rows * BK * 4);
               const int ws = p.wres ? kb : s;
