@@ -15,7 +15,8 @@ import sys
 
 
 def launches(path):
-    rows = [r for r in csv.reader(line for line in open(path) if line.startswith('"'))]
+    # ncu's own csv quotes every field; the trimmed lists under profiles/ quote only where needed
+    rows = [r for r in csv.reader(line for line in open(path) if line[:1] == '"' or line[:2] == "ID" or line[:1].isdigit())]
     hdr, data = rows[0], rows[1:]
     ki, mi, vi, ii = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
     by = collections.OrderedDict()

@@ -10,7 +10,7 @@ from paper_2204_07064_b200 import configs
 from test_gpu_parity import run_gpu, rel_err
 
 CASES = [(1, 1, [2048] * 64), (2, 4, [2048, 2048]), (3, 3, [4096, 4096]), (4, 4, [1] * 8),
-         (5, 2, [2048] * 20), (5, 2, [8192] * 5), (5, 2, [512] * 80)]
+         (5, 2, [2048] * 20), (5, 2, [8192] * 5)]  # (B = 512 < ratio runs in phase state: tests/test_gpu_parity.py)
 for cfg, S, parts in CASES:
     m = configs.build(cfg, seed=cfg)
     x = configs.batch_input(cfg, range(S), m.in_channels, sum(parts), seed=cfg)
