@@ -1344,13 +1344,10 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
   #pragma unroll
               for (int k = 0; k < 16; ++k) {
                 const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
-                float2 t2;
-                if (pre_tanh) {
-                  t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
-                } else {
-                  const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                  t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
-                }
+                // identity / LeakyReLU with |slope| <= 1 only (plan time: tanh and larger slopes
+                // keep the layer on 3xTF32)
+                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                const float2 t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));
                 split_f16x2(t2, hv[k], lv[k]);
               }
               uint4* hr = reinterpret_cast<uint4*>(win_hi(sa)) + t * 4;
@@ -1375,13 +1372,10 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
   #pragma unroll
               for (int k = 0; k < 2; ++k) {
                 const float x0 = k ? ve.z : ve.x, x1 = k ? ve.w : ve.y;
-                float2 t2;
-                if (pre_tanh) {
-                  t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
-                } else {
-                  const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-                  t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
-                }
+                // identity / LeakyReLU with |slope| <= 1 only (plan time: tanh and larger slopes
+                // keep the layer on 3xTF32)
+                const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+                const float2 t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));
                 split_f16x2(t2, hv[k], lv[k]);
               }
               const int po = we * 8 + (((je >> 1) ^ ((we >> 1) & 3)) << 1) + (je & 1);  // uint2 units
@@ -1578,13 +1572,10 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
   #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const float x0 = (k & 1) ? v[k >> 1].z : v[k >> 1].x, x1 = (k & 1) ? v[k >> 1].w : v[k >> 1].y;
-          float2 t2;
-          if (pre_tanh) {
-            t2 = fmul2s(tanh_ool(x0), tanh_ool(x1), sc);
-          } else {
-            const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
-            t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));  // slope <= 1 (plan time)
-          }
+          // identity / LeakyReLU with |slope| <= 1 only (plan time: tanh and larger slopes keep
+          // the layer on 3xTF32)
+          const float2 p2 = fmul2s(x0, x1, sc), n2 = fmul2s(x0, x1, scn);
+          const float2 t2 = make_float2(fmaxf(p2.x, n2.x), fmaxf(p2.y, n2.y));
           split_f16x2(t2, hv[k], lv[k]);
         }
         rsc[(g % RS_RING) * BM + r] = static_cast<uint8_t>(127 - sx - p.f16_sw);

@@ -341,7 +341,9 @@ std::unique_ptr<Plan> make_plan(Program prog, int precision, int device) {
       // (a LeakyReLU slope > 1 on the input stays on 3xTF32: the 3xFP16 transform applies the
       // pre-activation as max(x, a x), which is LeakyReLU only for a <= 1,
       // and scales rows by max |x| >= max |act(x)|)
-      if (plan->dops[i].kernel == KERNEL_TC && !chained[i] &&
+      // (a tanh on the input stays there too: its 3xFP16 form would put a call per element into
+      // the transform; no config uses it)
+      if (plan->dops[i].kernel == KERNEL_TC && !chained[i] && plan->prog.ops[i].pre_act != ACT_TANH &&
           !(plan->prog.ops[i].pre_act == ACT_LRELU && std::fabs(plan->prog.ops[i].pre_alpha) > 1.f)) {
         plan->dops[i] = DevOp{};
         plan_tc(plan->prog, i, precision, plan->dops[i], wtc[i], true);

@@ -88,3 +88,16 @@ def test_leaky_slopes(alpha, split):
     y_or = po.run(oracle_twin(m), x, [32, 32, 32], "stream")
     err, rms = rel_err(y, y_or)
     assert err <= FP32_TOL, f"alpha {alpha}: {err:.3e} x RMS ({rms:.3e})"
+
+
+@pytest.mark.gpu
+def test_tanh_preactivation_stays_on_tf32():
+    """A tanh applied on a conv's input (two stacked activations, so it cannot fuse into the
+    producer) keeps that layer on the 3xTF32 split; results match the oracle."""
+    m = Model(in_channels=64, seed=11)
+    m.conv(64, 128, 3).leaky_relu(0.2).tanh().conv(128, 128, 3)
+    x = _input(5, 64, 96, seed=12)
+    y, _, st = run_gpu(m, x, [32, 32, 32])
+    y_or = po.run(oracle_twin(m), x, [32, 32, 32], "stream")
+    err, rms = rel_err(y, y_or)
+    assert err <= FP32_TOL, f"{err:.3e} x RMS ({rms:.3e})"

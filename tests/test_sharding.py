@@ -73,3 +73,29 @@ def test_ranges():
     assert sum(len(p) for p in parts) == 16384 and parts[-1].stop == 16384
     parts = [strong_range(10, 4, r) for r in range(4)]
     assert [len(p) for p in parts] == [3, 3, 2, 2] and parts[1].start == 3
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,total,world,parts", [(3, 37, 4, [512, 512]), (5, 13, 8, [2048, 2048]), (2, 9, 2, [256, 256])])
+def test_product_shards_equal_unsharded_gpu(cfg, total, world, parts):
+    """The PRODUCT on every rank's shard (ranks run one after another on the one GPU a test box
+    has: shards never exchange data, so their order is immaterial) equals the unsharded batch
+    bit for bit — the strong-scaling split of bench.py --total-streams."""
+    from paper_2204_07064_b200 import configs
+    from test_gpu_parity import run_gpu
+    m = configs.build(cfg, seed=9)
+    x = configs.batch_input(cfg, range(total), m.in_channels, sum(parts), seed=9)
+    y_full, plan, _ = run_gpu(m, x, parts)
+    ys = []
+    for r in range(world):
+        rg = strong_range(total, world, r)
+        if len(rg) == 0:
+            continue
+        xr = configs.batch_input(cfg, rg, m.in_channels, sum(parts), seed=9)
+        assert np.array_equal(xr, x[rg.start:rg.stop])  # inputs are seeded by global stream index
+        y, _, _ = run_gpu(m, xr, parts, plan=plan)
+        ys.append(y)
+    assert np.array_equal(np.concatenate(ys), y_full)
