@@ -1080,6 +1080,11 @@ struct DagLowerer {
 }  // namespace
 
 namespace {
+bool densify4_disabled() {
+  const char* e = std::getenv("SC_DENSIFY4");
+  return e && std::atoi(e) == 0;  // SC_DENSIFY4=0: at most 2 output frames per row
+}
+
 bool densify_disabled() {
   const char* e = std::getenv("SC_DENSIFY");
   return e && std::atoi(e) == 0;  // SC_DENSIFY=0: keep narrow convs in their plain form
@@ -1087,8 +1092,8 @@ bool densify_disabled() {
 
 // Narrow stride-1 convs on the tensor cores waste most of a tile: N <= 64 columns (the MMA
 // issue cost is per instruction, not per column) or a channel count padded to 32.  A
-// densified op reads the input as 2-frame super-rows (the strided convs' view) and emits both
-// output frames of a row at once: y[2i + phi] = b + sum_k w[k] x[2i + phi - P + k] becomes one
+// densified op reads the input as 2-frame (4-frame for N <= 32) super-rows (the strided convs'
+// view) and emits all output frames of a row at once, e.g. for two: y[2i + phi] = b + sum_k w[k] x[2i + phi - P + k] becomes one
 // GEMM row with N' = 2N columns (phase-major) over the window's super-rows; MACs are unchanged
 // for the padded-channel case and grow by (K + 1) / K otherwise.  Ops with a residual epilogue
 // keep their form (their skip must stay in lockstep under phase state).
@@ -1103,36 +1108,41 @@ void densify(Program& p) {
         op.phases != 1 || op.d != 1)
       continue;
     const bool narrow = op.nout <= 64 || (S0 * op.cin % 32 != 0 && (2 * S0 * op.cin) % 32 == 0);
-    // every non-phase call delivers a multiple of 2 S0 frames to this op
-    const bool even = (p.ratio * op.in_rate.num) % op.in_rate.den == 0 &&
-                      (p.ratio * op.in_rate.num / op.in_rate.den) % (2 * S0) == 0;
-    if (!narrow || !even) continue;
-    const int64_t extra = (2 * S0 - op.look % (2 * S0)) % (2 * S0);  // window on a super-row boundary
-    const int T0 = op.taps, N = op.nout, T1 = T0 + S0 + static_cast<int>(extra);
-    std::vector<float> w(static_cast<size_t>(T1) * op.cin * 2 * N, 0.f);
+    // D output frames per row: 2, or 4 for the narrowest layers (N <= 32, e.g. the gated head:
+    // N' = 4N fills a 128-column tile and a quarter fewer K-slabs cross the transform per frame)
+    // when every non-phase call delivers a multiple of D S0 frames to this op
+    auto even = [&](int D) {
+      return (p.ratio * op.in_rate.num) % op.in_rate.den == 0 &&
+             (p.ratio * op.in_rate.num / op.in_rate.den) % (D * S0) == 0;
+    };
+    if (!narrow || !even(2)) continue;
+    const int D = (op.nout <= 32 && S0 == 1 && even(4) && !densify4_disabled()) ? 4 : 2;
+    const int64_t extra = (D * S0 - op.look % (D * S0)) % (D * S0);  // window on a super-row boundary
+    const int T0 = op.taps, N = op.nout, T1 = T0 + (D - 1) * S0 + static_cast<int>(extra);
+    std::vector<float> w(static_cast<size_t>(T1) * op.cin * D * N, 0.f);
     for (int q = 0; q < T1; ++q)
-      for (int ph = 0; ph < 2; ++ph) {
+      for (int ph = 0; ph < D; ++ph) {
         const int k = q - ph * S0 - static_cast<int>(extra);
         if (k < 0 || k >= T0) continue;
         for (int c = 0; c < op.cin; ++c)
           for (int n = 0; n < N; ++n)
-            w[(static_cast<size_t>(q) * op.cin + c) * 2 * N + ph * N + n] =
+            w[(static_cast<size_t>(q) * op.cin + c) * D * N + ph * N + n] =
                 op.w[(static_cast<size_t>(k) * op.cin + c) * N + n];
       }
     op.w.swap(w);
-    std::vector<float> b(op.bias);
-    b.insert(b.end(), op.bias.begin(), op.bias.end());
+    std::vector<float> b;
+    for (int ph = 0; ph < D; ++ph) b.insert(b.end(), op.bias.begin(), op.bias.end());
     op.bias.swap(b);
     op.look += extra;
     op.taps = T1;
-    op.S = 2 * S0;
-    op.row_step = 2 * S0;
-    op.phases = 2;
-    op.nout = 2 * N;
-    op.out_rstride *= 2;
+    op.S = D * S0;
+    op.row_step = D * S0;
+    op.phases = D;
+    op.nout = D * N;
+    op.out_rstride *= D;
     p.bufs[op.in_buf].cache = std::max(p.bufs[op.in_buf].cache, op.look);
-    p.bufs[op.in_buf].align = Lowerer::lcm(p.bufs[op.in_buf].align, 2 * S0);
-    op.name += " x2";
+    p.bufs[op.in_buf].align = Lowerer::lcm(p.bufs[op.in_buf].align, D * S0);
+    op.name += D == 4 ? " x4" : " x2";
   }
 }
 }  // namespace
