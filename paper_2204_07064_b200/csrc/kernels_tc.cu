@@ -430,10 +430,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// tanh / sigmoid are kept out of line: inlining them into the fully unrolled transform and
-// epilogue loops bloats the kernel past the instruction cache (measured: 4-16 us epilogues).
+// tanh is kept out of line: inlining it into the fully unrolled transform and epilogue loops
+// bloats the kernel past the instruction cache (measured: 4-16 us epilogues).
 __device__ __noinline__ float tanh_ool(float v) { return tanhf(v); }
-__device__ __noinline__ float gate_ool(float a, float g) { return tanhf(a) * (1.0f / (1.0f + expf(-g))); }
 // The gated head's tanh(a) sigmoid(g) from two hardware exponentials and two approximate
 // reciprocals: tanh(a) = (e^2a - 1) / (e^2a + 1) with a clamped to +-15 (tanh(15) = 1 - 2e-13)
 // — and, below |a| = 0.1 where e^2a - 1 cancels, the odd series a - a^3/3 + 2a^5/15 - 17a^7/315
@@ -906,8 +905,7 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
             f = __uint_as_float(eb << 23);
             if (++cb_ == NB) cb_ = 0, cph ^= 1;
           }
-  #pragma unroll
-          // main chunk, 32 columns per wait (16 for X2: its 96-register budget)
+          // main chunk, 32 columns per TMEM load (16 for the narrowest tiles)
           constexpr int LDC = COLS >= 32 ? 32 : 16;
   #pragma unroll
           for (int cc = 0; cc < COLS; cc += LDC) {
@@ -1530,7 +1528,6 @@ __global__ void __launch_bounds__(Roles<HF>::NT, 1)
       const int taps = nk / p.cblocks;
       // rows past G x R (a partial tile) are never stored: read any in-slot row for them
       const int srow = (!p.awin || r >= p.G * p.R) ? (r < p.G * p.R ? r : 0) : (r / p.R) * (p.R + p.halo) + r % p.R;
-      const bool pre_tanh = p.pre_act == ACT_TANH;
       const float pre_s = slope_of(p.pre_act, p.pre_alpha);
       const int s_lo = -126 > -127 - p.f16_sw ? -126 : -127 - p.f16_sw;
       const int s_hi = 127 < 126 - p.f16_sw ? 127 : 126 - p.f16_sw;
