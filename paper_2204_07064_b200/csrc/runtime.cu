@@ -780,14 +780,18 @@ CallPlan& State::call_plan(int64_t F) {
       p.tiles_per_stream = 1;
       p.m_tiles = (streams + p.G - 1) / p.G;
     }
-    // few output tiles (deep layers at small stream counts, e.g. 1 frame x 2048 streams): halve
-    // the N tile until the grid covers the SMs.  The K order does not depend on BN, so results
+    // few output tiles (deep layers at small stream counts, e.g. 1 frame x 128 streams): halve
+    // the N tile towards a grid that covers the SMs.  The K order does not depend on BN, so results
     // are bit-identical to the full-width tile (buffer-partition / stream-count invariance).
     if (!c.gate && plan->dops[i].chain < 0 && !small_bn_disabled()) {
       int sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
-      while (p.BN > 32 && static_cast<int64_t>(p.m_tiles) * ((c.nout + p.BN - 1) / p.BN) < sms &&
-             c.nout % (p.BN / 2) == 0)
+      // ... but only while the narrower tiles still fit one wave: the per-slab cost of these tiles
+      // is mostly the transform of the input rows, which does not shrink with BN, so a second wave
+      // of narrow tiles costs more than the idle SMs it fills (cfg5 at 2048 streams: 1.81 -> 1.70
+      // ms per step; at 128 streams narrowing still gains 10-25%)
+      while (p.BN > 32 && c.nout % (p.BN / 2) == 0 &&
+             static_cast<int64_t>(p.m_tiles) * ((c.nout + p.BN / 2 - 1) / (p.BN / 2)) <= sms)
         p.BN /= 2;
     }
     if (p.BN != d.BN) {  // this call's weight boxes: BN rows
