@@ -162,3 +162,27 @@ def test_cpp_cached_module_api_host():
     exe = B.build_cpp_tests()
     r = subprocess.run([str(exe), "host"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0 and "OK host" in r.stdout, r.stdout + r.stderr
+
+
+def test_densify_plan_time(monkeypatch):
+    """Narrow stride-1 convs are lowered to super-row GEMMs at plan time (graph.cpp densify): two
+    output frames per row, four for N <= 32 (the gated head); the algorithmic MAC count
+    (SPEC's literal count, kernels.cpp:96-99 per output) does not change."""
+    from paper_2204_07064_b200 import configs
+    from paper_2204_07064_b200.runtime import Plan
+    for cfg in (4, 5):
+        p = Plan(configs.build(cfg), device=-1)
+        ops = [l for l in p.describe().split("\n") if " gate" in l]
+        assert len(ops) == 1 and " x4 " in ops[0] and "nout=128" in ops[0] and "taps=12" in ops[0], ops
+        macs = p.macs_per_sample
+        monkeypatch.setenv("SC_DENSIFY4", "0")
+        p2 = Plan(configs.build(cfg), device=-1)
+        ops2 = [l for l in p2.describe().split("\n") if " gate" in l]
+        assert " x2 " in ops2[0] and "nout=64" in ops2[0], ops2
+        assert p2.macs_per_sample == macs
+        monkeypatch.setenv("SC_DENSIFY", "0")
+        p3 = Plan(configs.build(cfg), device=-1)
+        assert " x2 " not in p3.describe() and " x4 " not in p3.describe()
+        assert p3.macs_per_sample == macs
+        monkeypatch.delenv("SC_DENSIFY")
+        monkeypatch.delenv("SC_DENSIFY4")
