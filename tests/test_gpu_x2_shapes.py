@@ -42,6 +42,8 @@ SHAPES = [
     ("k3d5_c128_awin", lambda: _res_unit(128, 3, 5), 9, [64, 64], [16] * 8),
     ("k3d5_c512_units_partial", lambda: _res_unit(512, 3, 5), 130, [2, 2, 2, 2], [4, 4]),
     ("k3d3_c96_odd_slabs", lambda: _res_unit(96, 3, 3), 21, [8] * 6, [24, 24]),
+    ("k3d1_c32_one_block_window", lambda: _res_unit(32, 3, 1), 20, [16] * 4, [32, 32]),
+    ("k5_c32_64_one_block", lambda: _conv(32, 64, 5), 45, [8] * 4, [16, 16]),
     ("k1_c256_128", lambda: _conv(256, 128, 1), 40, [8, 8, 8], [24]),
     ("k1_c96_64_odd", lambda: _conv(96, 64, 1), 70, [4] * 6, [12, 12]),
     ("k1_c32_one_slab", lambda: _conv(32, 32, 1), 33, [16, 16], [8] * 4),
